@@ -1,0 +1,217 @@
+"""ctypes binding of the CPU oracle (oracle/pf_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` leg.  The product package
+(paper_2604_24994_b200) never imports this module, and this module never
+imports the product package.  See pf_oracle.c's header for what each entry
+point computes and which passage of PAPER.md / SPEC.md / SURVEY.md it follows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pf_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+O1, O2, O3 = 1, 2, 3
+T_STOP = 1e-4
+
+
+class OCamera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("c2w", C.c_float * 12), ("near_plane", C.c_float)]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain C, OpenMP, no FMA contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+               "-fPIC", "-shared", "-Wall", "-o", tmp, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB_PATH)
+        P = C.c_void_p
+        i64 = C.c_int64
+        L.oracle_bin_cells.argtypes = [i64, P, P, P, P, P, P, P]
+        L.oracle_emit_sort.argtypes = [i64, P, P, P, C.c_int32, P, P]
+        L.oracle_emit_sort.restype = i64
+        L.oracle_tile_ranges.argtypes = [i64, P, C.c_int32, P]
+        L.oracle_render.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, i64, P, P, P, P,
+                                    P, P, C.c_int]
+        L.oracle_backward.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, i64, P, P,
+                                      P, P, P, P, P, C.c_int]
+        L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, i64, P, P,
+                                           C.c_double, P, P]
+        L.oracle_pixel_ray.argtypes = [P, C.c_int32, C.c_int32, P, P, P]
+        L.oracle_composite.argtypes = [i64, P, P, P, P, P]
+        L.oracle_composite.restype = i64
+        L.oracle_num_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def make_camera(cam) -> OCamera:
+    oc = OCamera()
+    oc.width, oc.height = int(cam.width), int(cam.height)
+    oc.fx, oc.fy, oc.cx, oc.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    for k, v in enumerate(np.asarray(cam.c2w, np.float32).reshape(12)):
+        oc.c2w[k] = float(v)
+    oc.near_plane = cam.near
+    return oc
+
+
+class _SceneArrays:
+    def __init__(self, sc):
+        self.N = sc.num_cells
+        self.sites = _c(sc.sites, np.float32)
+        self.weights = _c(sc.weights, np.float32)
+        self.radii = _c(sc.radii, np.float32)
+        self.density = _c(sc.density, np.float32)
+        self.rgb = _c(sc.rgb, np.float32)
+        self.off = _c(sc.nbr_offsets, np.int64)
+        self.idx = _c(sc.nbr_indices, np.int32)
+        if self.idx.size == 0:
+            self.idx = np.zeros(1, np.int32)
+        self.bg = np.asarray(sc.background, np.float32)
+
+    def args(self):
+        return [self.N, _p(self.sites), _p(self.weights), _p(self.radii), _p(self.density),
+                _p(self.rgb), _p(self.off), _p(self.idx), _p(self.bg)]
+
+
+# ---------------------------------------------------------------------------
+# binning specification (fp32)
+# ---------------------------------------------------------------------------
+
+def bin_cells(sc, cam):
+    """-> rect i32[N,4] (tx0,ty0,tx1,ty1), count i32[N], keybits u32[N]."""
+    A = _SceneArrays(sc)
+    rect = np.zeros((A.N, 4), np.int32)
+    count = np.zeros(A.N, np.int32)
+    kb = np.zeros(A.N, np.uint32)
+    oc = make_camera(cam)
+    lib().oracle_bin_cells(A.N, _p(A.sites), _p(A.weights), _p(A.radii), C.byref(oc),
+                           _p(rect), _p(count), _p(kb))
+    return rect, count, kb
+
+
+def binning(sc, cam):
+    """Full binning spec: dict(rect, count, keybits, keys u64[P], vals u32[P], ranges u32[T,2])."""
+    rect, count, kb = bin_cells(sc, cam)
+    tiles_x = (cam.width + 15) // 16
+    tiles_y = (cam.height + 15) // 16
+    L = lib()
+    P = L.oracle_emit_sort(sc.num_cells, _p(rect), _p(count), _p(kb), tiles_x, None, None)
+    keys = np.zeros(max(P, 1), np.uint64)
+    vals = np.zeros(max(P, 1), np.uint32)
+    L.oracle_emit_sort(sc.num_cells, _p(rect), _p(count), _p(kb), tiles_x, _p(keys), _p(vals))
+    ranges = np.zeros((tiles_x * tiles_y, 2), np.uint32)
+    L.oracle_tile_ranges(P, _p(keys), tiles_x * tiles_y, _p(ranges))
+    return dict(rect=rect, count=count, keybits=kb, keys=keys[:P], vals=vals[:P],
+                ranges=ranges, P=int(P), tiles_x=tiles_x, tiles_y=tiles_y)
+
+
+# ---------------------------------------------------------------------------
+# render / backward
+# ---------------------------------------------------------------------------
+
+def render(sc, cam, mode=O3, pixels=None, counters=False, signature=False, nthreads=0):
+    """Render (double).  pixels: None (full image) or int array [n,2] of (x,y).
+    Returns dict(out f64[n,4] or [H,W,4], counters i64[n,4], sig u64[n], nseg, viol)."""
+    A = _SceneArrays(sc)
+    oc = make_camera(cam)
+    if pixels is None:
+        n = cam.width * cam.height
+        pix = None
+    else:
+        pix = _c(np.asarray(pixels).reshape(-1, 2), np.int32)
+        n = pix.shape[0]
+    out = np.zeros((n, 4), np.float64)
+    cnt = np.zeros((n, 4), np.int64) if counters else None
+    sig = np.zeros(n, np.uint64) if signature else None
+    nseg = np.zeros(n, np.int64)
+    viol = np.zeros(1, np.int64)
+    lib().oracle_render(mode, *A.args(), C.byref(oc), n, _p(pix), _p(out), _p(cnt), _p(sig),
+                        _p(nseg), _p(viol), nthreads)
+    if pixels is None:
+        out = out.reshape(cam.height, cam.width, 4)
+    return dict(out=out, counters=cnt, sig=sig, nseg=nseg, viol=int(viol[0]))
+
+
+def backward(sc, cam, grad_out, mode=O3, pixels=None, nthreads=0):
+    """Gradients of L = sum <grad_out, out>.  grad_out f32[H,W,4] (pixels=None) or [n,4].
+    Returns dict(sites f64[N,3], weights, radii, density f64[N], rgb f64[N,3])."""
+    A = _SceneArrays(sc)
+    oc = make_camera(cam)
+    if pixels is None:
+        n = cam.width * cam.height
+        pix = None
+    else:
+        pix = _c(np.asarray(pixels).reshape(-1, 2), np.int32)
+        n = pix.shape[0]
+    g = _c(np.asarray(grad_out).reshape(n, 4), np.float32)
+    N = A.N
+    gs = np.zeros((N, 3)); gw = np.zeros(N); gr = np.zeros(N); gsig = np.zeros(N)
+    grgb = np.zeros((N, 3))
+    lib().oracle_backward(mode, *A.args(), C.byref(oc), n, _p(pix), _p(g), _p(gs), _p(gw),
+                          _p(gr), _p(gsig), _p(grgb), nthreads)
+    return dict(sites=gs, weights=gw, radii=gr, density=gsig, rgb=grgb)
+
+
+def cell_interval(sc, i, Q, d, t_near=0.0, mode=O2):
+    """(hit, t_in, t_out, kinds[kin,kout,jin,jout]) of cell i on the ray Q + t d."""
+    A = _SceneArrays(sc)
+    Qa = _c(Q, np.float64)
+    da = _c(d, np.float64)
+    res = np.zeros(2)
+    kinds = np.zeros(4, np.int32)
+    hit = lib().oracle_cell_interval(mode, A.N, _p(A.sites), _p(A.weights), _p(A.radii),
+                                     _p(A.off), _p(A.idx), int(i), _p(Qa), _p(da),
+                                     float(t_near), _p(res), _p(kinds))
+    return bool(hit), float(res[0]), float(res[1]), kinds
+
+
+def pixel_ray(cam, x, y):
+    oc = make_camera(cam)
+    Q = np.zeros(3); d = np.zeros(3); tn = np.zeros(1)
+    lib().oracle_pixel_ray(C.byref(oc), int(x), int(y), _p(Q), _p(d), _p(tn))
+    return Q, d, float(tn[0])
+
+
+def composite(sigma, dt, rgb, bg=(0.0, 0.0, 0.0)):
+    sigma = _c(sigma, np.float64); dt = _c(dt, np.float64)
+    rgb = _c(np.asarray(rgb).reshape(-1, 3), np.float64)
+    bga = _c(bg, np.float64)
+    out = np.zeros(4)
+    K = lib().oracle_composite(len(sigma), _p(sigma), _p(dt), _p(rgb), _p(bga), _p(out))
+    return out, int(K)
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())

@@ -1,0 +1,775 @@
+/*
+ * pf_oracle.c -- plain, slow, obviously-correct CPU oracle for the Power Foam
+ * rasterizer hot path (arXiv 2604.24994).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, constant or helper with the CUDA path
+ * (paper_2604_24994_b200/csrc); the two meet only through the arrays of
+ * pf_synth (the seeded generators).
+ *
+ * What it computes (citations: P:<line> = /root/reference/PAPER.md,
+ * S:<line> = SPEC.md, SURVEY §x = /root/repo/SURVEY.md):
+ *
+ *  (1) The rendered image, by the plain definition.  For the
+ *      pixel ray x(t) = Q + t d, t >= t_near, and every cell i:
+ *        I_i = { t : |x(t)-p_i|^2 <= r_i^2                  (bounding sphere B_i,
+ *                                                            P:189 "radius of a
+ *                                                            bounding sphere")
+ *                    pow(x(t),i) <= pow(x(t),j)  for all j  (power cell, P:570-573
+ *                                                            Eq. power_cell)
+ *                    t >= t_near }                          (near plane, C10)
+ *      with pow(x,i) = |x-p_i|^2 - w_i  (P:565 Eq. pow_dist).  Every constraint
+ *      is written straight from that definition: the sphere is a quadratic in
+ *      t, and pow(x(t),i) - pow(x(t),j) = [pow(Q,i)-pow(Q,j)]
+ *      + 2 t d.(p_j - p_i) is linear in t (the radical plane, P:577-585 with the
+ *      sign of the weight term corrected).
+ *      Non-empty intervals are sorted by entry t (ties by cell index) -- the
+ *      order comes from the geometry, NOT from the sort key -- and composited
+ *      front to back in double ("evaluated exactly as a sum over the
+ *      segments"; alpha = 1-exp(-sigma dt); stop after the segment
+ *      that makes T < 1e-4; out = (C + T bg, T), C5).
+ *
+ *      Candidate sets (which j enter the "for all j", which i are tried):
+ *        O1: every cell is a candidate and every other cell is a plane
+ *            (the literal definition);
+ *        O2: every cell is a candidate; planes only from i's neighbour list
+ *            (exact for Čech lists with w = r^2: P:230-235, SURVEY Lemma L1);
+ *        O3: candidates are the cells of the pixel's tile list produced by the
+ *            fp32 binning below (the paper's rasterisation algorithm, P:213,
+ *            "global sort by depths ... similar to 3DGS"); planes from lists.
+ *      O1 == O2 == O3 on shared pixels is itself a test.
+ *
+ *  (2) The backward pass: the exact derivative of (1) for a fixed active set
+ *      and termination index, L = sum_pixels <grad_out, out> (
+ *      endpoint derivatives of the sphere and the radical plane).
+ *
+ *  (3) The binning specification: per-cell
+ *      screen rectangle of the bounding sphere, tile rectangle, count and the
+ *      order-preserving bits of the sort key K_i = pow(Q, p_i) (P:596-603,
+ *      Theorem 2), then the (tile<<32 | keybits, cell) pairs sorted stably and
+ *      per-tile ranges.  This part is an fp32 *specification* (it defines
+ *      integers, so it is evaluated in single precision, one IEEE op at a time,
+ *      left to right, no FMA: compile with -ffp-contract=off).
+ *
+ * Pins: tests/test_oracle_*.py check every function here against values the
+ * paper / SPEC print, closed forms, invariants, brute force and finite
+ * differences.
+ */
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#if !defined(FLT_EVAL_METHOD) || FLT_EVAL_METHOD != 0
+#error "the fp32 binning specification needs FLT_EVAL_METHOD == 0 (SSE float)"
+#endif
+
+typedef struct {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float c2w[12]; /* row-major [R | Q]: R[m][k] = c2w[4m+k], Q[m] = c2w[4m+3] */
+    float near_plane;
+} oc_camera;
+
+typedef struct {
+    int64_t N;
+    const float *sites, *weights, *radii, *density, *rgb;
+    const int64_t *nbr_off;
+    const int32_t *nbr_idx;
+    double bg[3];
+} oc_scene;
+
+#define O1_ALL_PAIRS 1
+#define O2_LIST_PLANES 2
+#define O3_TILE_LISTS 3
+
+#define T_STOP 1e-4
+
+/* ======================================================================== */
+/* (3) fp32 binning specification                                           */
+/* ======================================================================== */
+
+static uint32_t key_bits(float K)
+{
+    /* order-preserving map float -> u32 */
+    uint32_t u;
+    memcpy(&u, &K, 4);
+    return (u >> 31) ? ~u : (u ^ 0x80000000u);
+}
+
+/* screen-space extent of the sphere along one image axis.
+ * a = camera-space coordinate along the axis (x or y), z = depth. */
+static void axis_extent(float a, float z, float r, float f, float c, float near_plane,
+                        int in_front, float *lo, float *hi)
+{
+    float ulo, uhi;
+    if (in_front) {
+        /* tangent planes through the camera centre containing the other axis */
+        float q = sqrtf((a * a + z * z) - r * r);
+        float den = (z - r) * (z + r);
+        ulo = (a * z - r * q) / den;
+        uhi = (a * z + r * q) / den;
+    } else {
+        /* sphere straddles the near plane: box [a-r,a+r] x [near, z+r] */
+        float amin = a - r, amax = a + r;
+        ulo = amin / (amin >= 0.0f ? z + r : near_plane);
+        uhi = amax / (amax >= 0.0f ? near_plane : z + r);
+    }
+    *lo = f * ulo + c;
+    *hi = f * uhi + c;
+}
+
+static float clampf_(float v, float lo, float hi)
+{
+    return fminf(fmaxf(v, lo), hi);
+}
+
+/* rect[4*i] = (tx0, ty0, tx1, ty1) half-open tile rectangle; count = area. */
+int oracle_bin_cells(int64_t N, const float *sites, const float *weights, const float *radii,
+                     const oc_camera *cam, int32_t *rect, int32_t *count, uint32_t *keybits)
+{
+    const int tiles_x = (cam->width + 15) / 16, tiles_y = (cam->height + 15) / 16;
+    const float *M = cam->c2w;
+    const float Q0 = M[3], Q1 = M[7], Q2 = M[11];
+    for (int64_t i = 0; i < N; ++i) {
+        float v0 = sites[3 * i + 0] - Q0;
+        float v1 = sites[3 * i + 1] - Q1;
+        float v2 = sites[3 * i + 2] - Q2;
+        /* camera coordinates c = R^T v, c_k = (R0k v0 + R1k v1) + R2k v2 */
+        float cxx = (M[0] * v0 + M[4] * v1) + M[8] * v2;
+        float cyy = (M[1] * v0 + M[5] * v1) + M[9] * v2;
+        float czz = (M[2] * v0 + M[6] * v1) + M[10] * v2;
+        /* sort key: power distance of the camera centre */
+        float K = ((v0 * v0 + v1 * v1) + v2 * v2) - weights[i];
+        float r = radii[i];
+        keybits[i] = key_bits(K);
+        rect[4 * i + 0] = rect[4 * i + 1] = rect[4 * i + 2] = rect[4 * i + 3] = 0;
+        count[i] = 0;
+        if (!(czz + r > cam->near_plane) || !(r > 0.0f))
+            continue; /* entirely behind the near plane (or degenerate) */
+        int in_front = (czz - r > cam->near_plane);
+        float xlo, xhi, ylo, yhi;
+        axis_extent(cxx, czz, r, cam->fx, cam->cx, cam->near_plane, in_front, &xlo, &xhi);
+        axis_extent(cyy, czz, r, cam->fy, cam->cy, cam->near_plane, in_front, &ylo, &yhi);
+        /* 1-pixel guard, 16-pixel tiles, clamp in float before the int conversion */
+        float fx0 = clampf_(floorf((xlo - 1.0f) * 0.0625f), 0.0f, (float)tiles_x);
+        float fx1 = clampf_(floorf((xhi + 1.0f) * 0.0625f) + 1.0f, 0.0f, (float)tiles_x);
+        float fy0 = clampf_(floorf((ylo - 1.0f) * 0.0625f), 0.0f, (float)tiles_y);
+        float fy1 = clampf_(floorf((yhi + 1.0f) * 0.0625f) + 1.0f, 0.0f, (float)tiles_y);
+        int tx0 = (int)fx0, tx1 = (int)fx1, ty0 = (int)fy0, ty1 = (int)fy1;
+        if (tx1 > tx0 && ty1 > ty0) {
+            rect[4 * i + 0] = tx0;
+            rect[4 * i + 1] = ty0;
+            rect[4 * i + 2] = tx1;
+            rect[4 * i + 3] = ty1;
+            count[i] = (tx1 - tx0) * (ty1 - ty0);
+        }
+    }
+    return 0;
+}
+
+typedef struct {
+    uint64_t key;
+    uint32_t val;
+} oc_pair;
+
+static int cmp_pair(const void *a, const void *b)
+{
+    const oc_pair *x = (const oc_pair *)a, *y = (const oc_pair *)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    /* stable w.r.t. cell-major emission: equal keys keep cell order (C12) */
+    if (x->val != y->val) return x->val < y->val ? -1 : 1;
+    return 0;
+}
+
+/* Emits (tile<<32 | keybits, cell) in cell-major order and sorts stably.
+ * Returns P (number of pairs); keys/vals may be NULL to query P. */
+int64_t oracle_emit_sort(int64_t N, const int32_t *rect, const int32_t *count,
+                         const uint32_t *keybits, int32_t tiles_x, uint64_t *keys, uint32_t *vals)
+{
+    int64_t P = 0;
+    for (int64_t i = 0; i < N; ++i) P += count[i];
+    if (!keys || !vals) return P;
+    oc_pair *pairs = (oc_pair *)malloc(sizeof(oc_pair) * (size_t)(P > 0 ? P : 1));
+    int64_t k = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        if (count[i] == 0) continue;
+        for (int ty = rect[4 * i + 1]; ty < rect[4 * i + 3]; ++ty)
+            for (int tx = rect[4 * i + 0]; tx < rect[4 * i + 2]; ++tx) {
+                uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + (uint64_t)tx;
+                pairs[k].key = (tile << 32) | (uint64_t)keybits[i];
+                pairs[k].val = (uint32_t)i;
+                ++k;
+            }
+    }
+    qsort(pairs, (size_t)P, sizeof(oc_pair), cmp_pair);
+    for (int64_t q = 0; q < P; ++q) {
+        keys[q] = pairs[q].key;
+        vals[q] = pairs[q].val;
+    }
+    free(pairs);
+    return P;
+}
+
+/* ranges[2t], ranges[2t+1] = [start, end) of tile t in the sorted keys; (0,0) if empty */
+int oracle_tile_ranges(int64_t P, const uint64_t *keys, int32_t num_tiles, uint32_t *ranges)
+{
+    memset(ranges, 0, sizeof(uint32_t) * 2 * (size_t)num_tiles);
+    for (int64_t q = 0; q < P; ++q) {
+        uint32_t t = (uint32_t)(keys[q] >> 32);
+        if (q == 0 || (uint32_t)(keys[q - 1] >> 32) != t) ranges[2 * t] = (uint32_t)q;
+        if (q == P - 1 || (uint32_t)(keys[q + 1] >> 32) != t) ranges[2 * t + 1] = (uint32_t)(q + 1);
+    }
+    return 0;
+}
+
+/* ======================================================================== */
+/* (1) rays, intervals, compositing in double                               */
+/* ======================================================================== */
+
+/* ray through the centre of pixel (px, py) = (x+0.5, y+0.5) (C11):
+ * d_cam = ((px-cx)/fx, (py-cy)/fy, 1), d = normalize(R d_cam),
+ * t_near = near * |d_cam| (C10: camera-space z >= near). */
+static void pixel_ray(const oc_camera *cam, double px, double py, double Q[3], double d[3],
+                      double *t_near)
+{
+    const float *M = cam->c2w;
+    double dc[3] = {(px - (double)cam->cx) / (double)cam->fx,
+                    (py - (double)cam->cy) / (double)cam->fy, 1.0};
+    double ndc = sqrt(dc[0] * dc[0] + dc[1] * dc[1] + dc[2] * dc[2]);
+    double n2 = 0.0;
+    for (int m = 0; m < 3; ++m) {
+        d[m] = (double)M[4 * m + 0] * dc[0] + (double)M[4 * m + 1] * dc[1] +
+               (double)M[4 * m + 2] * dc[2];
+        n2 += d[m] * d[m];
+        Q[m] = (double)M[4 * m + 3];
+    }
+    double nd = sqrt(n2);
+    for (int m = 0; m < 3; ++m) d[m] /= nd;
+    *t_near = (double)cam->near_plane * ndc;
+}
+
+/* which constraint bounds an interval end */
+#define END_SPHERE 0
+#define END_NEAR 1
+#define END_PLANE 2
+
+typedef struct {
+    double t_in, t_out;
+    int32_t cell;
+    int32_t kin, kout;   /* END_* */
+    int32_t jin, jout;   /* neighbour cell for END_PLANE */
+    int32_t list_pos;    /* position in the tile list (O3), else -1 */
+} oc_seg;
+
+static double powd(const double x[3], const float *p, float w)
+{
+    double a = x[0] - p[0], b = x[1] - p[1], c = x[2] - p[2];
+    return a * a + b * b + c * c - (double)w;
+}
+
+/* Interval of cell i along the ray.  Returns 1 (and fills *s) if the ray meets
+ * the sphere of i after t_near (a "hit"), 0 otherwise; s->t_out > s->t_in iff
+ * the bounded power cell has a non-empty intersection with the ray.
+ * mode O1: planes against every j != i (index order); O2/O3: against i's list.
+ * *nplanes receives the number of plane evaluations (counter X_p). */
+static int cell_interval(const oc_scene *S, int mode, int64_t i, const double Q[3],
+                         const double d[3], double t_near, oc_seg *s, int64_t *nplanes)
+{
+    const float *p = S->sites + 3 * i;
+    double c[3] = {p[0] - Q[0], p[1] - Q[1], p[2] - Q[2]};
+    /* |Q + t d - p|^2 <= r^2  <=>  (t - tc)^2 <= r^2 - |c - tc d|^2 */
+    double tc = d[0] * c[0] + d[1] * c[1] + d[2] * c[2];
+    double e[3] = {c[0] - tc * d[0], c[1] - tc * d[1], c[2] - tc * d[2]};
+    double r = (double)S->radii[i];
+    double h = r * r - (e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+    if (!(h > 0.0)) return 0;
+    double sq = sqrt(h);
+    if (!(tc + sq > t_near)) return 0;
+    s->cell = (int32_t)i;
+    s->list_pos = -1;
+    s->t_in = tc - sq;
+    s->kin = END_SPHERE;
+    s->jin = -1;
+    s->t_out = tc + sq;
+    s->kout = END_SPHERE;
+    s->jout = -1;
+    if (t_near > s->t_in) {
+        s->t_in = t_near;
+        s->kin = END_NEAR;
+    }
+    double powQi = powd(Q, p, S->weights[i]);
+    int64_t jb, je;
+    if (mode == O1_ALL_PAIRS) {
+        jb = 0;
+        je = S->N;
+    } else {
+        jb = S->nbr_off[i];
+        je = S->nbr_off[i + 1];
+    }
+    int empty = 0;
+    for (int64_t q = jb; q < je; ++q) {
+        int64_t j = (mode == O1_ALL_PAIRS) ? q : (int64_t)S->nbr_idx[q];
+        if (j == i) continue;
+        const float *pj = S->sites + 3 * j;
+        ++*nplanes;
+        /* pow(x(t),i) <= pow(x(t),j)  <=>  A t <= B */
+        double A = 2.0 * (d[0] * ((double)pj[0] - p[0]) + d[1] * ((double)pj[1] - p[1]) +
+                          d[2] * ((double)pj[2] - p[2]));
+        double B = powd(Q, pj, S->weights[j]) - powQi;
+        if (A > 0.0) {
+            double t = B / A;
+            if (t < s->t_out) {
+                s->t_out = t;
+                s->kout = END_PLANE;
+                s->jout = (int32_t)j;
+            }
+        } else if (A < 0.0) {
+            double t = B / A;
+            if (t > s->t_in) {
+                s->t_in = t;
+                s->kin = END_PLANE;
+                s->jin = (int32_t)j;
+            }
+        } else if (B < 0.0) {
+            empty = 1; /* ray parallel to the plane, on j's side (C14) */
+        }
+    }
+    if (empty) s->t_out = s->t_in;
+    return 1;
+}
+
+static int cmp_seg(const void *a, const void *b)
+{
+    const oc_seg *x = (const oc_seg *)a, *y = (const oc_seg *)b;
+    if (x->t_in != y->t_in) return x->t_in < y->t_in ? -1 : 1;
+    return x->cell < y->cell ? -1 : (x->cell > y->cell);
+}
+
+/* per-thread scratch */
+typedef struct {
+    oc_seg *segs;
+    int64_t cap;
+} oc_scratch;
+
+static void scratch_reserve(oc_scratch *s, int64_t n)
+{
+    if (n > s->cap) {
+        free(s->segs);
+        s->cap = n;
+        s->segs = (oc_seg *)malloc(sizeof(oc_seg) * (size_t)n);
+    }
+}
+
+/* binning products needed by O3 */
+typedef struct {
+    int32_t tiles_x, tiles_y;
+    uint32_t *vals;   /* sorted cell ids */
+    uint32_t *ranges; /* [T][2] */
+} oc_bins;
+
+static int build_bins(const oc_scene *S, const oc_camera *cam, oc_bins *B)
+{
+    int64_t N = S->N;
+    B->tiles_x = (cam->width + 15) / 16;
+    B->tiles_y = (cam->height + 15) / 16;
+    int32_t T = B->tiles_x * B->tiles_y;
+    int32_t *rect = (int32_t *)malloc(sizeof(int32_t) * 4 * (size_t)N);
+    int32_t *count = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+    uint32_t *kb = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)N);
+    oracle_bin_cells(N, S->sites, S->weights, S->radii, cam, rect, count, kb);
+    int64_t P = oracle_emit_sort(N, rect, count, kb, B->tiles_x, NULL, NULL);
+    uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(P > 0 ? P : 1));
+    B->vals = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(P > 0 ? P : 1));
+    oracle_emit_sort(N, rect, count, kb, B->tiles_x, keys, B->vals);
+    B->ranges = (uint32_t *)malloc(sizeof(uint32_t) * 2 * (size_t)T);
+    oracle_tile_ranges(P, keys, T, B->ranges);
+    free(rect);
+    free(count);
+    free(kb);
+    free(keys);
+    return 0;
+}
+
+static void free_bins(oc_bins *B)
+{
+    free(B->vals);
+    free(B->ranges);
+}
+
+/* Collects the non-empty segments of one pixel ray, sorted by entry t.
+ * counters (O3 only, list order):
+ *   cnt[0] = X_s list entries examined up to termination,
+ *   cnt[1] = X_h sphere hits among them, cnt[2] = X_p plane evaluations of
+ *   those hits, cnt[3] = X_c composited segments; *viol = number of segment
+ *   pairs whose key (list) order disagrees with entry order (Theorem 2). */
+static int64_t collect_segments(const oc_scene *S, int mode, const oc_bins *B, int x, int y,
+                                const double Q[3], const double d[3], double t_near,
+                                oc_scratch *scr, int64_t *hits_planes, int64_t *viol)
+{
+    int64_t nseg = 0, np = 0;
+    if (mode == O3_TILE_LISTS) {
+        int t = (y / 16) * B->tiles_x + (x / 16);
+        uint32_t b = B->ranges[2 * t], e = B->ranges[2 * t + 1];
+        scratch_reserve(scr, (int64_t)(e - b) + 1);
+        for (uint32_t q = b; q < e; ++q) {
+            oc_seg s;
+            int64_t npc = 0;
+            if (cell_interval(S, mode, B->vals[q], Q, d, t_near, &s, &npc)) {
+                s.list_pos = (int32_t)(q - b);
+                /* record every hit (even empty ones) for the counters */
+                scr->segs[nseg++] = s;
+            }
+            np += npc;
+        }
+    } else {
+        scratch_reserve(scr, S->N + 1);
+        for (int64_t i = 0; i < S->N; ++i) {
+            oc_seg s;
+            if (cell_interval(S, mode, i, Q, d, t_near, &s, &np)) scr->segs[nseg++] = s;
+        }
+    }
+    (void)hits_planes;
+    /* keep non-empty intervals (dt > 0) */
+    int64_t k = 0;
+    for (int64_t q = 0; q < nseg; ++q)
+        if (scr->segs[q].t_out > scr->segs[q].t_in) scr->segs[k++] = scr->segs[q];
+    qsort(scr->segs, (size_t)k, sizeof(oc_seg), cmp_seg);
+    if (viol && mode == O3_TILE_LISTS)
+        for (int64_t q = 1; q < k; ++q)
+            if (scr->segs[q].list_pos < scr->segs[q - 1].list_pos) ++*viol;
+    return k;
+}
+
+/* Front-to-back compositing; returns K (number of composited segments, the
+ * termination index).  out[4] = (C + T bg, T). */
+static int64_t composite(const oc_scene *S, const oc_seg *segs, int64_t n, double out[4])
+{
+    double T = 1.0, C[3] = {0, 0, 0};
+    int64_t k = 0;
+    for (; k < n;) {
+        const oc_seg *s = segs + k;
+        double sig = (double)S->density[s->cell];
+        double tau = sig * (s->t_out - s->t_in);
+        double alpha = 1.0 - exp(-tau);
+        for (int c = 0; c < 3; ++c) C[c] += T * alpha * (double)S->rgb[3 * s->cell + c];
+        T *= exp(-tau);
+        ++k;
+        if (T < T_STOP) break;
+    }
+    for (int c = 0; c < 3; ++c) out[c] = C[c] + T * S->bg[c];
+    out[3] = T;
+    return k;
+}
+
+static uint64_t mix64(uint64_t h, uint64_t v)
+{
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h;
+}
+
+static void pixel_counters(const oc_scene *S, const oc_bins *B, int x, int y, const double Q[3],
+                           const double d[3], double t_near, const oc_seg *segs, int64_t K,
+                           int terminated, int64_t *cnt)
+{
+    /* list-order counters of the tile walk up to the terminating entry */
+    int t = (y / 16) * B->tiles_x + (x / 16);
+    uint32_t b = B->ranges[2 * t], e = B->ranges[2 * t + 1];
+    int64_t last = (int64_t)(e - b) - 1;
+    if (terminated && K > 0) last = segs[K - 1].list_pos;
+    int64_t xs = 0, xh = 0, xp = 0;
+    for (int64_t q = 0; q <= last; ++q) {
+        oc_seg s;
+        int64_t npc = 0;
+        ++xs;
+        if (cell_interval(S, O3_TILE_LISTS, B->vals[b + q], Q, d, t_near, &s, &npc)) {
+            ++xh;
+            xp += npc;
+        }
+    }
+    cnt[0] = xs;
+    cnt[1] = xh;
+    cnt[2] = xp;
+    cnt[3] = K;
+}
+
+static void make_scene(oc_scene *S, int64_t N, const float *sites, const float *weights,
+                       const float *radii, const float *density, const float *rgb,
+                       const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg)
+{
+    S->N = N;
+    S->sites = sites;
+    S->weights = weights;
+    S->radii = radii;
+    S->density = density;
+    S->rgb = rgb;
+    S->nbr_off = nbr_off;
+    S->nbr_idx = nbr_idx;
+    for (int c = 0; c < 3; ++c) S->bg[c] = bg ? (double)bg[c] : 0.0;
+}
+
+/*
+ * Render npix pixels (pix_xy = int32 pairs (x,y); NULL = the full image,
+ * row-major).  out: double[npix*4].  Optional outputs (may be NULL):
+ *   counters int64[npix*4] (O3 only), sig uint64[npix] (hash of the active-set
+ *   signature: cells, end kinds, plane ids, termination index), nseg int64[npix],
+ *   viol int64[1] (Theorem-2 order violations, O3 only).
+ */
+int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
+                  const float *radii, const float *density, const float *rgb,
+                  const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
+                  const oc_camera *cam, int64_t npix, const int32_t *pix_xy, double *out,
+                  int64_t *counters, uint64_t *sig, int64_t *nseg_out, int64_t *viol,
+                  int nthreads)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg);
+    oc_bins B;
+    memset(&B, 0, sizeof(B));
+    if (mode == O3_TILE_LISTS || counters) build_bins(&S, cam, &B);
+    if (!pix_xy) npix = (int64_t)cam->width * cam->height;
+    int64_t total_viol = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel reduction(+ : total_viol)
+    {
+        oc_scratch scr = {NULL, 0};
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t q = 0; q < npix; ++q) {
+            int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
+            int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
+            double Q[3], d[3], tn;
+            pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+            int64_t v = 0;
+            int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, &v);
+            total_viol += v;
+            int64_t K = composite(&S, scr.segs, n, out + 4 * q);
+            if (counters)
+                pixel_counters(&S, &B, x, y, Q, d, tn, scr.segs, K, out[4 * q + 3] < T_STOP,
+                               counters + 4 * q);
+            if (nseg_out) nseg_out[q] = K;
+            if (sig) {
+                uint64_t h = 1469598103934665603ull;
+                for (int64_t k = 0; k < K; ++k) {
+                    const oc_seg *s = scr.segs + k;
+                    h = mix64(h, (uint64_t)s->cell);
+                    h = mix64(h, (uint64_t)(s->kin * 4 + s->kout));
+                    h = mix64(h, (uint64_t)(uint32_t)s->jin);
+                    h = mix64(h, (uint64_t)(uint32_t)s->jout);
+                }
+                h = mix64(h, (uint64_t)K);
+                sig[q] = h;
+            }
+        }
+        free(scr.segs);
+    }
+    if (viol) *viol = total_viol;
+    if (B.vals) free_bins(&B);
+    return 0;
+}
+
+/* ======================================================================== */
+/* (2) backward                                                             */
+/* ======================================================================== */
+
+/* d t_end / d theta for one interval end (absolute t), SURVEY App. A.
+ *   sphere end:  dt/dp_i = (x*-p_i)/(d.(x*-p_i)),  dt/dr_i = r_i/(d.(x*-p_i))
+ *   plane end (i,j): dt/dp_i = (x*-p_i)/a, dt/dp_j = (p_j-x*)/a,
+ *                    dt/dw_i = 1/(2a),   dt/dw_j = -1/(2a),  a = d.(p_j-p_i)
+ *   near end: 0.
+ * Adds sgn * gdt * (those) into the gradient arrays. */
+static void end_grad(const oc_scene *S, int kind, int64_t i, int64_t j, double t,
+                     const double Q[3], const double d[3], double sgn_gdt, double *g_sites,
+                     double *g_w, double *g_r)
+{
+    if (kind == END_NEAR) return;
+    const float *p = S->sites + 3 * i;
+    double x[3] = {Q[0] + t * d[0], Q[1] + t * d[1], Q[2] + t * d[2]};
+    double xp[3] = {x[0] - p[0], x[1] - p[1], x[2] - p[2]};
+    if (kind == END_SPHERE) {
+        double den = d[0] * xp[0] + d[1] * xp[1] + d[2] * xp[2];
+        for (int m = 0; m < 3; ++m) {
+#pragma omp atomic
+            g_sites[3 * i + m] += sgn_gdt * xp[m] / den;
+        }
+#pragma omp atomic
+        g_r[i] += sgn_gdt * (double)S->radii[i] / den;
+        return;
+    }
+    const float *pj = S->sites + 3 * j;
+    double a = d[0] * ((double)pj[0] - p[0]) + d[1] * ((double)pj[1] - p[1]) +
+               d[2] * ((double)pj[2] - p[2]);
+    for (int m = 0; m < 3; ++m) {
+#pragma omp atomic
+        g_sites[3 * i + m] += sgn_gdt * xp[m] / a;
+#pragma omp atomic
+        g_sites[3 * j + m] += sgn_gdt * ((double)pj[m] - x[m]) / a;
+    }
+#pragma omp atomic
+    g_w[i] += sgn_gdt * 0.5 / a;
+#pragma omp atomic
+    g_w[j] -= sgn_gdt * 0.5 / a;
+}
+
+/*
+ * Gradients of L = sum_pixels <grad_out[pixel], out[pixel]> for npix pixels
+ * (same pixel convention as oracle_render; grad_out float[npix*4]).
+ * Accumulates (+=) into double arrays g_sites[N*3], g_w[N], g_r[N], g_sigma[N],
+ * g_rgb[N*3].  Compositing derivative: with
+ * S_k = sum_{m>k} T_m a_m c_m + T_{K+1} bg,
+ *   dL/dc_k = T_k a_k G,  dL/dtau_k = G.(T_{k+1} c_k - S_k) - G_T T_{K+1},
+ *   dL/dsigma_k = dL/dtau_k dt_k,  dL/ddt_k = dL/dtau_k sigma_k.
+ */
+int oracle_backward(int mode, int64_t N, const float *sites, const float *weights,
+                    const float *radii, const float *density, const float *rgb,
+                    const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
+                    const oc_camera *cam, int64_t npix, const int32_t *pix_xy,
+                    const float *grad_out, double *g_sites, double *g_w, double *g_r,
+                    double *g_sigma, double *g_rgb, int nthreads)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg);
+    oc_bins B;
+    memset(&B, 0, sizeof(B));
+    if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
+    if (!pix_xy) npix = (int64_t)cam->width * cam->height;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel
+    {
+        oc_scratch scr = {NULL, 0};
+        double *Tk = NULL, *Ak = NULL;
+        int64_t capk = 0;
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t q = 0; q < npix; ++q) {
+            int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
+            int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
+            double Q[3], d[3], tn;
+            pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+            int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL);
+            double out[4];
+            int64_t K = composite(&S, scr.segs, n, out);
+            if (K + 1 > capk) {
+                free(Tk);
+                free(Ak);
+                capk = K + 1;
+                Tk = (double *)malloc(sizeof(double) * (size_t)capk);
+                Ak = (double *)malloc(sizeof(double) * (size_t)capk);
+            }
+            /* T_k (transmittance before segment k) and alpha_k */
+            double T = 1.0;
+            for (int64_t k = 0; k < K; ++k) {
+                const oc_seg *s = scr.segs + k;
+                double tau = (double)S.density[s->cell] * (s->t_out - s->t_in);
+                Tk[k] = T;
+                Ak[k] = 1.0 - exp(-tau);
+                T *= exp(-tau);
+            }
+            double Tend = T; /* T_{K+1} */
+            const float *g = grad_out + 4 * q;
+            double G[3] = {g[0], g[1], g[2]}, GT = g[3];
+            for (int64_t k = 0; k < K; ++k) {
+                const oc_seg *s = scr.segs + k;
+                int64_t i = s->cell;
+                double dt = s->t_out - s->t_in;
+                double sig = (double)S.density[i];
+                double Tnext = Tk[k] * exp(-sig * dt);
+                /* S_k = sum_{m>k} T_m a_m c_m + T_{K+1} bg */
+                double Sk[3];
+                for (int c = 0; c < 3; ++c) Sk[c] = Tend * S.bg[c];
+                for (int64_t m = k + 1; m < K; ++m)
+                    for (int c = 0; c < 3; ++c)
+                        Sk[c] += Tk[m] * Ak[m] * (double)S.rgb[3 * scr.segs[m].cell + c];
+                double dtau = -GT * Tend;
+                for (int c = 0; c < 3; ++c) {
+                    dtau += G[c] * (Tnext * (double)S.rgb[3 * i + c] - Sk[c]);
+#pragma omp atomic
+                    g_rgb[3 * i + c] += Tk[k] * Ak[k] * G[c];
+                }
+#pragma omp atomic
+                g_sigma[i] += dtau * dt;
+                double gdt = dtau * sig;
+                if (gdt != 0.0) {
+                    end_grad(&S, s->kout, i, s->jout, s->t_out, Q, d, gdt, g_sites, g_w, g_r);
+                    end_grad(&S, s->kin, i, s->jin, s->t_in, Q, d, -gdt, g_sites, g_w, g_r);
+                }
+            }
+        }
+        free(scr.segs);
+        free(Tk);
+        free(Ak);
+    }
+    if (B.vals) free_bins(&B);
+    return 0;
+}
+
+/* ======================================================================== */
+/* debug entry points for the pins                                          */
+/* ======================================================================== */
+
+/* Interval of cell i along an arbitrary ray (Q, d unit, t_near).  mode O1 or O2.
+ * res[0..1] = t_in, t_out (absolute); kinds[0..3] = kin, kout, jin, jout.
+ * Returns 1 on a sphere hit, 0 otherwise. */
+int oracle_cell_interval(int mode, int64_t N, const float *sites, const float *weights,
+                         const float *radii, const int64_t *nbr_off, const int32_t *nbr_idx,
+                         int64_t i, const double *Q, const double *d, double t_near,
+                         double *res, int32_t *kinds)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, NULL, NULL, nbr_off, nbr_idx, NULL);
+    oc_seg s;
+    int64_t np = 0;
+    int hit = cell_interval(&S, mode, i, Q, d, t_near, &s, &np);
+    if (!hit) return 0;
+    res[0] = s.t_in;
+    res[1] = s.t_out;
+    kinds[0] = s.kin;
+    kinds[1] = s.kout;
+    kinds[2] = s.jin;
+    kinds[3] = s.jout;
+    return 1;
+}
+
+/* The ray of pixel (x, y): Q[3], d[3], t_near. */
+int oracle_pixel_ray(const oc_camera *cam, int32_t x, int32_t y, double *Q, double *d,
+                     double *t_near)
+{
+    pixel_ray(cam, x + 0.5, y + 0.5, Q, d, t_near);
+    return 0;
+}
+
+/* Front-to-back compositing of explicit segments (sigma[k], dt[k], rgb[3k]):
+ * out[4] = (C + T bg, T); returns the termination index. */
+int64_t oracle_composite(int64_t n, const double *sigma, const double *dt, const double *rgb,
+                         const double *bg, double *out)
+{
+    double T = 1.0, C[3] = {0, 0, 0};
+    int64_t k = 0;
+    for (; k < n;) {
+        double tau = sigma[k] * dt[k];
+        double alpha = 1.0 - exp(-tau);
+        for (int c = 0; c < 3; ++c) C[c] += T * alpha * rgb[3 * k + c];
+        T *= exp(-tau);
+        ++k;
+        if (T < T_STOP) break;
+    }
+    for (int c = 0; c < 3; ++c) out[c] = C[c] + T * bg[c];
+    out[3] = T;
+    return k;
+}
+
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
