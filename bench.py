@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""bench.py -- Power Foam rasterizer throughput on B200 (BASELINE.json metric).
+
+Default workload: train8_1m (1M-cell Mip-NeRF-360-shaped foam, 8 views at
+1920x1080 per GPU, forward + backward, per-cell gradient all-reduce over NCCL
+when N > 1).  One step = one pass of the whole hot path (K0 edge records, K1
+projection/binning, K2 scan, K3 emit, K4 radix sort, K5 ranges, K6 forward
+blend, K7 backward, K8 unpack, + all-reduce) over one batch of 8 views.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.  `value` = frames (views) per second of fwd+bwd
+for the whole job (all ranks; weak scaling: each rank owns 8 distinct views).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "frames/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+
+
+# ----------------------------------------------------------------------------
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="train8_1m",
+                    choices=["train8_1m", "mip360_1m", "nerfsynth200k", "sweep64_3m", "small360"])
+    ap.add_argument("--views", type=int, default=None, help="views per GPU (default: preset)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_cameras(name, n_views, world, rank):
+    """Weak scaling: rank r renders views r, r+N, ... of an orbit of n_views*N cameras."""
+    import pf_synth
+    total = n_views * world
+    if name in ("train8_1m", "mip360_1m", "sweep64_3m"):
+        step = math.radians(5.625) if name == "sweep64_3m" else 2 * math.pi / total
+        cams = pf_synth._cams_mip360(total, 1920, 1080, az_step=step,
+                                     jitter=0.3 if name == "sweep64_3m" else 0.0, seed=3)
+    elif name == "nerfsynth200k":
+        cams = pf_synth._cams_nerfsynth(total, 800, 800)
+    else:
+        cams = pf_synth.make_cameras(name, n=total)
+    return cams[rank::world]
+
+
+def default_views(name):
+    return {"train8_1m": 8, "mip360_1m": 1, "nerfsynth200k": 8, "sweep64_3m": 64,
+            "small360": 4}[name]
+
+
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if f[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+def flops_model(cnt):
+    """Algorithmic FP32 work per view from the per-pixel counters:
+    F_fwd = 8 X_s + 14 X_h + 16 X_p + 15 X_c;  F_bwd = F_fwd (replay) + 60 X_c
+    + 30 * (active plane endpoints, <= 2 X_c)."""
+    Xs, Xh, Xp, Xc = (float(v) for v in cnt)
+    f_fwd = 8 * Xs + 14 * Xh + 16 * Xp + 15 * Xc
+    f_bwd = f_fwd + 60 * Xc + 30 * 2 * Xc
+    return f_fwd, f_bwd
+
+
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_PATH)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args):
+    """The oracle (CPU, double) timed on this host on a bounded sample."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import pf_synth
+    wl = args.workload
+    sc = pf_synth.make_scene(wl)
+    nv = args.views or default_views(wl)
+    cams = workload_cameras(wl, nv, 1, 0)
+    res = cpu_baseline(sc, cams[0], args.cpu_seconds, train=wl != "mip360_1m")
+    steps = []
+    for _ in range(max(args.warmup, 0)):
+        pass
+    for _ in range(args.steps):
+        r = cpu_baseline(sc, cams[0], args.cpu_seconds / max(args.steps, 1), train=wl != "mip360_1m",
+                         calib=res)
+        steps.append(r["value"])
+    val = float(np.median(steps)) if steps else res["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl, "cells": sc.num_cells, "views": nv,
+                       "width": cams[0].width, "height": cams[0].height},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": res["cores"],
+                             "kind": "oracle", "sample": res["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(sc, cam, seconds, train=True, calib=None):
+    """Times the oracle (O3 tile-list mode, double, OpenMP over pixels) on a
+    bounded sample of pixel rows of one view; extrapolates to frames/s."""
+    import oracle
+    import pf_synth
+    H, W = cam.height, cam.width
+    g = pf_synth.make_grad_out(1, H, W, seed=12)[0]
+
+    def run(rows):
+        y = np.arange(rows) * max(H // max(rows, 1), 1)
+        y = y[y < H][:rows]
+        pix = np.stack(np.meshgrid(np.arange(W), y), -1).reshape(-1, 2)
+        t0 = time.perf_counter()
+        oracle.render(sc, cam, mode=oracle.O3, pixels=pix)
+        if train:
+            oracle.backward(sc, cam, g[pix[:, 1], pix[:, 0]], mode=oracle.O3, pixels=pix)
+        return time.perf_counter() - t0, pix.shape[0]
+
+    if calib is None:
+        t1, n1 = run(2)
+        per_px = max(t1 / n1, 1e-9)
+    else:
+        per_px = calib["per_px"]
+    rows = int(max(1, min(H, seconds / per_px / W)))
+    t, n = run(rows)
+    frac = n / float(H * W)
+    fps = frac / t
+    return {"value": fps, "per_px": t / n, "cores": oracle.num_threads(),
+            "sample": f"{n} pixels ({rows} rows) of one {W}x{H} view, O3 "
+                      f"{'forward+backward' if train else 'forward'} incl. its own binning, "
+                      f"{t:.1f}s; frames/s extrapolated from the pixel fraction"}
+
+
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_24994_b200 as pf
+    import pf_synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = args.workload
+    nv = args.views or default_views(wl)
+    t_gen = time.perf_counter()
+    sc = pf_synth.make_scene(wl)
+    cams = workload_cameras(wl, nv, ws, rank)
+    t_gen = time.perf_counter() - t_gen
+    H, W = cams[0].height, cams[0].width
+    train = wl != "mip360_1m"
+    r = pf.Renderer.from_scene(sc, dev, flags=0)
+    N = sc.num_cells
+    grad_out = torch.from_numpy(pf_synth.make_grad_out(nv, H, W, seed=12 + rank)).to(dev)
+    flat = torch.zeros(9 * N, device=dev, dtype=torch.float32)
+    out = torch.empty((nv, H, W, 4), device=dev, dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        r.forward(cams, out=out)
+        if train:
+            flat.zero_()
+            r.backward(cams, grad_out, flat)
+            if ws > 1:
+                dist.all_reduce(flat)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # ---------------- timed region (device events, max over ranks) ----------
+    r.set_profiling(True)
+    r.stage_times()
+    l0 = r.launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    launches = r.launch_count() - l0
+    stages = r.stage_times()
+    r.set_profiling(False)
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    fps = ws * nv / (ms_step / 1e3)
+
+    # ---------------- forward-only throughput (extra) ------------------------
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        r.forward(cams, out=out)
+    f1.record(stream)
+    barrier()
+    tf = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
+    if ws > 1:
+        dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+    fwd_fps = ws * nv / (float(tf.item()) / 1e3)
+
+    # ---------------- end to end: host buffers through the public API -------
+    e2e = None
+    if not args.no_e2e:
+        g_host = grad_out.cpu().pin_memory()
+        grad_host = torch.empty(9 * N, dtype=torch.float32).pin_memory()
+        g_dev = torch.empty_like(grad_out)
+
+        def e2e_step():
+            g_dev.copy_(g_host, non_blocking=True)
+            r.forward(cams, out=out)
+            flat.zero_()
+            r.backward(cams, g_dev, flat)
+            if ws > 1:
+                dist.all_reduce(flat)
+            grad_host.copy_(flat, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        a1.record(stream)
+        barrier()
+        te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * nv / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(g_host.numel() * 4),
+               "d2h_bytes_per_step": int(grad_host.numel() * 4),
+               "note": "H2D of the step's dL/dimage from pinned host + fwd + bwd "
+                       "(+ all-reduce) + D2H of the per-cell gradients, every step"}
+
+    # ---------------- counters -> algorithmic flops, roofline ----------------
+    cnt = np.zeros(4)
+    for c in cams[:2]:
+        cnt += r.debug_counters(c).sum(dim=(0, 1)).double().cpu().numpy()
+    cnt /= min(2, len(cams))
+    f_fwd, f_bwd = flops_model(cnt)
+    peaks, peaks_kind = load_peaks()
+    k6_ms, k6_n = stages["K6_forward"]
+    k7_ms, k7_n = stages["K7_backward"]
+    sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    dom = "K7_backward" if (train and k7_ms >= k6_ms) else "K6_forward"
+    d_ms, d_n = stages[dom]
+    d_avg = d_ms / max(d_n, 1)
+    d_flops = f_bwd if dom == "K7_backward" else f_fwd
+    achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
+    roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
+                "traffic": None,
+                "peak_note": f"FP32 = {SM_COUNT} SM x {FP32_LANES_PER_SM} lanes x 2 x "
+                             f"{sm_max:.0f} MHz (guide unit counts; no tensor-core path)",
+                "avg_launch_ms": d_avg,
+                "algorithmic_flops_per_launch": d_flops}
+    sort_ms, sort_n = stages["K4_sort"]
+    pairs = r.pair_counts(nv)
+    P = float(np.mean(pairs))
+    passes = math.ceil((32 + math.ceil(math.log2((W + 15) // 16 * ((H + 15) // 16)))) / 8)
+    sort_bytes = 32.0 * P * passes
+    sort_gbs = sort_bytes / (sort_ms / max(sort_n, 1) / 1e3) / 1e9 if sort_ms > 0 else None
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(sc, cams[0], args.cpu_seconds, train=train)
+            cpu = {"value": cpu["value"], "unit": UNIT, "cores": cpu["cores"], "kind": "oracle",
+                   "sample": cpu["sample"]}
+        except Exception as ex:  # noqa
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps if train else fwd_fps, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (pf_synth seeded generator, random-init foam)",
+            "config": {"workload": wl, "cells": N, "edges": sc.num_edges, "views_per_gpu": nv,
+                       "global_batch_views": nv * ws, "width": W, "height": H,
+                       "pass": "fwd+bwd" if train else "fwd",
+                       "parallelism": f"dp{ws} (views sharded, per-cell grad all-reduce)",
+                       "l2": "inputs larger than L2 (scene records+edges+grad_out > 126 MB)"},
+            "clocks": clocks, "gpu_launches": int(launches),
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "fwd_fps": fwd_fps, "fwdbwd_fps": fps if train else None,
+            "mpix_s": (fps if train else fwd_fps) * W * H / 1e6, "fwd_mpix_s": fwd_fps * W * H / 1e6,
+            "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "stage_launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
+            "pairs_per_view": P, "counters_per_view": {"X_s": cnt[0], "X_h": cnt[1],
+                                                       "X_p": cnt[2], "X_c": cnt[3]},
+            "sort": {"ms_per_view": sort_ms / max(sort_n, 1), "passes": passes,
+                     "bytes_per_view": sort_bytes, "achieved_gbs": sort_gbs,
+                     "hbm_frac": (sort_gbs / hbm) if sort_gbs else None},
+            "peaks_source": peaks_kind, "scene_gen_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    r.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

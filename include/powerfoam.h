@@ -1,0 +1,184 @@
+/*
+ * powerfoam.h -- C ABI of the B200-native Power Foam rasterizer
+ * (arXiv 2604.24994: tile-based differentiable rasterization of bounded
+ * power-diagram cells, forward and backward).
+ *
+ * Citations: P:<line> = PAPER.md, S:<line> = SPEC.md, SURVEY §x = SURVEY.md,
+ * DESIGN §x = DESIGN.md (the readings of the paper that fix what is left open).
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ *  - Every function returns an int status (PF_OK = 0) and never throws.
+ *    On a non-zero status pf_last_error() returns a thread-local message.
+ *  - Array arguments are DEVICE pointers owned by the caller (in practice
+ *    PyTorch tensors); the library stores scene pointers without copying them
+ *    and re-reads them at every forward (so in-place optimizer updates between
+ *    steps are seen).  Parameters must not change between a forward and its
+ *    matching backward.
+ *  - Camera arrays (pf_camera) are HOST memory.
+ *  - `stream` is a cudaStream_t (declared here as an opaque pointer so this
+ *    header does not need the CUDA headers); every call enqueues its work on it
+ *    and returns.  The one exception: pf_render_forward reads the pair counts
+ *    of all its views back to the host once per call (one stream sync), to size
+ *    the per-tile lists.
+ *  - A handle is bound to the device that was current at creation; calls on one
+ *    handle are not thread-safe; separate handles are independent.
+ *  - Pixel (x, y) has its centre at (x + 0.5, y + 0.5); tiles are 16x16 pixels;
+ *    images are row-major.
+ */
+#ifndef POWERFOAM_H
+#define POWERFOAM_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PF_API __attribute__((visibility("default")))
+#else
+#define PF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *pf_stream_t; /* == cudaStream_t */
+typedef struct pf_scene pf_scene;        /* opaque; owns workspaces and saved state only */
+
+/* status codes (S:615 exit-code convention: 1 malformed input, 2 render failure) */
+enum {
+    PF_OK = 0,
+    PF_ERR_INVALID_ARGUMENT = 1, /* null pointer, N < 1, W/H < 1 or > 32768, fx/fy <= 0,
+                                    non-finite camera, validation failure (PF_VALIDATE) */
+    PF_ERR_CUDA = 2,             /* launch / asynchronous CUDA error (message has the text) */
+    PF_ERR_OUT_OF_MEMORY = 3,
+    PF_ERR_STATE = 4             /* backward without a matching forward (views / sizes differ) */
+};
+
+/* scene flags */
+enum {
+    PF_VALIDATE = 1u << 0,     /* check the scene on the device at creation (finite values,
+                                  r > 0, sigma >= 0, neighbour ids in [0,N) and != i) */
+    PF_STATIC_SCENE = 1u << 1  /* parameters never change after creation: the edge records
+                                  (K0) are built once in pf_create_scene, not per forward */
+};
+
+/*
+ * The scene: N bounded power cells and their neighbour lists.
+ *   cell i = power site p_i with weight w_i ("squared radius (also known ...
+ *   as a weight)"; the paper ties w_i = r_i^2, the ABI takes both),
+ *   bounding sphere B_i of radius r_i, density sigma_i >= 0 and constant
+ *   linear radiance rgb_i (appearance reading SURVEY C6).
+ *   Bounded cell C_i = {x : pow(x,i) <= pow(x,j) for all j} ∩ B_i with
+ *   pow(x,i) = |x - p_i|^2 - w_i.
+ *   nbr_indices[nbr_offsets[i] .. nbr_offsets[i+1]) must contain every j whose
+ *   radical plane can cut B_i: the Čech complex (all overlapping spheres)
+ *   suffices when w = r^2; extra neighbours are allowed.
+ */
+typedef struct {
+    int64_t num_cells;          /* N >= 1 */
+    int64_t num_edges;          /* E = nbr_offsets[N] (host copy of the last offset) */
+    const float *sites;         /* device f32[N,3]  p_i (world units), row-major */
+    const float *weights;       /* device f32[N]    w_i */
+    const float *radii;         /* device f32[N]    r_i > 0 */
+    const float *density;       /* device f32[N]    sigma_i >= 0 (1/world units) */
+    const float *rgb;           /* device f32[N,3]  linear radiance */
+    const int64_t *nbr_offsets; /* device i64[N+1] CSR offsets, nbr_offsets[0] = 0 */
+    const int32_t *nbr_indices; /* device i32[E]   neighbour ids */
+    float background[3];        /* constant background radiance */
+    uint32_t flags;             /* PF_VALIDATE | PF_STATIC_SCENE */
+} pf_scene_desc;
+
+/* Pinhole camera, OpenCV axes (x right, y down, z forward).
+ * Pixel ray: d_cam = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1), d = normalize(R d_cam),
+ * origin Q; the ray is clipped to camera-space z >= near_plane, i.e.
+ * t >= near_plane * |d_cam|. */
+typedef struct {
+    int32_t width, height; /* pixels, 1..32768 */
+    float fx, fy, cx, cy;  /* pixel units, fx, fy > 0 */
+    float c2w[12];         /* row-major 3x4 [R | Q], world-from-camera */
+    float near_plane;      /* > 0 */
+} pf_camera;
+
+/* Creates a handle for the scene described by *desc (pointers are stored, not
+ * copied).  With PF_VALIDATE the scene is checked on the device (one sync). */
+PF_API int pf_create_scene(const pf_scene_desc *desc, pf_scene **out, pf_stream_t stream);
+
+/*
+ * Forward render of num_views >= 1 views (all of the same width x height).
+ * out: device f32[V,H,W,4], out[v,y,x] = (R, G, B, T_final).
+ * Per view: project every bounding sphere and bin it to 16x16 tiles,
+ * key = pow(Q, p_i) (Theorem 2), radix-sort (tile, key) pairs
+ * ("global sort by depths ... similar to 3DGS"), then per pixel walk the
+ * tile list: interval of the ray in each bounded cell from the sphere and the
+ * radical planes of its neighbours (P:228, P:577-585 with the weight sign of
+ * SURVEY C1), composite front to back with alpha = 1 - exp(-sigma dt)
+ * (SURVEY C4), stop after the segment that makes T < 1e-4 (C7),
+ * out = (C + T bg, T).  Forward results are bit-deterministic.
+ * Saves per-view state (sorted lists, final colours) for pf_render_backward.
+ */
+PF_API int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t num_views, float *out,
+                      pf_stream_t stream);
+
+/*
+ * Backward of the immediately preceding pf_render_forward with the same cameras
+ * (else PF_ERR_STATE).  grad_out: device f32[V,H,W,4] = dL/d(out) (channel 3 =
+ * dL/dT_final).  ACCUMULATES (+=) dL/d(param) into the five caller arrays
+ * (device f32 [N,3], [N], [N], [N], [N,3]); the caller zeroes them.  Exact
+ * derivative of the forward for its active constraints and termination index
+ * (SURVEY App. A).  Float atomics: deterministic up to summation order.
+ */
+PF_API int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t num_views,
+                       const float *grad_out, float *grad_sites, float *grad_weights,
+                       float *grad_radii, float *grad_density, float *grad_rgb,
+                       pf_stream_t stream);
+
+/* Frees everything the handle owns (not the caller's arrays).  NULL is a no-op. */
+PF_API int pf_destroy(pf_scene *s);
+
+/* Thread-local message for the last non-zero status of this thread. */
+PF_API const char *pf_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Debug / measurement exports (used by the parity tests and bench.py).
+ * ------------------------------------------------------------------------- */
+
+/*
+ * Binning outputs of one camera, device outputs:
+ *   rect i32[N,4] (tx0, ty0, tx1, ty1 half-open), count i32[N], keybits u32[N],
+ *   keys u64[P], vals u32[P] (sorted), ranges u32[T,2] ([start,end), (0,0) empty).
+ * *num_pairs (host) receives P.  If keys == NULL only rect/count/keybits and P
+ * are produced (so the caller can size keys/vals).  Synchronizes the stream.
+ */
+PF_API int pf_debug_binning(pf_scene *s, const pf_camera *cam, int32_t *rect, int32_t *count,
+                     uint32_t *keybits, uint64_t *keys, uint32_t *vals, uint32_t *ranges,
+                     int64_t *num_pairs, pf_stream_t stream);
+
+/*
+ * Per-pixel work counters of one forward view (counting build of the forward
+ * kernel): counters i64[H,W,4] = (X_s list entries examined, X_h sphere hits,
+ * X_p plane evaluations, X_c composited segments) -- SURVEY §8(d).
+ */
+PF_API int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_stream_t stream);
+
+/* Kernel launches issued by this handle since creation (bench "gpu_launches"). */
+PF_API int64_t pf_launch_count(const pf_scene *s);
+
+/*
+ * Stage timing.  While enabled, CUDA events are recorded (on the call's
+ * stream) around every launch of the named stages; pf_stage_times synchronizes,
+ * writes per-stage totals in milliseconds and launch counts, and clears them.
+ * Stages: 0 edge records (K0), 1 preprocess (K1), 2 scan (K2), 3 emit (K3),
+ * 4 sort (K4), 5 ranges (K5), 6 forward blend (K6), 7 backward (K7), 8 unpack (K8).
+ */
+#define PF_NUM_STAGES 9
+PF_API int pf_set_profiling(pf_scene *s, int enable);
+PF_API int pf_stage_times(pf_scene *s, double *ms /* [PF_NUM_STAGES] */,
+                   int64_t *launches /* [PF_NUM_STAGES] */);
+
+/* Pairs P of each view of the last forward (host int64[num_views]). */
+PF_API int pf_last_pair_counts(const pf_scene *s, int64_t *pairs, int32_t num_views);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POWERFOAM_H */

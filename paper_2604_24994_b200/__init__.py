@@ -1,0 +1,283 @@
+"""paper_2604_24994_b200 -- B200-native Power Foam rasterizer (arXiv 2604.24994).
+
+Thin ctypes binding of the C-ABI library ``libpowerfoam.so`` (include/powerfoam.h).
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels.  PyTorch supplies device memory, streams and process groups.
+There is no CPU fallback: if the library cannot be loaded, every entry point
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import _build
+
+__all__ = ["PFError", "Renderer", "render", "load_library", "PF_VALIDATE", "PF_STATIC_SCENE",
+           "STAGES"]
+
+PF_VALIDATE = 1
+PF_STATIC_SCENE = 2
+STAGES = ["K0_edge_records", "K1_preprocess", "K2_scan", "K3_emit", "K4_sort", "K5_ranges",
+          "K6_forward", "K7_backward", "K8_unpack"]
+_STATUS = {0: "PF_OK", 1: "PF_ERR_INVALID_ARGUMENT", 2: "PF_ERR_CUDA",
+           3: "PF_ERR_OUT_OF_MEMORY", 4: "PF_ERR_STATE"}
+
+EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_backward", "pf_destroy",
+           "pf_last_error", "pf_debug_binning", "pf_debug_counters", "pf_launch_count",
+           "pf_set_profiling", "pf_stage_times", "pf_last_pair_counts"]
+
+
+class PFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("c2w", C.c_float * 12), ("near_plane", C.c_float)]
+
+
+class _SceneDesc(C.Structure):
+    _fields_ = [("num_cells", C.c_int64), ("num_edges", C.c_int64),
+                ("sites", C.c_void_p), ("weights", C.c_void_p), ("radii", C.c_void_p),
+                ("density", C.c_void_p), ("rgb", C.c_void_p), ("nbr_offsets", C.c_void_p),
+                ("nbr_indices", C.c_void_p), ("background", C.c_float * 3),
+                ("flags", C.c_uint32)]
+
+
+_lib = None
+
+
+def load_library(build_if_missing: bool = True):
+    """Loads libpowerfoam.so (building it with nvcc if absent or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if build_if_missing:
+        try:
+            path = _build.build()
+        except Exception:  # no nvcc on this box: use the shipped .so if present
+            if not os.path.exists(path):
+                raise
+    if not os.path.exists(path):
+        raise RuntimeError(f"libpowerfoam.so not found at {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
+    P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    L.pf_create_scene.argtypes = [C.POINTER(_SceneDesc), C.POINTER(C.c_void_p), P]
+    L.pf_render_forward.argtypes = [P, C.POINTER(_Camera), i32, P, P]
+    L.pf_render_backward.argtypes = [P, C.POINTER(_Camera), i32, P, P, P, P, P, P, P]
+    L.pf_destroy.argtypes = [P]
+    L.pf_last_error.restype = C.c_char_p
+    L.pf_debug_binning.argtypes = [P, C.POINTER(_Camera), P, P, P, P, P, P, C.POINTER(i64), P]
+    L.pf_debug_counters.argtypes = [P, C.POINTER(_Camera), P, P]
+    L.pf_launch_count.argtypes = [P]
+    L.pf_launch_count.restype = i64
+    L.pf_set_profiling.argtypes = [P, C.c_int]
+    L.pf_stage_times.argtypes = [P, P, P]
+    L.pf_last_pair_counts.argtypes = [P, P, i32]
+    for name in EXPORTS:
+        getattr(L, name).restype = getattr(L, name).restype or C.c_int
+    L.pf_last_error.restype = C.c_char_p
+    L.pf_launch_count.restype = i64
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise PFError(status, load_library().pf_last_error().decode())
+
+
+def _cams(cams) -> tuple:
+    if not isinstance(cams, (list, tuple)):
+        cams = [cams]
+    arr = (_Camera * len(cams))()
+    for k, c in enumerate(cams):
+        arr[k].width, arr[k].height = int(c.width), int(c.height)
+        arr[k].fx, arr[k].fy, arr[k].cx, arr[k].cy = (float(c.fx), float(c.fy), float(c.cx),
+                                                      float(c.cy))
+        m = [float(v) for v in (c.c2w.tolist() if hasattr(c.c2w, "tolist") else c.c2w)]
+        for q in range(12):
+            arr[k].c2w[q] = m[q]
+        arr[k].near_plane = float(c.near if hasattr(c, "near") else c.near_plane)
+    return arr, len(cams)
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev_f32(t, shape=None):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
+            and t.is_contiguous()):
+        raise TypeError("expected a contiguous float32 CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
+    return C.c_void_p(t.data_ptr())
+
+
+class Renderer:
+    """Owns one pf_scene handle over caller tensors (kept referenced here).
+
+    sites f32[N,3], weights f32[N], radii f32[N], density f32[N], rgb f32[N,3],
+    nbr_offsets i64[N+1], nbr_indices i32[E]: CUDA tensors on one device.
+    """
+
+    def __init__(self, sites, weights, radii, density, rgb, nbr_offsets, nbr_indices,
+                 background=(0.0, 0.0, 0.0), flags: int = 0, num_edges: int | None = None,
+                 stream=None):
+        L = load_library()
+        self.N = int(sites.shape[0])
+        self.device = sites.device
+        self._tensors = (sites, weights, radii, density, rgb, nbr_offsets, nbr_indices)
+        for t in (sites, weights, radii, density, rgb):
+            _dev_f32(t)
+        if nbr_offsets.dtype != torch.int64 or nbr_indices.dtype != torch.int32:
+            raise TypeError("nbr_offsets must be int64 and nbr_indices int32")
+        if not (nbr_offsets.is_cuda and nbr_indices.is_cuda):
+            raise TypeError("neighbour lists must be CUDA tensors")
+        E = int(nbr_indices.numel()) if num_edges is None else int(num_edges)
+        d = _SceneDesc()
+        d.num_cells = self.N
+        d.num_edges = E
+        d.sites, d.weights, d.radii = sites.data_ptr(), weights.data_ptr(), radii.data_ptr()
+        d.density, d.rgb = density.data_ptr(), rgb.data_ptr()
+        d.nbr_offsets = nbr_offsets.data_ptr()
+        d.nbr_indices = nbr_indices.data_ptr() if E > 0 else None
+        for c in range(3):
+            d.background[c] = float(background[c])
+        d.flags = int(flags)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(L.pf_create_scene(C.byref(d), C.byref(h), _stream(stream)))
+        self._h = h
+        self._L = L
+
+    @classmethod
+    def from_scene(cls, sc, device="cuda", flags: int = 0):
+        """Uploads a pf_synth.Scene-like object (numpy arrays) and wraps it."""
+        dev = torch.device(device)
+        t = lambda a, dt: torch.as_tensor(a).to(device=dev, dtype=dt).contiguous()
+        return cls(t(sc.sites, torch.float32), t(sc.weights, torch.float32),
+                   t(sc.radii, torch.float32), t(sc.density, torch.float32),
+                   t(sc.rgb, torch.float32), t(sc.nbr_offsets, torch.int64),
+                   t(sc.nbr_indices, torch.int32), background=sc.background, flags=flags)
+
+    # -------------------------------------------------------------- hot path
+    def forward(self, cams, out=None, stream=None):
+        arr, V = _cams(cams)
+        H, W = arr[0].height, arr[0].width
+        if out is None:
+            out = torch.empty((V, H, W, 4), device=self.device, dtype=torch.float32)
+        _dev_f32(out, (V, H, W, 4))
+        _check(self._L.pf_render_forward(self._h, arr, V, C.c_void_p(out.data_ptr()),
+                                         _stream(stream)))
+        return out
+
+    def backward(self, cams, grad_out, grads=None, stream=None):
+        """Accumulates dL/dparams into `grads` (dict or flat f32[9N] tensor; zeros if None)."""
+        arr, V = _cams(cams)
+        H, W = arr[0].height, arr[0].width
+        _dev_f32(grad_out, (V, H, W, 4))
+        if grads is None:
+            grads = torch.zeros(9 * self.N, device=self.device, dtype=torch.float32)
+        views = self.grad_views(grads) if isinstance(grads, torch.Tensor) else grads
+        ptrs = [_dev_f32(views[k]) for k in ("sites", "weights", "radii", "density", "rgb")]
+        _check(self._L.pf_render_backward(self._h, arr, V, C.c_void_p(grad_out.data_ptr()),
+                                          *ptrs, _stream(stream)))
+        return views
+
+    def grad_views(self, flat):
+        """Views of a flat f32[9N] gradient buffer as the five arrays (one NCCL buffer)."""
+        N = self.N
+        return {"sites": flat[0:3 * N].view(N, 3), "weights": flat[3 * N:4 * N],
+                "radii": flat[4 * N:5 * N], "density": flat[5 * N:6 * N],
+                "rgb": flat[6 * N:9 * N].view(N, 3)}
+
+    # ----------------------------------------------------------- debug / stats
+    def debug_binning(self, cam, stream=None):
+        arr, _ = _cams(cam)
+        N, dev = self.N, self.device
+        rect = torch.empty((N, 4), device=dev, dtype=torch.int32)
+        count = torch.empty(N, device=dev, dtype=torch.int32)
+        kb = torch.empty(N, device=dev, dtype=torch.int32)
+        P = C.c_int64()
+        _check(self._L.pf_debug_binning(self._h, arr, rect.data_ptr(), count.data_ptr(),
+                                        kb.data_ptr(), None, None, None, C.byref(P),
+                                        _stream(stream)))
+        n = max(int(P.value), 1)
+        tx, ty = (arr[0].width + 15) // 16, (arr[0].height + 15) // 16
+        keys = torch.empty(n, device=dev, dtype=torch.int64)
+        vals = torch.empty(n, device=dev, dtype=torch.int32)
+        ranges = torch.empty((tx * ty, 2), device=dev, dtype=torch.int32)
+        _check(self._L.pf_debug_binning(self._h, arr, rect.data_ptr(), count.data_ptr(),
+                                        kb.data_ptr(), keys.data_ptr(), vals.data_ptr(),
+                                        ranges.data_ptr(), C.byref(P), _stream(stream)))
+        Pn = int(P.value)
+        return dict(rect=rect, count=count, keybits=kb, keys=keys[:Pn], vals=vals[:Pn],
+                    ranges=ranges, P=Pn)
+
+    def debug_counters(self, cam, stream=None):
+        arr, _ = _cams(cam)
+        cnt = torch.zeros((arr[0].height, arr[0].width, 4), device=self.device,
+                          dtype=torch.int64)
+        _check(self._L.pf_debug_counters(self._h, arr, cnt.data_ptr(), _stream(stream)))
+        return cnt
+
+    def launch_count(self) -> int:
+        return int(self._L.pf_launch_count(self._h))
+
+    def set_profiling(self, on: bool):
+        _check(self._L.pf_set_profiling(self._h, int(bool(on))))
+
+    def stage_times(self):
+        ms = (C.c_double * 9)()
+        n = (C.c_int64 * 9)()
+        _check(self._L.pf_stage_times(self._h, ms, n))
+        return {STAGES[k]: (float(ms[k]), int(n[k])) for k in range(9)}
+
+    def pair_counts(self, V: int):
+        out = (C.c_int64 * V)()
+        _check(self._L.pf_last_pair_counts(self._h, out, V))
+        return [int(v) for v in out]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _RenderFn(torch.autograd.Function):
+    """Differentiable render: inputs are the five parameter tensors; the
+    neighbour lists and cameras are non-differentiable context."""
+
+    @staticmethod
+    def forward(ctx, renderer, cams, sites, weights, radii, density, rgb):
+        ctx.renderer, ctx.cams = renderer, cams
+        return renderer.forward(cams)
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        r = ctx.renderer
+        g = torch.zeros(9 * r.N, device=r.device, dtype=torch.float32)
+        v = r.backward(ctx.cams, grad_out.contiguous(), g)
+        return None, None, v["sites"], v["weights"], v["radii"], v["density"], v["rgb"]
+
+
+def render(renderer: Renderer, cams):
+    """Autograd-aware forward over the renderer's parameter tensors."""
+    s, w, r, d, c = renderer._tensors[:5]
+    return _RenderFn.apply(renderer, cams, s, w, r, d, c)

@@ -1,0 +1,525 @@
+// pf_api.cu -- host side of the C ABI (include/powerfoam.h): handle, argument
+// checks, grow-only workspaces, per-view saved state, error strings, stage timing.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "pf_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(e == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PF_CUDA(expr)                                        \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+    } while (0)
+
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool finitef(float v) { return isfinite(v); }
+
+int check_camera(const pf_camera &c)
+{
+    if (c.width < 1 || c.height < 1 || c.width > 32768 || c.height > 32768)
+        return fail(PF_ERR_INVALID_ARGUMENT, "camera width/height must be in [1, 32768]");
+    if (!(c.fx > 0.0f) || !(c.fy > 0.0f) || !finitef(c.fx) || !finitef(c.fy))
+        return fail(PF_ERR_INVALID_ARGUMENT, "camera fx/fy must be finite and > 0");
+    if (!finitef(c.cx) || !finitef(c.cy))
+        return fail(PF_ERR_INVALID_ARGUMENT, "camera cx/cy must be finite");
+    for (int k = 0; k < 12; ++k)
+        if (!finitef(c.c2w[k])) return fail(PF_ERR_INVALID_ARGUMENT, "camera c2w not finite");
+    if (!(c.near_plane > 0.0f) || !finitef(c.near_plane))
+        return fail(PF_ERR_INVALID_ARGUMENT, "camera near_plane must be finite and > 0");
+    return PF_OK;
+}
+
+pf::CamParams cam_params(const pf_camera &c)
+{
+    pf::CamParams p;
+    p.W = c.width;
+    p.H = c.height;
+    p.tiles_x = (c.width + pf::kTile - 1) / pf::kTile;
+    p.tiles_y = (c.height + pf::kTile - 1) / pf::kTile;
+    p.fx = c.fx;
+    p.fy = c.fy;
+    p.cx = c.cx;
+    p.cy = c.cy;
+    for (int k = 0; k < 12; ++k) p.M[k] = c.c2w[k];
+    p.near_plane = c.near_plane;
+    return p;
+}
+
+int tile_bits(int T)
+{
+    int b = 0;
+    while ((1 << b) < T) ++b;
+    return b;
+}
+
+int reserve_view_bins(pf_scene *s, pf::ViewState &v)
+{
+    size_t N = (size_t)s->ds.N;
+    PF_CUDA(v.rect.reserve(16 * N));
+    PF_CUDA(v.count.reserve(4 * N));
+    PF_CUDA(v.keybits.reserve(4 * N));
+    PF_CUDA(v.offsets.reserve(4 * N));
+    return PF_OK;
+}
+
+// K3..K5 of one view whose K1/K2 already ran and whose v.P is known.
+// Leaves the sorted keys in *keys_out (scratch) and the sorted values in v.vals.
+int emit_sort_ranges(pf_scene *s, pf::ViewState &v, cudaStream_t st, uint64_t **keys_out)
+{
+    const int64_t P = v.P;
+    const int T = v.cam.tiles_x * v.cam.tiles_y;
+    PF_CUDA(v.ranges.reserve(sizeof(uint2) * (size_t)T));
+    *keys_out = nullptr;
+    if (P == 0) {
+        PF_CUDA(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(uint2) * (size_t)T, st));
+        return PF_OK;
+    }
+    size_t p = (size_t)P;
+    PF_CUDA(s->keys0.reserve(8 * p));
+    PF_CUDA(s->keys1.reserve(8 * p));
+    PF_CUDA(s->vals1.reserve(4 * p));
+    PF_CUDA(v.vals.reserve(4 * p));
+    uint64_t *k0 = s->keys0.as<uint64_t>(), *k1 = s->keys1.as<uint64_t>();
+    uint32_t *v0 = v.vals.as<uint32_t>(), *v1 = s->vals1.as<uint32_t>();
+    PF_CUDA(pf::launch_emit(s, v, k0, v0, st));
+    bool alt = false;
+    PF_CUDA(pf::radix_sort_pairs(s, k0, v0, k1, v1, P, 32 + tile_bits(T), &alt, st));
+    if (alt) PF_CUDA(cudaMemcpyAsync(v0, v1, 4 * p, cudaMemcpyDeviceToDevice, st));
+    uint64_t *ks = alt ? k1 : k0;
+    PF_CUDA(pf::launch_ranges(s, v, ks, st));
+    *keys_out = ks;
+    return PF_OK;
+}
+
+// K1 + K2 for views [0, V) then one readback of all pair totals.
+int bin_views(pf_scene *s, int V, cudaStream_t st)
+{
+    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t) * (size_t)V));
+    int64_t *d_tot = s->scan_totals.as<int64_t>();
+    for (int v = 0; v < V; ++v) {
+        pf::ViewState &vs = s->views[v];
+        int rc = reserve_view_bins(s, vs);
+        if (rc) return rc;
+        PF_CUDA(pf::launch_preprocess(s, vs, st));
+        PF_CUDA(pf::launch_scan_counts(s, vs, d_tot + v, st));
+    }
+    if ((int)s->pinned_n < V) {
+        if (s->pinned) cudaFreeHost(s->pinned);
+        s->pinned = nullptr;
+        s->pinned_n = 0;
+        PF_CUDA(cudaMallocHost(&s->pinned, sizeof(int64_t) * (size_t)(V + 16)));
+        s->pinned_n = V + 16;
+    }
+    PF_CUDA(cudaMemcpyAsync(s->pinned, d_tot, sizeof(int64_t) * (size_t)V,
+                            cudaMemcpyDeviceToHost, st));
+    PF_CUDA(cudaStreamSynchronize(st));
+    for (int v = 0; v < V; ++v) {
+        int64_t P = s->pinned[v];
+        if (P < 0 || P >= (int64_t)0xFFFFFFFFll)
+            return fail(PF_ERR_OUT_OF_MEMORY, "tile/cell pair count exceeds 2^32");
+        s->views[v].P = P;
+    }
+    return PF_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+namespace pf {
+
+cudaError_t DevBuf::reserve(size_t n)
+{
+    if (n <= bytes && ptr) return cudaSuccess;
+    size_t want = n + n / 4 + 256;
+    if (ptr) {
+        cudaError_t e = cudaDeviceSynchronize();  // the old buffer may still be in use
+        if (e != cudaSuccess) return e;
+        cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&ptr, want);
+    if (e != cudaSuccess) {
+        ptr = nullptr;
+        return e;
+    }
+    bytes = want;
+    return cudaSuccess;
+}
+
+void DevBuf::release()
+{
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+}
+
+void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev)
+{
+    *ev = nullptr;
+    if (!s->profiling) return;
+    (void)stage;
+    if (s->event_pool.empty()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        s->event_pool.push_back(e);
+    }
+    *ev = s->event_pool.back();
+    s->event_pool.pop_back();
+    cudaEventRecord(*ev, st);
+}
+
+void stage_end(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t ev)
+{
+    if (!ev) return;
+    cudaEvent_t e2;
+    if (s->event_pool.empty()) {
+        if (cudaEventCreate(&e2) != cudaSuccess) return;
+    } else {
+        e2 = s->event_pool.back();
+        s->event_pool.pop_back();
+    }
+    cudaEventRecord(e2, st);
+    s->events.push_back(StageEvent{stage, ev, e2});
+}
+
+}  // namespace pf
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *pf_last_error(void) { return g_err.c_str(); }
+
+int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
+{
+    if (!out) return fail(PF_ERR_INVALID_ARGUMENT, "out handle pointer is NULL");
+    *out = nullptr;
+    if (!d) return fail(PF_ERR_INVALID_ARGUMENT, "scene descriptor is NULL");
+    if (d->num_cells < 1) return fail(PF_ERR_INVALID_ARGUMENT, "num_cells must be >= 1");
+    if (d->num_cells >= (int64_t)1 << 31)
+        return fail(PF_ERR_INVALID_ARGUMENT, "num_cells must be < 2^31");
+    if (d->num_edges < 0 || d->num_edges >= (int64_t)1 << 32)
+        return fail(PF_ERR_INVALID_ARGUMENT, "num_edges must be in [0, 2^32)");
+    if (!d->sites || !d->weights || !d->radii || !d->density || !d->rgb || !d->nbr_offsets ||
+        (d->num_edges > 0 && !d->nbr_indices))
+        return fail(PF_ERR_INVALID_ARGUMENT, "a scene array pointer is NULL");
+    for (int c = 0; c < 3; ++c)
+        if (!isfinite(d->background[c]))
+            return fail(PF_ERR_INVALID_ARGUMENT, "background not finite");
+    cudaStream_t st = (cudaStream_t)stream;
+    pf_scene *s = new (std::nothrow) pf_scene();
+    if (!s) return fail(PF_ERR_OUT_OF_MEMORY, "host allocation failed");
+    if (cudaGetDevice(&s->device) != cudaSuccess) {
+        delete s;
+        return fail(PF_ERR_CUDA, "no current CUDA device");
+    }
+    s->flags = d->flags;
+    pf::DeviceScene &ds = s->ds;
+    ds.N = d->num_cells;
+    ds.E = d->num_edges;
+    ds.sites = d->sites;
+    ds.weights = d->weights;
+    ds.radii = d->radii;
+    ds.density = d->density;
+    ds.rgb = d->rgb;
+    ds.nbr_off = d->nbr_offsets;
+    ds.nbr_idx = d->nbr_indices;
+    for (int c = 0; c < 3; ++c) ds.bg[c] = d->background[c];
+    int rc = PF_OK;
+    do {
+        size_t N = (size_t)ds.N, E = (size_t)(ds.E > 0 ? ds.E : 1);
+        cudaError_t e;
+        if ((e = s->cellA.reserve(16 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellA"); break; }
+        if ((e = s->cellB.reserve(16 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellB"); break; }
+        if ((e = s->cellE.reserve(8 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellE"); break; }
+        if ((e = s->edges.reserve(16 * E)) != cudaSuccess) { rc = cuda_fail(e, "alloc edges"); break; }
+        ds.cellA = s->cellA.as<float4>();
+        ds.cellB = s->cellB.as<float4>();
+        ds.cellE = s->cellE.as<uint2>();
+        ds.edges = s->edges.as<float4>();
+        if (d->flags & PF_VALIDATE) {
+            int *flag = nullptr;
+            if ((e = cudaMalloc(&flag, sizeof(int))) != cudaSuccess) { rc = cuda_fail(e, "alloc"); break; }
+            int host = 0;
+            e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+            if (e == cudaSuccess) e = pf::launch_validate(s, flag, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            cudaFree(flag);
+            if (e != cudaSuccess) { rc = cuda_fail(e, "validation"); break; }
+            if (host) {
+                std::string why = "scene validation failed:";
+                if (host & 1) why += " non-finite site;";
+                if (host & 2) why += " non-finite rgb;";
+                if (host & 4) why += " non-finite weight;";
+                if (host & 8) why += " radius not finite/positive;";
+                if (host & 16) why += " density not finite/non-negative;";
+                if (host & 32) why += " bad neighbour offsets;";
+                if (host & 64) why += " neighbour index out of range or self loop;";
+                rc = fail(PF_ERR_INVALID_ARGUMENT, why);
+                break;
+            }
+        }
+        if (d->flags & PF_STATIC_SCENE) {
+            if ((e = pf::launch_edge_records(s, st)) != cudaSuccess) { rc = cuda_fail(e, "K0"); break; }
+            s->edges_built = true;
+        }
+    } while (0);
+    if (rc != PF_OK) {
+        pf_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return PF_OK;
+}
+
+int pf_destroy(pf_scene *s)
+{
+    if (!s) return PF_OK;
+    DeviceGuard g(s->device);
+    cudaDeviceSynchronize();
+    s->cellA.release();
+    s->cellB.release();
+    s->cellE.release();
+    s->edges.release();
+    s->keys0.release();
+    s->keys1.release();
+    s->vals1.release();
+    s->sort_hist.release();
+    s->scan_tmp.release();
+    s->scan_totals.release();
+    s->acc.release();
+    for (auto &v : s->views) {
+        v.rect.release();
+        v.count.release();
+        v.keybits.release();
+        v.offsets.release();
+        v.vals.release();
+        v.ranges.release();
+        v.saved.release();
+    }
+    if (s->pinned) cudaFreeHost(s->pinned);
+    for (auto &e : s->events) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    for (auto e : s->event_pool) cudaEventDestroy(e);
+    delete s;
+    return PF_OK;
+}
+
+int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
+                      pf_stream_t stream)
+{
+    if (!s) return fail(PF_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    if (!cams || V < 1) return fail(PF_ERR_INVALID_ARGUMENT, "need >= 1 camera");
+    if (!out) return fail(PF_ERR_INVALID_ARGUMENT, "out is NULL");
+    for (int v = 0; v < V; ++v) {
+        int rc = check_camera(cams[v]);
+        if (rc) return rc;
+        if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+            return fail(PF_ERR_INVALID_ARGUMENT, "all views of one call must share width/height");
+    }
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    s->fwd_views = 0;
+    if (!(s->flags & PF_STATIC_SCENE) || !s->edges_built) {
+        PF_CUDA(pf::launch_edge_records(s, st));
+        s->edges_built = true;
+    }
+    if ((int)s->views.size() < V) s->views.resize(V);
+    for (int v = 0; v < V; ++v) s->views[v].cam = cam_params(cams[v]);
+    int rc = bin_views(s, V, st);
+    if (rc) return rc;
+    const size_t npix = (size_t)cams[0].width * cams[0].height;
+    for (int v = 0; v < V; ++v) {
+        pf::ViewState &vs = s->views[v];
+        uint64_t *ks = nullptr;
+        rc = emit_sort_ranges(s, vs, st, &ks);
+        if (rc) return rc;
+        PF_CUDA(vs.saved.reserve(16 * npix));
+        PF_CUDA(pf::launch_forward(s, vs, out + 4 * npix * (size_t)v, nullptr, st));
+    }
+    s->fwd_cams.assign(cams, cams + V);
+    s->fwd_views = V;
+    return PF_OK;
+}
+
+int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t V, const float *grad_out,
+                       float *grad_sites, float *grad_weights, float *grad_radii,
+                       float *grad_density, float *grad_rgb, pf_stream_t stream)
+{
+    if (!s) return fail(PF_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    if (!cams || V < 1 || !grad_out)
+        return fail(PF_ERR_INVALID_ARGUMENT, "need cameras and grad_out");
+    if (!grad_sites || !grad_weights || !grad_radii || !grad_density || !grad_rgb)
+        return fail(PF_ERR_INVALID_ARGUMENT, "a gradient array pointer is NULL");
+    if (V != s->fwd_views || (int)s->fwd_cams.size() < V ||
+        memcmp(cams, s->fwd_cams.data(), sizeof(pf_camera) * (size_t)V) != 0)
+        return fail(PF_ERR_STATE, "backward needs the immediately preceding forward with the same cameras");
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)s->ds.N;
+    PF_CUDA(s->acc.reserve(N * (16 + 16 + 4)));
+    PF_CUDA(cudaMemsetAsync(s->acc.ptr, 0, N * (16 + 16 + 4), st));
+    const size_t npix = (size_t)cams[0].width * cams[0].height;
+    for (int v = 0; v < V; ++v) {
+        pf::ViewState &vs = s->views[v];
+        if (vs.P == 0) continue;
+        PF_CUDA(pf::launch_backward(s, vs, grad_out + 4 * npix * (size_t)v, st));
+    }
+    PF_CUDA(pf::launch_unpack(s, grad_sites, grad_weights, grad_radii, grad_density, grad_rgb, st));
+    return PF_OK;
+}
+
+int pf_debug_binning(pf_scene *s, const pf_camera *cam, int32_t *rect, int32_t *count,
+                     uint32_t *keybits, uint64_t *keys, uint32_t *vals, uint32_t *ranges,
+                     int64_t *num_pairs, pf_stream_t stream)
+{
+    if (!s || !cam || !num_pairs) return fail(PF_ERR_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_camera(*cam);
+    if (rc) return rc;
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    // use a dedicated view slot so the forward's saved state is untouched
+    pf::ViewState &vs = s->debug_view;
+    vs.cam = cam_params(*cam);
+    int64_t *d_tot;
+    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t)));
+    d_tot = s->scan_totals.as<int64_t>();
+    rc = reserve_view_bins(s, vs);
+    if (rc) return rc;
+    PF_CUDA(pf::launch_preprocess(s, vs, st));
+    PF_CUDA(pf::launch_scan_counts(s, vs, d_tot, st));
+    int64_t P = 0;
+    PF_CUDA(cudaMemcpyAsync(&P, d_tot, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PF_CUDA(cudaStreamSynchronize(st));
+    vs.P = P;
+    *num_pairs = P;
+    const size_t N = (size_t)s->ds.N;
+    if (rect) PF_CUDA(cudaMemcpyAsync(rect, vs.rect.ptr, 16 * N, cudaMemcpyDeviceToDevice, st));
+    if (count) PF_CUDA(cudaMemcpyAsync(count, vs.count.ptr, 4 * N, cudaMemcpyDeviceToDevice, st));
+    if (keybits) PF_CUDA(cudaMemcpyAsync(keybits, vs.keybits.ptr, 4 * N, cudaMemcpyDeviceToDevice, st));
+    if (keys) {
+        uint64_t *ks = nullptr;
+        rc = emit_sort_ranges(s, vs, st, &ks);
+        if (rc) return rc;
+        if (P > 0) {
+            PF_CUDA(cudaMemcpyAsync(keys, ks, 8 * (size_t)P, cudaMemcpyDeviceToDevice, st));
+            if (vals) PF_CUDA(cudaMemcpyAsync(vals, vs.vals.ptr, 4 * (size_t)P, cudaMemcpyDeviceToDevice, st));
+        }
+        if (ranges)
+            PF_CUDA(cudaMemcpyAsync(ranges, vs.ranges.ptr,
+                                    sizeof(uint2) * (size_t)vs.cam.tiles_x * vs.cam.tiles_y,
+                                    cudaMemcpyDeviceToDevice, st));
+    }
+    PF_CUDA(cudaStreamSynchronize(st));
+    return PF_OK;
+}
+
+int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_stream_t stream)
+{
+    if (!s || !cam || !counters) return fail(PF_ERR_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_camera(*cam);
+    if (rc) return rc;
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!(s->flags & PF_STATIC_SCENE) || !s->edges_built) {
+        PF_CUDA(pf::launch_edge_records(s, st));
+        s->edges_built = true;
+    }
+    pf::ViewState &vs = s->debug_view;
+    vs.cam = cam_params(*cam);
+    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t)));
+    int64_t *d_tot = s->scan_totals.as<int64_t>();
+    rc = reserve_view_bins(s, vs);
+    if (rc) return rc;
+    PF_CUDA(pf::launch_preprocess(s, vs, st));
+    PF_CUDA(pf::launch_scan_counts(s, vs, d_tot, st));
+    int64_t P = 0;
+    PF_CUDA(cudaMemcpyAsync(&P, d_tot, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PF_CUDA(cudaStreamSynchronize(st));
+    vs.P = P;
+    uint64_t *ks;
+    rc = emit_sort_ranges(s, vs, st, &ks);
+    if (rc) return rc;
+    PF_CUDA(cudaMemsetAsync(counters, 0, 32 * (size_t)cam->width * cam->height, st));
+    PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, st));
+    PF_CUDA(cudaStreamSynchronize(st));
+    return PF_OK;
+}
+
+int64_t pf_launch_count(const pf_scene *s) { return s ? s->launches : -1; }
+
+int pf_set_profiling(pf_scene *s, int enable)
+{
+    if (!s) return fail(PF_ERR_INVALID_ARGUMENT, "NULL handle");
+    s->profiling = enable != 0;
+    return PF_OK;
+}
+
+int pf_stage_times(pf_scene *s, double *ms, int64_t *launches)
+{
+    if (!s || !ms) return fail(PF_ERR_INVALID_ARGUMENT, "NULL argument");
+    DeviceGuard g(s->device);
+    for (int k = 0; k < PF_NUM_STAGES; ++k) {
+        ms[k] = 0.0;
+        if (launches) launches[k] = 0;
+    }
+    for (auto &e : s->events) {
+        PF_CUDA(cudaEventSynchronize(e.b));
+        float t = 0.0f;
+        PF_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
+        if (e.stage >= 0 && e.stage < PF_NUM_STAGES) {
+            ms[e.stage] += t;
+            if (launches) launches[e.stage] += 1;
+        }
+        s->event_pool.push_back(e.a);
+        s->event_pool.push_back(e.b);
+    }
+    s->events.clear();
+    return PF_OK;
+}
+
+int pf_last_pair_counts(const pf_scene *s, int64_t *pairs, int32_t V)
+{
+    if (!s || !pairs) return fail(PF_ERR_INVALID_ARGUMENT, "NULL argument");
+    for (int v = 0; v < V; ++v) pairs[v] = v < (int)s->views.size() ? s->views[v].P : 0;
+    return PF_OK;
+}
+
+}  // extern "C"

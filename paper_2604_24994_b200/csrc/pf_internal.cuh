@@ -1,0 +1,115 @@
+// pf_internal.cuh -- internal declarations of libpowerfoam (B200 / sm_100a).
+// Nothing here is shared with oracle/ (the CPU oracle is independent code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/powerfoam.h"
+
+namespace pf {
+
+constexpr int kTile = 16;           // 16x16-pixel tiles
+constexpr int kTilePix = kTile * kTile;
+constexpr float kTStop = 1e-4f;     // early termination threshold
+
+// Per-view camera constants handed to kernels by value.
+struct CamParams {
+    int W, H, tiles_x, tiles_y;
+    float fx, fy, cx, cy;
+    float M[12];     // c2w row-major
+    float near_plane;
+};
+
+// Device-side records built by K0 from the caller's arrays.
+//   cellA[i] = (p.x, p.y, p.z, r)      cellB[i] = (sigma, R, G, B)
+//   cellE[i] = (first edge, degree)    edges[q] = (n.x, n.y, n.z, k)
+// with n = p_j - p_i and k = 0.5 * (|n|^2 - (w_j - w_i)) for edge q = (i -> j):
+// the bounded cell of i keeps the side  a t' <= k + n.e  of the radical plane,
+// a = d.n, in the cell-local ray frame (P:577-585 with the
+// weight sign of SURVEY C1).
+struct DeviceScene {
+    int64_t N = 0, E = 0;
+    const float *sites = nullptr, *weights = nullptr, *radii = nullptr, *density = nullptr,
+                *rgb = nullptr;
+    const int64_t *nbr_off = nullptr;
+    const int32_t *nbr_idx = nullptr;
+    float bg[3] = {0, 0, 0};
+    float4 *cellA = nullptr, *cellB = nullptr, *edges = nullptr;
+    uint2 *cellE = nullptr;
+};
+
+// grow-only device buffer
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t reserve(size_t n);
+    void release();
+    template <class T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+struct ViewState {
+    CamParams cam{};
+    int64_t P = 0;
+    DevBuf rect, count, keybits, offsets;   // binning of this view (N-sized)
+    DevBuf vals, ranges;                     // sorted cell ids, per-tile [start,end)
+    DevBuf saved;                            // float4[H*W] final (C + T bg, T)
+};
+
+struct StageEvent {
+    int stage;
+    cudaEvent_t a, b;
+};
+
+}  // namespace pf
+
+struct pf_scene {
+    int device = 0;
+    uint32_t flags = 0;
+    pf::DeviceScene ds;
+    pf::DevBuf cellA, cellB, cellE, edges;
+    bool edges_built = false;
+    // sort / emit scratch
+    pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
+    pf::DevBuf acc;                 // backward packed accumulators
+    std::vector<pf::ViewState> views;
+    pf::ViewState debug_view;       // pf_debug_* scratch (leaves the forward state intact)
+    std::vector<pf_camera> fwd_cams;
+    int32_t fwd_views = 0;          // views saved by the last forward
+    int64_t *pinned = nullptr;      // pinned host readback of pair totals
+    int pinned_n = 0;
+    int64_t launches = 0;
+    bool profiling = false;
+    std::vector<pf::StageEvent> events;
+    std::vector<cudaEvent_t> event_pool;
+};
+
+namespace pf {
+
+// ---- launch wrappers (defined in the .cu files); return cudaGetLastError() ----
+cudaError_t launch_edge_records(pf_scene *s, cudaStream_t st);
+cudaError_t launch_validate(pf_scene *s, int *d_flag, cudaStream_t st);
+cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st);
+cudaError_t launch_scan_counts(pf_scene *s, ViewState &v, int64_t *d_total, cudaStream_t st);
+cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
+                        cudaStream_t st);
+cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+                             uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
+                             cudaStream_t st);
+cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaStream_t st);
+cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
+                           cudaStream_t st);
+cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
+cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
+                          cudaStream_t st);
+
+// stage timing helpers (pf_api.cu)
+void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev);
+void stage_end(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t ev);
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace pf

@@ -1,0 +1,387 @@
+// pf_prep.cu -- K0 edge records, scene validation, K1 projection + tile binning +
+// sort key, K2 scan of the per-cell pair counts, K3 pair emission, K5 tile ranges.
+//
+// K1 is an fp32 SPECIFICATION: it produces
+// integers (tile rectangles, key bits) that must be bit-identical to the CPU
+// oracle, so every operation is an explicit IEEE round-to-nearest intrinsic
+// evaluated left to right with no FMA contraction.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+
+// ------------------------------------------------------------------------
+// K0: cell and edge records
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k0_edge_records(DeviceScene ds)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ds.N) return;
+    float px = ds.sites[3 * i], py = ds.sites[3 * i + 1], pz = ds.sites[3 * i + 2];
+    float wi = ds.weights[i];
+    int64_t b = ds.nbr_off[i], e = ds.nbr_off[i + 1];
+    ds.cellA[i] = make_float4(px, py, pz, ds.radii[i]);
+    ds.cellB[i] = make_float4(ds.density[i], ds.rgb[3 * i], ds.rgb[3 * i + 1], ds.rgb[3 * i + 2]);
+    ds.cellE[i] = make_uint2((uint32_t)b, (uint32_t)(e - b));
+    for (int64_t q = b; q < e; ++q) {
+        int j = ds.nbr_idx[q];
+        float nx = ds.sites[3 * j] - px, ny = ds.sites[3 * j + 1] - py,
+              nz = ds.sites[3 * j + 2] - pz;
+        float nn = nx * nx + ny * ny + nz * nz;
+        // pow(x,i) <= pow(x,j)  <=>  (x - p_i).n <= 0.5 (|n|^2 - (w_j - w_i))
+        float k = 0.5f * (nn - (ds.weights[j] - wi));
+        ds.edges[q] = make_float4(nx, ny, nz, k);
+    }
+}
+
+cudaError_t launch_edge_records(pf_scene *s, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 0, st, &ev);
+    k0_edge_records<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(s->ds);
+    ++s->launches;
+    stage_end(s, 0, st, ev);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------
+// validation (PF_VALIDATE)
+// ------------------------------------------------------------------------
+__global__ void k_validate(DeviceScene ds, int *flag)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ds.N) return;
+    int bad = 0;
+    for (int m = 0; m < 3; ++m) {
+        bad |= !isfinite(ds.sites[3 * i + m]) ? 1 : 0;
+        bad |= !isfinite(ds.rgb[3 * i + m]) ? 2 : 0;
+    }
+    bad |= !isfinite(ds.weights[i]) ? 4 : 0;
+    bad |= !(ds.radii[i] > 0.0f) || !isfinite(ds.radii[i]) ? 8 : 0;
+    bad |= !(ds.density[i] >= 0.0f) || !isfinite(ds.density[i]) ? 16 : 0;
+    int64_t b = ds.nbr_off[i], e = ds.nbr_off[i + 1];
+    if (b < 0 || e < b || e > ds.E) bad |= 32;
+    else
+        for (int64_t q = b; q < e; ++q) {
+            int j = ds.nbr_idx[q];
+            if (j < 0 || j >= ds.N || j == i) bad |= 64;
+        }
+    if (bad) atomicOr(flag, bad);
+}
+
+cudaError_t launch_validate(pf_scene *s, int *d_flag, cudaStream_t st)
+{
+    k_validate<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(s->ds, d_flag);
+    ++s->launches;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------
+// K1: project the bounding sphere, tile rectangle, count, key bits
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t order_bits(float K)
+{
+    uint32_t u = __float_as_uint(K);
+    return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+
+// Extent of the sphere's image along one axis (a = camera coordinate along the
+// axis, z = depth), in pixels.  Sphere in front of the near plane: the two
+// tangent planes through the camera centre; straddling: the box
+// [a-r, a+r] x [near, z+r].
+__device__ __forceinline__ void sphere_extent(float a, float z, float r, float f, float c,
+                                              float nearp, bool in_front, float &lo, float &hi)
+{
+    float ulo, uhi;
+    if (in_front) {
+        float q = __fsqrt_rn(__fsub_rn(__fadd_rn(__fmul_rn(a, a), __fmul_rn(z, z)),
+                                       __fmul_rn(r, r)));
+        float den = __fmul_rn(__fsub_rn(z, r), __fadd_rn(z, r));
+        float az = __fmul_rn(a, z), rq = __fmul_rn(r, q);
+        ulo = __fdiv_rn(__fsub_rn(az, rq), den);
+        uhi = __fdiv_rn(__fadd_rn(az, rq), den);
+    } else {
+        float amin = __fsub_rn(a, r), amax = __fadd_rn(a, r);
+        float zfar = __fadd_rn(z, r);
+        ulo = __fdiv_rn(amin, amin >= 0.0f ? zfar : nearp);
+        uhi = __fdiv_rn(amax, amax >= 0.0f ? nearp : zfar);
+    }
+    lo = __fadd_rn(__fmul_rn(f, ulo), c);
+    hi = __fadd_rn(__fmul_rn(f, uhi), c);
+}
+
+__device__ __forceinline__ int tile_lo(float px, int ntiles)
+{
+    float t = floorf(__fmul_rn(__fsub_rn(px, 1.0f), 0.0625f));
+    return (int)fminf(fmaxf(t, 0.0f), (float)ntiles);
+}
+__device__ __forceinline__ int tile_hi(float px, int ntiles)
+{
+    float t = __fadd_rn(floorf(__fmul_rn(__fadd_rn(px, 1.0f), 0.0625f)), 1.0f);
+    return (int)fminf(fmaxf(t, 0.0f), (float)ntiles);
+}
+
+__global__ void __launch_bounds__(256)
+k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights,
+              const float *__restrict__ radii, int64_t N, CamParams cam, int4 *__restrict__ rect,
+              int *__restrict__ count, uint32_t *__restrict__ keybits)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const float *M = cam.M;
+    float v0 = __fsub_rn(sites[3 * i + 0], M[3]);
+    float v1 = __fsub_rn(sites[3 * i + 1], M[7]);
+    float v2 = __fsub_rn(sites[3 * i + 2], M[11]);
+    // camera coordinates: c_k = (R_0k v0 + R_1k v1) + R_2k v2
+    float ca = __fadd_rn(__fadd_rn(__fmul_rn(M[0], v0), __fmul_rn(M[4], v1)), __fmul_rn(M[8], v2));
+    float cb = __fadd_rn(__fadd_rn(__fmul_rn(M[1], v0), __fmul_rn(M[5], v1)), __fmul_rn(M[9], v2));
+    float cz = __fadd_rn(__fadd_rn(__fmul_rn(M[2], v0), __fmul_rn(M[6], v1)), __fmul_rn(M[10], v2));
+    // sort key K_i = pow(Q, p_i) = |p_i - Q|^2 - w_i   (Theorem 2)
+    float K = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)),
+                                  __fmul_rn(v2, v2)),
+                        weights[i]);
+    float r = radii[i];
+    keybits[i] = order_bits(K);
+    int4 rc = make_int4(0, 0, 0, 0);
+    int cnt = 0;
+    if ((__fadd_rn(cz, r) > cam.near_plane) && (r > 0.0f)) {
+        bool in_front = __fsub_rn(cz, r) > cam.near_plane;
+        float xlo, xhi, ylo, yhi;
+        sphere_extent(ca, cz, r, cam.fx, cam.cx, cam.near_plane, in_front, xlo, xhi);
+        sphere_extent(cb, cz, r, cam.fy, cam.cy, cam.near_plane, in_front, ylo, yhi);
+        int tx0 = tile_lo(xlo, cam.tiles_x), tx1 = tile_hi(xhi, cam.tiles_x);
+        int ty0 = tile_lo(ylo, cam.tiles_y), ty1 = tile_hi(yhi, cam.tiles_y);
+        if (tx1 > tx0 && ty1 > ty0) {
+            rc = make_int4(tx0, ty0, tx1, ty1);
+            cnt = (tx1 - tx0) * (ty1 - ty0);
+        }
+    }
+    rect[i] = rc;
+    count[i] = cnt;
+}
+
+cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 1, st, &ev);
+    k1_preprocess<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
+        s->ds.sites, s->ds.weights, s->ds.radii, s->ds.N, v.cam, v.rect.as<int4>(),
+        v.count.as<int>(), v.keybits.as<uint32_t>());
+    ++s->launches;
+    stage_end(s, 1, st, ev);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------
+// K2: exclusive scan of the counts (3 phases: block sums, scan of sums, rescan)
+// ------------------------------------------------------------------------
+constexpr int kScanThreads = 256, kScanItems = 16, kScanChunk = kScanThreads * kScanItems;
+
+template <class T> __device__ __forceinline__ T warp_incl_scan(T v)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+// exclusive block scan of one value per thread; returns the block total in *total
+template <class T> __device__ __forceinline__ T block_excl_scan(T v, T *smem_warp, T *total)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T inc = warp_incl_scan(v);
+    if (lane == 31) smem_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        T w = lane < nw ? smem_warp[lane] : T(0);
+        T wi = warp_incl_scan(w);
+        if (lane < nw) smem_warp[lane] = wi - w;
+        if (lane == nw - 1) smem_warp[32] = wi;
+    }
+    __syncthreads();
+    T res = inc - v + smem_warp[warp];
+    *total = smem_warp[32];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k2_block_sums(const int *__restrict__ cnt, int64_t n,
+                                                             long long *__restrict__ sums)
+{
+    __shared__ long long sw[33];
+    int64_t base = (int64_t)blockIdx.x * kScanChunk;
+    long long acc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t idx = base + (int64_t)k * kScanThreads + threadIdx.x;
+        if (idx < n) acc += cnt[idx];
+    }
+    long long tot;
+    block_excl_scan<long long>(acc, sw, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// single block: exclusive scan of nb block sums in place, total -> *total
+__global__ void __launch_bounds__(1024) k2_scan_sums(long long *sums, int nb, long long *total)
+{
+    __shared__ long long sw[33];
+    long long carry = 0;
+    for (int base = 0; base < nb; base += 1024) {
+        int i = base + threadIdx.x;
+        long long v = i < nb ? sums[i] : 0;
+        long long tot;
+        long long ex = block_excl_scan<long long>(v, sw, &tot);
+        if (i < nb) sums[i] = ex + carry;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k2_rescan(const int *__restrict__ cnt, int64_t n, const long long *__restrict__ sums,
+          uint32_t *__restrict__ offs)
+{
+    __shared__ long long sw[33];
+    __shared__ int tile[kScanChunk];
+    int64_t base = (int64_t)blockIdx.x * kScanChunk;
+    // coalesced load into smem, then each thread scans a contiguous run of items
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t idx = base + (int64_t)k * kScanThreads + threadIdx.x;
+        tile[k * kScanThreads + threadIdx.x] = idx < n ? cnt[idx] : 0;
+    }
+    __syncthreads();
+    long long run = 0;
+    int v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = tile[threadIdx.x * kScanItems + k];
+        run += v[k];
+    }
+    long long tot;
+    long long ex = block_excl_scan<long long>(run, sw, &tot) + sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        tile[threadIdx.x * kScanItems + k] = (int)(uint32_t)ex;  // low 32 bits (P < 2^32)
+        ex += v[k];
+    }
+    __syncthreads();
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t idx = base + (int64_t)k * kScanThreads + threadIdx.x;
+        if (idx < n) offs[idx] = (uint32_t)tile[k * kScanThreads + threadIdx.x];
+    }
+}
+
+cudaError_t exclusive_scan_counts(pf_scene *s, const int *cnt, int64_t n, uint32_t *offs,
+                                  long long *d_total, cudaStream_t st)
+{
+    int nb = ceil_div(n, kScanChunk);
+    cudaError_t err = s->scan_tmp.reserve(sizeof(long long) * (size_t)(nb + 1));
+    if (err != cudaSuccess) return err;
+    long long *sums = s->scan_tmp.as<long long>();
+    k2_block_sums<<<nb, kScanThreads, 0, st>>>(cnt, n, sums);
+    k2_scan_sums<<<1, 1024, 0, st>>>(sums, nb, d_total);
+    k2_rescan<<<nb, kScanThreads, 0, st>>>(cnt, n, sums, offs);
+    s->launches += 3;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_counts(pf_scene *s, ViewState &v, int64_t *d_total, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 2, st, &ev);
+    cudaError_t err = exclusive_scan_counts(s, v.count.as<int>(), s->ds.N,
+                                            v.offsets.as<uint32_t>(), (long long *)d_total, st);
+    stage_end(s, 2, st, ev);
+    return err;
+}
+
+// ------------------------------------------------------------------------
+// K3: emit (tile << 32 | keybits, cell) pairs -- one warp per 32 cells, the
+// warp writes each cell's pairs cooperatively (coalesced, big rects balanced)
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__restrict__ count,
+        const uint32_t *__restrict__ keybits, const uint32_t *__restrict__ offs,
+        unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals)
+{
+    const int lane = threadIdx.x & 31;
+    int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
+    int64_t i = i0 + lane;
+    int cnt = 0;
+    int4 rc = make_int4(0, 0, 0, 0);
+    uint32_t kb = 0, off = 0;
+    if (i < N) {
+        cnt = count[i];
+        if (cnt) {
+            rc = rect[i];
+            kb = keybits[i];
+            off = offs[i];
+        }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);
+    while (todo) {
+        int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        int c = __shfl_sync(0xffffffffu, cnt, src);
+        int x0 = __shfl_sync(0xffffffffu, rc.x, src);
+        int y0 = __shfl_sync(0xffffffffu, rc.y, src);
+        int w = __shfl_sync(0xffffffffu, rc.z, src) - x0;
+        uint32_t k = __shfl_sync(0xffffffffu, kb, src);
+        uint32_t o = __shfl_sync(0xffffffffu, off, src);
+        uint32_t cell = (uint32_t)(i0 + src);
+        for (int q = lane; q < c; q += 32) {
+            int dy = q / w, dx = q - dy * w;
+            unsigned long long tile = (unsigned long long)((y0 + dy) * tiles_x + (x0 + dx));
+            keys[o + q] = (tile << 32) | k;
+            vals[o + q] = cell;
+        }
+    }
+}
+
+cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
+                        cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 3, st, &ev);
+    k3_emit<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
+        s->ds.N, v.cam.tiles_x, v.rect.as<int4>(), v.count.as<int>(), v.keybits.as<uint32_t>(),
+        v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals);
+    ++s->launches;
+    stage_end(s, 3, st, ev);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------
+// K5: per-tile ranges [start, end) of the sorted pairs ((0,0) for empty tiles)
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k5_ranges(const unsigned long long *__restrict__ keys,
+                                                 int64_t P, uint2 *__restrict__ ranges)
+{
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P) return;
+    uint32_t t = (uint32_t)(keys[q] >> 32);
+    if (q == 0 || (uint32_t)(keys[q - 1] >> 32) != t) ranges[t].x = (uint32_t)q;
+    if (q == P - 1 || (uint32_t)(keys[q + 1] >> 32) != t) ranges[t].y = (uint32_t)(q + 1);
+}
+
+cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaStream_t st)
+{
+    int T = v.cam.tiles_x * v.cam.tiles_y;
+    cudaError_t err = cudaMemsetAsync(v.ranges.ptr, 0, sizeof(uint2) * (size_t)T, st);
+    if (err != cudaSuccess) return err;
+    if (v.P == 0) return cudaSuccess;
+    cudaEvent_t ev;
+    stage_begin(s, 5, st, &ev);
+    k5_ranges<<<ceil_div(v.P, 256), 256, 0, st>>>((const unsigned long long *)keys, v.P,
+                                                   v.ranges.as<uint2>());
+    ++s->launches;
+    stage_end(s, 5, st, ev);
+    return cudaGetLastError();
+}
+
+}  // namespace pf

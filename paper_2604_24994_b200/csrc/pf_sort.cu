@@ -1,0 +1,142 @@
+// pf_sort.cu -- K4: stable LSD radix sort of (u64 key, u32 value) pairs, 8-bit
+// digits, only over the significant low `end_bit` bits (32 key bits + the tile
+// bits, "global sort ... similar to 3DGS").
+//
+// Per pass:  (1) per-block digit histograms (digit-major [256][nblocks]),
+//            (2) exclusive scan of that array (the K2 scan kernels),
+//            (3) stable scatter: warp-level multisplit ranking with
+//                __match_any_sync, per-warp digit counters in shared memory,
+//                block prefix over warps, global base from the scan.
+// Stability: warp w of block b owns keys [b*4096 + w*512, +512) in 16 rounds of
+// 32 consecutive keys; ranks follow (round, lane) = input order.
+#include <cuda_runtime.h>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+
+cudaError_t exclusive_scan_counts(pf_scene *s, const int *cnt, int64_t n, uint32_t *offs,
+                                  long long *d_total, cudaStream_t st);
+
+constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems;
+constexpr int kRadixBits = 8, kRadix = 1 << kRadixBits;
+
+__global__ void __launch_bounds__(kSortThreads)
+k4_histogram(const unsigned long long *__restrict__ keys, int64_t n, int shift, int nb,
+             int *__restrict__ hist)
+{
+    __shared__ int h[8][kRadix];
+    const int warp = threadIdx.x >> 5;
+    for (int q = threadIdx.x; q < 8 * kRadix; q += kSortThreads) (&h[0][0])[q] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+    for (int k = 0; k < kSortItems; ++k) {
+        int64_t idx = base + (int64_t)k * kSortThreads + threadIdx.x;
+        if (idx < n) {
+            int d = (int)((keys[idx] >> shift) & (kRadix - 1));
+            atomicAdd(&h[warp][d], 1);
+        }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += h[w][d];
+        hist[(int64_t)d * nb + blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restrict__ vin,
+           unsigned long long *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
+           int shift, int nb, const uint32_t *__restrict__ digit_offs)
+{
+    __shared__ uint32_t wh[8][kRadix];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int q = threadIdx.x; q < 8 * kRadix; q += kSortThreads) (&wh[0][0])[q] = 0;
+    __syncthreads();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (32 * kSortItems);
+    unsigned long long key[kSortItems];
+    uint32_t val[kSortItems], rank[kSortItems];
+    int dig[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        int64_t idx = wbase + r * 32 + lane;
+        bool valid = idx < n;
+        key[r] = valid ? kin[idx] : 0ull;
+        val[r] = valid ? vin[idx] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        int64_t idx = wbase + r * 32 + lane;
+        bool valid = idx < n;
+        int d = valid ? (int)((key[r] >> shift) & (kRadix - 1)) : kRadix;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        uint32_t before = valid ? wh[warp][d] : 0u;
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wh[warp][d] = before + __popc(peers);
+        __syncwarp();
+        rank[r] = before + __popc(peers & lt_mask);
+        dig[r] = d;
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+        uint32_t run = digit_offs[(int64_t)d * nb + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t c = wh[w][d];
+            wh[w][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        if (dig[r] < kRadix) {
+            uint32_t pos = wh[warp][dig[r]] + rank[r];
+            kout[pos] = key[r];
+            vout[pos] = val[r];
+        }
+    }
+}
+
+cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+                             uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
+                             cudaStream_t st)
+{
+    *result_in_alt = false;
+    if (n <= 1) return cudaSuccess;
+    int nb = ceil_div(n, kSortTile);
+    size_t hist_n = (size_t)kRadix * nb;
+    cudaError_t err = s->sort_hist.reserve(hist_n * (sizeof(int) + sizeof(uint32_t)) + 64);
+    if (err != cudaSuccess) return err;
+    int *hist = s->sort_hist.as<int>();
+    uint32_t *offs = reinterpret_cast<uint32_t *>(hist + hist_n);
+    long long *dummy_total = reinterpret_cast<long long *>(
+        (reinterpret_cast<uintptr_t>(offs + hist_n) + 15) & ~uintptr_t(15));
+    unsigned long long *ka = (unsigned long long *)keys, *kb = (unsigned long long *)keys_alt;
+    uint32_t *va = vals, *vb = vals_alt;
+    bool alt = false;
+    cudaEvent_t ev;
+    stage_begin(s, 4, st, &ev);
+    for (int shift = 0; shift < end_bit; shift += kRadixBits) {
+        k4_histogram<<<nb, kSortThreads, 0, st>>>(ka, n, shift, nb, hist);
+        ++s->launches;
+        err = exclusive_scan_counts(s, hist, (int64_t)hist_n, offs, dummy_total, st);
+        if (err != cudaSuccess) return err;
+        k4_scatter<<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, nb, offs);
+        ++s->launches;
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+        unsigned long long *tk = ka; ka = kb; kb = tk;
+        uint32_t *tv = va; va = vb; vb = tv;
+        alt = !alt;
+    }
+    stage_end(s, 4, st, ev);
+    *result_in_alt = alt;
+    return cudaGetLastError();
+}
+
+}  // namespace pf

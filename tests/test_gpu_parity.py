@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C-ABI library) against the CPU oracle on
+the same seeded inputs.  Bars (BASELINE.json north_star):
+binning bit-exact; images <= 1e-4 abs per fp32 channel; gradients <= 1e-3
+relative (normwise per array)."""
+import numpy as np
+import pytest
+
+import oracle
+import pf_synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+_cache = {}
+
+
+def case(name, variant=None):
+    key = (name, variant)
+    if key not in _cache:
+        if name == "tiny":
+            sc = pf_synth.make_scene("tiny")
+            cams = pf_synth.make_cameras("tiny", variant=variant or "outside")
+        elif name == "tiny_knn8":
+            sc = pf_synth.make_scene("tiny", variant="knn8")
+            cams = pf_synth.make_cameras("tiny")
+        elif name == "tiny_w0":
+            sc = pf_synth.make_scene("tiny", variant="allpairs_w0")
+            cams = pf_synth.make_cameras("tiny")
+        elif name == "small":
+            sc = pf_synth.make_scene("small")
+            cams = pf_synth.make_cameras("small")
+        elif name == "small360":
+            sc = pf_synth.make_scene("small360")
+            cams = pf_synth.make_cameras("small360", n=4)
+        elif name == "nerfsynth200k":
+            sc = pf_synth.make_scene("nerfsynth200k")
+            cams = pf_synth.make_cameras("nerfsynth200k")
+        elif name == "train8_1m":
+            sc = pf_synth.make_scene("train8_1m")
+            cams = pf_synth.make_cameras("train8_1m")
+        else:
+            raise KeyError(name)
+        _cache[key] = (sc, cams)
+    return _cache[key]
+
+
+def renderer(sc, flags=None):
+    import paper_2604_24994_b200 as pf
+    return pf.Renderer.from_scene(sc, "cuda", flags=pf.PF_VALIDATE if flags is None else flags)
+
+
+def grad_check(gpu, ref, tol=GRAD_TOL):
+    msgs = []
+    for k in ("sites", "weights", "radii", "density", "rgb"):
+        a = gpu[k].detach().cpu().numpy().astype(np.float64).reshape(-1)
+        b = ref[k].reshape(-1)
+        nb = np.linalg.norm(b)
+        rel = np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
+        msgs.append(f"{k}: {rel:.2e}")
+        assert rel <= tol, ", ".join(msgs)
+    return msgs
+
+
+# --------------------------------------------------------------- binning
+
+@pytest.mark.parametrize("name,variant", [("tiny", "outside"), ("tiny", "inside"),
+                                          ("small", None), ("small360", None),
+                                          ("nerfsynth200k", None), ("train8_1m", None)])
+def test_binning_bit_exact(name, variant):
+    sc, cams = case(name, variant)
+    r = renderer(sc)
+    for cam in cams[:2]:
+        g = r.debug_binning(cam)
+        o = oracle.binning(sc, cam)
+        assert np.array_equal(g["rect"].cpu().numpy(), o["rect"])
+        assert np.array_equal(g["count"].cpu().numpy(), o["count"])
+        assert np.array_equal(g["keybits"].cpu().numpy().view(np.uint32), o["keybits"])
+        assert g["P"] == o["P"]
+        assert np.array_equal(g["keys"].cpu().numpy().view(np.uint64), o["keys"])
+        assert np.array_equal(g["vals"].cpu().numpy().view(np.uint32), o["vals"])
+        assert np.array_equal(g["ranges"].cpu().numpy().view(np.uint32), o["ranges"])
+    r.close()
+
+
+# --------------------------------------------------------------- forward
+
+@pytest.mark.parametrize("name,variant", [("tiny", "outside"), ("tiny", "inside"),
+                                          ("tiny_knn8", None), ("tiny_w0", None),
+                                          ("small", None), ("small360", None)])
+def test_forward_full_image(name, variant):
+    sc, cams = case(name, variant)
+    r = renderer(sc)
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    for v, cam in enumerate(cams):
+        mode = oracle.O1 if name.startswith("tiny") else oracle.O3
+        ref = oracle.render(sc, cam, mode=mode)["out"]
+        err = np.abs(out[v] - ref)
+        assert err.max() <= IMG_TOL, (v, err.max())
+    r.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small360"])
+def test_forward_counters_match_oracle(name):
+    sc, cams = case(name)
+    r = renderer(sc)
+    cam = cams[0]
+    g = r.debug_counters(cam).cpu().numpy().reshape(-1, 4)
+    o = oracle.render(sc, cam, mode=oracle.O3, counters=True)["counters"]
+    mism = np.any(g != o, axis=1).mean()
+    assert mism <= 1e-3, mism
+    assert abs(g.sum(0) - o.sum(0)).max() <= 1e-3 * o.sum(0).max()
+    r.close()
+
+
+@pytest.mark.parametrize("name", ["nerfsynth200k", "train8_1m"])
+def test_forward_large_sampled_pixels(name):
+    """Full BASELINE sizes, all views in one call (the bench launch configuration);
+    oracle on sampled pixels (O3 tile lists, plus O1 all-pairs on a few)."""
+    sc, cams = case(name)
+    r = renderer(sc, flags=0)
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(0)
+    for v in (0, len(cams) - 1):
+        cam = cams[v]
+        pix = np.stack([rng.integers(0, cam.width, 3000), rng.integers(0, cam.height, 3000)], 1)
+        ref = oracle.render(sc, cam, mode=oracle.O3, pixels=pix)["out"]
+        got = out[v][pix[:, 1], pix[:, 0]]
+        assert np.abs(got - ref).max() <= IMG_TOL
+        few = pix[:24]
+        ref1 = oracle.render(sc, cam, mode=oracle.O1, pixels=few)["out"]
+        assert np.abs(out[v][few[:, 1], few[:, 0]] - ref1).max() <= IMG_TOL
+    assert np.isfinite(out).all()
+    r.close()
+
+
+def test_multiview_equals_single_view_and_deterministic():
+    sc, cams = case("small360")
+    r = renderer(sc)
+    multi = r.forward(cams).cpu().numpy()
+    again = r.forward(cams).cpu().numpy()
+    assert np.array_equal(multi, again)
+    for v, cam in enumerate(cams):
+        single = r.forward([cam]).cpu().numpy()[0]
+        assert np.array_equal(single, multi[v])
+    r.close()
+
+
+# --------------------------------------------------------------- backward
+
+@pytest.mark.parametrize("name,variant", [("tiny", "outside"), ("tiny", "inside"),
+                                          ("small", None), ("small360", None)])
+def test_backward_full_image(name, variant):
+    sc, cams = case(name, variant)
+    r = renderer(sc)
+    cams = cams[:2]
+    H, W = cams[0].height, cams[0].width
+    g = pf_synth.make_grad_out(len(cams), H, W, seed=11)
+    r.forward(cams)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    mode = oracle.O1 if name == "tiny" else oracle.O3
+    ref = None
+    for v, cam in enumerate(cams):
+        o = oracle.backward(sc, cam, g[v], mode=mode)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+
+
+@pytest.mark.parametrize("name", ["nerfsynth200k", "train8_1m"])
+def test_backward_large_sampled_pixels(name):
+    """Full sizes, all views in one call; dL/dout is non-zero only on sampled pixels,
+    so the oracle can compute the exact gradient pixel by pixel."""
+    sc, cams = case(name)
+    r = renderer(sc, flags=0)
+    H, W = cams[0].height, cams[0].width
+    rng = np.random.default_rng(1)
+    g = np.zeros((len(cams), H, W, 4), np.float32)
+    pix = {}
+    for v in (0, len(cams) - 1):
+        p = np.stack([rng.integers(0, W, 1500), rng.integers(0, H, 1500)], 1)
+        p = np.unique(p, axis=0)
+        pix[v] = p
+        g[v, p[:, 1], p[:, 0]] = rng.standard_normal((p.shape[0], 4)).astype(np.float32)
+    r.forward(cams)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    ref = None
+    for v, p in pix.items():
+        o = oracle.backward(sc, cams[v], g[v, p[:, 1], p[:, 0]], mode=oracle.O3, pixels=p)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+
+
+def test_backward_requires_matching_forward():
+    import paper_2604_24994_b200 as pf
+    sc, cams = case("tiny")
+    r = renderer(sc)
+    g = torch.zeros((1, 64, 64, 4), device="cuda")
+    with pytest.raises(pf.PFError) as e:
+        r.backward(cams, g)
+    assert e.value.status == 4
+    r.forward(cams)
+    other = pf_synth.make_cameras("tiny", variant="inside")
+    with pytest.raises(pf.PFError) as e:
+        r.backward(other, g)
+    assert e.value.status == 4
+    r.backward(cams, g)
+    r.close()
+
+
+def test_abi_argument_errors():
+    import paper_2604_24994_b200 as pf
+    sc, cams = case("tiny")
+    bad = sc.copy()
+    bad.nbr_indices = bad.nbr_indices.copy()
+    bad.nbr_indices[3] = sc.num_cells + 5
+    with pytest.raises(pf.PFError) as e:
+        renderer(bad)
+    assert e.value.status == 1
+    bad = sc.copy()
+    bad.radii = bad.radii.copy()
+    bad.radii[0] = -1.0
+    with pytest.raises(pf.PFError) as e:
+        renderer(bad)
+    assert e.value.status == 1
+    r = renderer(sc)
+    c = pf_synth.make_cameras("tiny")[0]
+    c.fx = 0.0
+    with pytest.raises(pf.PFError) as e:
+        r.forward([c])
+    assert e.value.status == 1
+    c = pf_synth.make_cameras("tiny")[0]
+    c.near = -1.0
+    with pytest.raises(pf.PFError):
+        r.forward([c])
+    r.close()
