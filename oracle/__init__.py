@@ -60,6 +60,9 @@ def lib():
                                       P, P, P, P, P, C.c_int]
         L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, i64, P, P,
                                            C.c_double, P, P]
+        L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, C.c_int32,
+                                             C.c_int32, P, i64]
+        L.oracle_pixel_segments.restype = i64
         L.oracle_pixel_ray.argtypes = [P, C.c_int32, C.c_int32, P, P, P]
         L.oracle_composite.argtypes = [i64, P, P, P, P, P]
         L.oracle_composite.restype = i64
@@ -195,6 +198,17 @@ def cell_interval(sc, i, Q, d, t_near=0.0, mode=O2):
                                      _p(A.off), _p(A.idx), int(i), _p(Qa), _p(da),
                                      float(t_near), _p(res), _p(kinds))
     return bool(hit), float(res[0]), float(res[1]), kinds
+
+
+def pixel_segments(sc, cam, x, y, mode=O3, cap=4096):
+    """Composited segments of pixel (x,y): list of dicts (cell, t_in, t_out, kin, kout,
+    jin, jout, list_pos); kinds 0 sphere, 1 near, 2 plane."""
+    A = _SceneArrays(sc)
+    oc = make_camera(cam)
+    buf = np.zeros((cap, 8))
+    n = lib().oracle_pixel_segments(mode, *A.args(), C.byref(oc), int(x), int(y), _p(buf), cap)
+    keys = ("cell", "t_in", "t_out", "kin", "kout", "jin", "jout", "list_pos")
+    return [dict(zip(keys, row)) for row in buf[:n]]
 
 
 def pixel_ray(cam, x, y):

@@ -737,6 +737,37 @@ int oracle_cell_interval(int mode, int64_t N, const float *sites, const float *w
     return 1;
 }
 
+/* The composited segments of one pixel (mode O1/O2/O3), in compositing order:
+ * seg[8k..8k+7] = (cell, t_in, t_out, kin, kout, jin, jout, list_pos).
+ * Returns the number of segments written (<= cap). */
+int64_t oracle_pixel_segments(int mode, int64_t N, const float *sites, const float *weights,
+                              const float *radii, const float *density, const float *rgb,
+                              const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
+                              const oc_camera *cam, int32_t x, int32_t y, double *seg,
+                              int64_t cap)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg);
+    oc_bins B;
+    memset(&B, 0, sizeof(B));
+    if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
+    oc_scratch scr = {NULL, 0};
+    double Q[3], d[3], tn, out[4];
+    pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+    int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL);
+    int64_t K = composite(&S, scr.segs, n, out);
+    int64_t m = K < cap ? K : cap;
+    for (int64_t k = 0; k < m; ++k) {
+        const oc_seg *g = scr.segs + k;
+        double *o = seg + 8 * k;
+        o[0] = g->cell; o[1] = g->t_in; o[2] = g->t_out; o[3] = g->kin;
+        o[4] = g->kout; o[5] = g->jin; o[6] = g->jout; o[7] = g->list_pos;
+    }
+    free(scr.segs);
+    if (B.vals) free_bins(&B);
+    return m;
+}
+
 /* The ray of pixel (x, y): Q[3], d[3], t_near. */
 int oracle_pixel_ray(const oc_camera *cam, int32_t x, int32_t y, double *Q, double *d,
                      double *t_near)

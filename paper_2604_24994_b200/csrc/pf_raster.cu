@@ -93,10 +93,23 @@ struct Seg {
     float dt;              // interval length (0 = empty)
 };
 
+// Per-pixel exact ray (fp64) kept in shared memory for the near-tangent path.
+struct PixelRays {
+    double dx[256], dy[256], dz[256];
+};
+
 // a8: ray-sphere test in the local frame: t_c = t0 + delta.c,
 // e = e0 - t0 delta - (delta.c) d,  h = r^2 - |e|^2;  hit iff h > 0 and the
 // exit t_c + sqrt(h) is beyond t_near.
-__device__ __forceinline__ bool sphere_hit(const Ray &R, const Stage &S, int j, Seg &g)
+// Near-tangent rays (|h| < kTangent r^2, ~0.1% of tests) are redone in fp64 from
+// the exact ray and the fp32 site: there fp32 loses h (the endpoint derivative
+// r/s is singular as s -> 0), and the hit decision and s, e
+// come from the fp64 values.  K6 and K7 share this code, so they agree bitwise.
+constexpr float kTangent = 1e-3f;
+
+__device__ __forceinline__ bool sphere_hit(const Ray &R, const Stage &S, int j, Seg &g,
+                                           const DeviceScene &ds, const CamParams &cam,
+                                           const PixelRays &PR)
 {
     const float cx = S.cx[j], cy = S.cy[j], cz = S.cz[j], t0 = S.t0[j], r = S.r[j];
     float dc = fmaf(R.ddx, cx, fmaf(R.ddy, cy, __fmul_rn(R.ddz, cz)));
@@ -104,7 +117,26 @@ __device__ __forceinline__ bool sphere_hit(const Ray &R, const Stage &S, int j, 
     g.ex = fmaf(-dc, R.dx, fmaf(-t0, R.ddx, S.e0x[j]));
     g.ey = fmaf(-dc, R.dy, fmaf(-t0, R.ddy, S.e0y[j]));
     g.ez = fmaf(-dc, R.dz, fmaf(-t0, R.ddz, S.e0z[j]));
-    float h = fmaf(-g.ex, g.ex, fmaf(-g.ey, g.ey, fmaf(-g.ez, g.ez, __fmul_rn(r, r))));
+    const float r2 = __fmul_rn(r, r);
+    float h = fmaf(-g.ex, g.ex, fmaf(-g.ey, g.ey, fmaf(-g.ez, g.ez, r2)));
+    if (fabsf(h) < __fmul_rn(kTangent, r2)) {
+        const float4 A = ds.cellA[S.cell[j]];
+        const int t = threadIdx.x;
+        const double dx = PR.dx[t], dy = PR.dy[t], dz = PR.dz[t];
+        const double c0 = __dsub_rn((double)A.x, (double)cam.M[3]);
+        const double c1 = __dsub_rn((double)A.y, (double)cam.M[7]);
+        const double c2 = __dsub_rn((double)A.z, (double)cam.M[11]);
+        const double tcd = __fma_rn(dx, c0, __fma_rn(dy, c1, __dmul_rn(dz, c2)));
+        const double e0 = __fma_rn(-tcd, dx, c0), e1 = __fma_rn(-tcd, dy, c1),
+                     e2 = __fma_rn(-tcd, dz, c2);
+        const double rd = (double)r;
+        const double hd = __fma_rn(-e0, e0, __fma_rn(-e1, e1, __fma_rn(-e2, e2, __dmul_rn(rd, rd))));
+        g.tc = __double2float_rn(tcd);
+        g.ex = __double2float_rn(e0);
+        g.ey = __double2float_rn(e1);
+        g.ez = __double2float_rn(e2);
+        h = (hd > 0.0) ? fmaxf(__double2float_rn(hd), 1e-37f) : -1.0f;
+    }
     if (!(h > 0.0f)) return false;
     g.s = __fsqrt_rn(h);
     return __fadd_rn(g.tc, g.s) > R.tnear;
@@ -177,7 +209,8 @@ struct PixelSetup {
     double Q[3], d0[3];
 };
 
-__device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, PixelSetup &P)
+__device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, PixelSetup &P,
+                                            PixelRays &PR)
 {
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -197,6 +230,9 @@ __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, Pixe
     P.R.ddy = __double2float_rn(__dsub_rn(d[1], P.d0[1]));
     P.R.ddz = __double2float_rn(__dsub_rn(d[2], P.d0[2]));
     P.R.tnear = __double2float_rn(tn);
+    PR.dx[threadIdx.x] = d[0];
+    PR.dy[threadIdx.x] = d[1];
+    PR.dz[threadIdx.x] = d[2];
 }
 
 }  // namespace
@@ -211,9 +247,10 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            long long *__restrict__ counters)
 {
     __shared__ Stage S;
+    __shared__ PixelRays PR;
     const int tile = blockIdx.x;
     PixelSetup P;
-    setup_pixel(cam, tile, P);
+    setup_pixel(cam, tile, P, PR);
     const uint2 rg = ranges[tile];
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     bool done = !P.valid;
@@ -229,7 +266,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) {
                 if (kCount) ++xs;
-                hit = sphere_hit(P.R, S, j, g);
+                hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             }
             if (!__any_sync(0xffffffffu, hit)) continue;
             clip_interval(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
@@ -335,10 +372,11 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             float4 *__restrict__ accB, float *__restrict__ accC)
 {
     __shared__ Stage S;
+    __shared__ PixelRays PR;
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
     PixelSetup P;
-    setup_pixel(cam, tile, P);
+    setup_pixel(cam, tile, P, PR);
     const uint2 rg = ranges[tile];
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     bool done = !P.valid;
@@ -358,7 +396,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             if (__all_sync(0xffffffffu, done)) break;
             Seg g;
             bool hit = false;
-            if (!done) hit = sphere_hit(P.R, S, j, g);
+            if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
             clip_interval(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
             bool seg = g.dt > 0.0f;
