@@ -1,13 +1,13 @@
 // pf_raster.cu -- K6 forward blend, K7 backward replay, K8 gradient unpack.
 //
-// One CTA per 16x16 tile (256 threads); warp w covers an 8x4 pixel block.
-// The tile's sorted cell list is walked in batches of 256 entries: each thread
-// stages one cell (record + the tile-centred ray frame computed in fp64,
-// SURVEY C18) into shared memory; then every warp walks the batch in lockstep,
-// all 32 lanes (pixels) on the same cell:
+// One CTA per 16x16 tile (256 threads); warp w covers an 8x4 pixel block and
+// walks the tile's sorted cell list independently (no CTA barriers), 32
+// entries at a time: lane-parallel fp64 cull of the entries against the warp's
+// ray cone + staging of the survivors with the warp-centred ray frame
+// (SURVEY C18), then all 32 lanes (pixels) in lockstep on each survivor:
 //   sphere test (a8) -> __any_sync cull -> half-space clipping against the
-//   cell's neighbour planes (a9, division free) -> front-to-back compositing
-//   (a10) -> warp vote / CTA count early termination.
+//   cell's neighbour planes (a9, division free, branch free) -> front-to-back
+//   compositing (a10) -> warp vote early termination.
 // The backward (K7) replays the identical walk front to back (bit-identical
 // intervals and transmittances, same inlined math with explicit IEEE
 // intrinsics), recovers S_k = out_rgb - C_k from the saved final colour, and
@@ -49,39 +49,31 @@ __device__ __forceinline__ void ray_dir(const CamParams &cam, double u, double v
                            __dsqrt_rn(__fma_rn(a, a, __fma_rn(b, b, 1.0))));
 }
 
-// Staged cell: tile-centred frame t0 = d0.c, e0 = c - t0 d0 (fp64 -> fp32),
-// c = p - Q, plus the record.  SoA in shared memory.
-struct Stage {
-    float t0[256], e0x[256], e0y[256], e0z[256], cx[256], cy[256], cz[256];
-    float r[256], sig[256], cr[256], cg[256], cb[256];
-    uint32_t eb[256], deg[256], cell[256];
+// ---------------------------------------------------------------------------
+// Per-warp state.  Warp w of the tile's CTA owns an 8x4 pixel block and walks
+// the tile's sorted list on its own (no CTA barriers): 32 list entries at a
+// time, one per lane, are culled against the warp's ray cone (fp64, exact
+// conservative test), and the survivors are staged in the warp's shared-memory
+// slots with the warp-centred ray frame t0 = d_w.c, e0 = c - t0 d_w (fp64 ->
+// fp32, SURVEY C18 applied per warp block instead of per tile).
+// ---------------------------------------------------------------------------
+constexpr int kWarps = 8;
+
+struct WarpStage {
+    float t0[32], e0x[32], e0y[32], e0z[32], cx[32], cy[32], cz[32], r[32];
+    float sig[32], cr[32], cg[32], cb[32];
+    uint32_t eb[32], deg[32], cell[32];
 };
 
-__device__ __forceinline__ void stage_cell(Stage &S, int slot, const DeviceScene &ds, uint32_t cell,
-                                           const double Q[3], const double d0[3])
-{
-    float4 A = ds.cellA[cell];
-    float4 B = ds.cellB[cell];
-    uint2 E = ds.cellE[cell];
-    double c0 = __dsub_rn((double)A.x, Q[0]), c1 = __dsub_rn((double)A.y, Q[1]),
-           c2 = __dsub_rn((double)A.z, Q[2]);
-    double t0 = __fma_rn(d0[0], c0, __fma_rn(d0[1], c1, __dmul_rn(d0[2], c2)));
-    S.t0[slot] = __double2float_rn(t0);
-    S.e0x[slot] = __double2float_rn(__fma_rn(-t0, d0[0], c0));
-    S.e0y[slot] = __double2float_rn(__fma_rn(-t0, d0[1], c1));
-    S.e0z[slot] = __double2float_rn(__fma_rn(-t0, d0[2], c2));
-    S.cx[slot] = __double2float_rn(c0);
-    S.cy[slot] = __double2float_rn(c1);
-    S.cz[slot] = __double2float_rn(c2);
-    S.r[slot] = A.w;
-    S.sig[slot] = B.x;
-    S.cr[slot] = B.y;
-    S.cg[slot] = B.z;
-    S.cb[slot] = B.w;
-    S.eb[slot] = E.x;
-    S.deg[slot] = E.y;
-    S.cell[slot] = cell;
-}
+// Per-pixel exact ray (fp64), read only by the near-tangent path.
+struct PixelRays {
+    double dx[256], dy[256], dz[256];
+};
+
+struct WarpCtx {           // one per warp, in shared memory
+    double wx, wy, wz;     // warp-centre direction d_w
+    double cos_t, sin_t;   // half-angle of the cone containing the warp's pixel rays
+};
 
 // ---- the per-(pixel, cell) math shared verbatim by K6 and K7 -------------
 
@@ -93,11 +85,6 @@ struct Seg {
     float dt;              // interval length (0 = empty)
 };
 
-// Per-pixel exact ray (fp64) kept in shared memory for the near-tangent path.
-struct PixelRays {
-    double dx[256], dy[256], dz[256];
-};
-
 // a8: ray-sphere test in the local frame: t_c = t0 + delta.c,
 // e = e0 - t0 delta - (delta.c) d,  h = r^2 - |e|^2;  hit iff h > 0 and the
 // exit t_c + sqrt(h) is beyond t_near.
@@ -107,7 +94,7 @@ struct PixelRays {
 // come from the fp64 values.  K6 and K7 share this code, so they agree bitwise.
 constexpr float kTangent = 1e-3f;
 
-__device__ __forceinline__ bool sphere_hit(const Ray &R, const Stage &S, int j, Seg &g,
+__device__ __forceinline__ bool sphere_hit(const Ray &R, const WarpStage &S, int j, Seg &g,
                                            const DeviceScene &ds, const CamParams &cam,
                                            const PixelRays &PR)
 {
@@ -135,24 +122,42 @@ __device__ __forceinline__ bool sphere_hit(const Ray &R, const Stage &S, int j, 
         g.ex = __double2float_rn(e0);
         g.ey = __double2float_rn(e1);
         g.ez = __double2float_rn(e2);
-        h = (hd > 0.0) ? fmaxf(__double2float_rn(hd), 1e-37f) : -1.0f;
+        h = (hd > 0.0) ? fmaxf(__double2float_rn(hd), 1e-30f) : -1.0f;
     }
     if (!(h > 0.0f)) return false;
-    g.s = __fsqrt_rn(h);
+    g.s = __fmul_rn(h, rsqrtf(h));
     return __fadd_rn(g.tc, g.s) > R.tnear;
 }
 
-// a9: clip the chord [-s, s] by the near plane and by every neighbour's radical
-// plane  a t' <= b,  a = d.n, b = k + n.e  (division free: bounds kept as
-// fractions with positive denominators; strict comparisons, first binding
-// constraint wins -- SURVEY C16).  Returns dt (0 if empty).
+// one radical plane  a t' <= b,  a = d.n, b = k + n.e, branch free: the current
+// bound on the side of sign(a) is N/D (D > 0); the candidate b/a is tighter iff
+// b D < N a (strict: the first binding constraint wins).
+__device__ __forceinline__ void clip_plane(const Ray &R, const float4 E, int q, Seg &g, bool &empty)
+{
+    const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
+    const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
+    const bool pos = a > 0.0f, neg = a < 0.0f;
+    const float N = pos ? g.hi_n : g.lo_n, D = pos ? g.hi_d : g.lo_d;
+    const bool tighter = __fmul_rn(b, D) < __fmul_rn(N, a);
+    const bool uh = pos && tighter, ul = neg && tighter;
+    g.hi_n = uh ? b : g.hi_n;
+    g.hi_d = uh ? a : g.hi_d;
+    g.hi_q = uh ? q : g.hi_q;
+    g.lo_n = ul ? -b : g.lo_n;
+    g.lo_d = ul ? -a : g.lo_d;
+    g.lo_q = ul ? q : g.lo_q;
+    empty |= (a == 0.0f) && (b < 0.0f);
+}
+
+// a9: clip the chord [-s, s] by the near plane and every neighbour's radical
+// plane (P:228, P:577-585 with the weight sign of SURVEY C1).
 __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__restrict__ edges,
                                               uint32_t eb, uint32_t deg, Seg &g, bool active)
 {
     g.lo_n = -g.s;
     g.lo_d = 1.0f;
     g.lo_q = kEndSphere;
-    float tnl = __fsub_rn(R.tnear, g.tc);
+    const float tnl = __fsub_rn(R.tnear, g.tc);
     if (tnl > g.lo_n) {
         g.lo_n = tnl;
         g.lo_q = kEndNear;
@@ -161,78 +166,138 @@ __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__rest
     g.hi_d = 1.0f;
     g.hi_q = kEndSphere;
     bool empty = false;
-#pragma unroll 4
-    for (uint32_t q = eb; q < eb + deg; ++q) {
-        float4 E = __ldg(edges + q);
-        float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
-        float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
-        if (a > 0.0f) {
-            if (__fmul_rn(b, g.hi_d) < __fmul_rn(g.hi_n, a)) {
-                g.hi_n = b;
-                g.hi_d = a;
-                g.hi_q = (int)q;
-            }
-        } else if (a < 0.0f) {
-            if (__fmul_rn(-b, g.lo_d) > __fmul_rn(g.lo_n, -a)) {
-                g.lo_n = -b;
-                g.lo_d = -a;
-                g.lo_q = (int)q;
-            }
-        } else if (b < 0.0f) {
-            empty = true;
-        }
+    uint32_t q = eb;
+    const uint32_t qe = eb + deg;
+    for (; q + 4 <= qe; q += 4) {
+        const float4 E0 = __ldg(edges + q), E1 = __ldg(edges + q + 1), E2 = __ldg(edges + q + 2),
+                     E3 = __ldg(edges + q + 3);
+        clip_plane(R, E0, (int)q, g, empty);
+        clip_plane(R, E1, (int)q + 1, g, empty);
+        clip_plane(R, E2, (int)q + 2, g, empty);
+        clip_plane(R, E3, (int)q + 3, g, empty);
     }
-    float dt = __fsub_rn(__fdiv_rn(g.hi_n, g.hi_d), __fdiv_rn(g.lo_n, g.lo_d));
+    for (; q < qe; ++q) clip_plane(R, __ldg(edges + q), (int)q, g, empty);
+    const float dt = __fsub_rn(__fdividef(g.hi_n, g.hi_d), __fdividef(g.lo_n, g.lo_d));
     g.dt = (active && !empty && dt > 0.0f) ? dt : 0.0f;
 }
 
-// a10: one front-to-back compositing step; returns exp(-tau)
-__device__ __forceinline__ float composite_step(float sig, float dt, float cr, float cg, float cb,
-                                                float &T, float &Cr, float &Cg, float &Cb,
-                                                float &alpha)
+// a10: one front-to-back compositing step (alpha = 1 - exp(-sigma dt))
+__device__ __forceinline__ void composite_step(float sig, float dt, float cr, float cg, float cb,
+                                               float &T, float &Cr, float &Cg, float &Cb,
+                                               float &alpha)
 {
-    float tau = __fmul_rn(sig, dt);
-    float ex = expf(-tau);
+    const float tau = __fmul_rn(sig, dt);
+    const float ex = __expf(-tau);
     alpha = __fsub_rn(1.0f, ex);
-    float w = __fmul_rn(T, alpha);
+    const float w = __fmul_rn(T, alpha);
     Cr = fmaf(w, cr, Cr);
     Cg = fmaf(w, cg, Cg);
     Cb = fmaf(w, cb, Cb);
     T = __fmul_rn(T, ex);
-    return ex;
 }
 
 struct PixelSetup {
     int x, y;
     bool valid;
     Ray R;
-    double Q[3], d0[3];
 };
 
+// pixel ray, warp cone and warp frame.  Every lane of a warp runs this.
 __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, PixelSetup &P,
-                                            PixelRays &PR)
+                                            PixelRays &PR, WarpCtx &W)
 {
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    P.x = tx * kTile + (warp & 1) * 8 + (lane & 7);
-    P.y = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 4;
+    P.x = x0 + (lane & 7);
+    P.y = y0 + (lane >> 3);
     P.valid = P.x < cam.W && P.y < cam.H;
-    P.Q[0] = cam.M[3];
-    P.Q[1] = cam.M[7];
-    P.Q[2] = cam.M[11];
-    ray_dir(cam, tx * kTile + 8.0, ty * kTile + 8.0, P.d0, nullptr);
+    double dw[3];
+    ray_dir(cam, x0 + 4.0, y0 + 2.0, dw, nullptr);
+    // cone half-angle: the largest angle to the four corner pixel rays (the
+    // angle to d_w is quasi-convex over the image plane, so corners bound it)
+    double dcn[3];
+    const int cxo = (lane & 1) ? 7 : 0, cyo = (lane & 2) ? 3 : 0;
+    ray_dir(cam, x0 + cxo + 0.5, y0 + cyo + 0.5, dcn, nullptr);
+    double cs = __fma_rn(dw[0], dcn[0], __fma_rn(dw[1], dcn[1], __dmul_rn(dw[2], dcn[2])));
+    cs = fmin(cs, __shfl_xor_sync(0xffffffffu, cs, 1));
+    cs = fmin(cs, __shfl_xor_sync(0xffffffffu, cs, 2));
+    cs = fmin(cs, 1.0);
+    if (lane == 0) {
+        W.wx = dw[0];
+        W.wy = dw[1];
+        W.wz = dw[2];
+        W.cos_t = cs;
+        W.sin_t = sqrt(fmax(0.0, 1.0 - cs * cs));
+    }
     double d[3], tn;
     ray_dir(cam, P.x + 0.5, P.y + 0.5, d, &tn);
     P.R.dx = __double2float_rn(d[0]);
     P.R.dy = __double2float_rn(d[1]);
     P.R.dz = __double2float_rn(d[2]);
-    P.R.ddx = __double2float_rn(__dsub_rn(d[0], P.d0[0]));
-    P.R.ddy = __double2float_rn(__dsub_rn(d[1], P.d0[1]));
-    P.R.ddz = __double2float_rn(__dsub_rn(d[2], P.d0[2]));
+    P.R.ddx = __double2float_rn(__dsub_rn(d[0], dw[0]));
+    P.R.ddy = __double2float_rn(__dsub_rn(d[1], dw[1]));
+    P.R.ddz = __double2float_rn(__dsub_rn(d[2], dw[2]));
     P.R.tnear = __double2float_rn(tn);
     PR.dx[threadIdx.x] = d[0];
     PR.dy[threadIdx.x] = d[1];
     PR.dz[threadIdx.x] = d[2];
+    __syncwarp();
+}
+
+// Lane `lane` takes list entry e (if < end): conservative sphere-vs-warp-cone
+// test in fp64; survivors are staged in slot `lane`.  Returns the ballot.
+// Cone test: the sphere (c, r) meets the cone (axis d_w, half-angle th) iff
+// the angle between c and d_w is <= th + asin(r/|c|), i.e. (|c| > r)
+// d_w.c >= cos(th) sqrt(|c|^2 - r^2) - sin(th) r;  always if |c| <= r.
+__device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene &ds,
+                                                const CamParams &cam,
+                                                const uint32_t *__restrict__ vals, uint32_t e,
+                                                uint32_t end, const WarpCtx &W, int lane)
+{
+    bool pass = false;
+    uint32_t cell = 0;
+    float4 A;
+    double t = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    if (e < end) {
+        cell = __ldg(vals + e);
+        A = __ldg(ds.cellA + cell);
+        c0 = __dsub_rn((double)A.x, (double)cam.M[3]);
+        c1 = __dsub_rn((double)A.y, (double)cam.M[7]);
+        c2 = __dsub_rn((double)A.z, (double)cam.M[11]);
+        t = __fma_rn(W.wx, c0, __fma_rn(W.wy, c1, __dmul_rn(W.wz, c2)));
+        const double cc = __fma_rn(c0, c0, __fma_rn(c1, c1, __dmul_rn(c2, c2)));
+        const double rr = (double)A.w;
+        const double r2 = __dmul_rn(rr, rr);
+        if (cc <= r2) {
+            pass = true;
+        } else {
+            const double lim = W.cos_t * sqrt(cc - r2) - W.sin_t * rr;
+            pass = t >= lim - 1e-7 * sqrt(cc);
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, pass);
+    if (pass) {
+        const float4 B = __ldg(ds.cellB + cell);
+        const uint2 E = __ldg(ds.cellE + cell);
+        S.t0[lane] = __double2float_rn(t);
+        S.e0x[lane] = __double2float_rn(__fma_rn(-t, W.wx, c0));
+        S.e0y[lane] = __double2float_rn(__fma_rn(-t, W.wy, c1));
+        S.e0z[lane] = __double2float_rn(__fma_rn(-t, W.wz, c2));
+        S.cx[lane] = __double2float_rn(c0);
+        S.cy[lane] = __double2float_rn(c1);
+        S.cz[lane] = __double2float_rn(c2);
+        S.r[lane] = A.w;
+        S.sig[lane] = B.x;
+        S.cr[lane] = B.y;
+        S.cg[lane] = B.z;
+        S.cb[lane] = B.w;
+        S.eb[lane] = E.x;
+        S.deg[lane] = E.y;
+        S.cell[lane] = cell;
+    }
+    __syncwarp();
+    return m;
 }
 
 }  // namespace
@@ -246,28 +311,27 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ vals, float4 *__restrict__ out, float4 *__restrict__ saved,
            long long *__restrict__ counters)
 {
-    __shared__ Stage S;
+    __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
-    const int tile = blockIdx.x;
+    __shared__ WarpCtx WC[kWarps];
+    const int tile = blockIdx.x, lane = threadIdx.x & 31;
+    WarpStage &S = WS[threadIdx.x >> 5];
+    WarpCtx &W = WC[threadIdx.x >> 5];
     PixelSetup P;
-    setup_pixel(cam, tile, P, PR);
+    setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     bool done = !P.valid;
     long long xs = 0, xh = 0, xp = 0, xc = 0;
-    for (uint32_t base = rg.x; base < rg.y; base += 256) {
-        if (__syncthreads_count(!done) == 0) break;
-        const int nb = (int)min(256u, rg.y - base);
-        if ((int)threadIdx.x < nb) stage_cell(S, threadIdx.x, ds, vals[base + threadIdx.x], P.Q, P.d0);
-        __syncthreads();
-        for (int j = 0; j < nb; ++j) {
-            if (__all_sync(0xffffffffu, done)) break;
+    for (uint32_t base = rg.x; base < rg.y; base += 32) {
+        if (__all_sync(0xffffffffu, done)) break;
+        unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
             Seg g;
             bool hit = false;
-            if (!done) {
-                if (kCount) ++xs;
-                hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
-            }
+            if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
             clip_interval(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
             if (kCount && hit) {
@@ -278,17 +342,23 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 float alpha;
                 composite_step(S.sig[j], g.dt, S.cr[j], S.cg[j], S.cb[j], T, Cr, Cg, Cb, alpha);
                 if (kCount) ++xc;
-                if (T < kTStop) done = true;
+                if (T < kTStop) {
+                    done = true;
+                    if (kCount) xs = (long long)(base + j - rg.x) + 1;
+                }
             }
+            if (__all_sync(0xffffffffu, done)) break;
         }
-        __syncthreads();
+        __syncwarp();
     }
     if (P.valid) {
-        float4 o = make_float4(fmaf(T, ds.bg[0], Cr), fmaf(T, ds.bg[1], Cg), fmaf(T, ds.bg[2], Cb), T);
-        size_t pix = (size_t)P.y * cam.W + P.x;
+        const float4 o = make_float4(fmaf(T, ds.bg[0], Cr), fmaf(T, ds.bg[1], Cg),
+                                     fmaf(T, ds.bg[2], Cb), T);
+        const size_t pix = (size_t)P.y * cam.W + P.x;
         if (out) out[pix] = o;
         if (saved) saved[pix] = o;
         if (kCount) {
+            if (!done) xs = (long long)(rg.y - rg.x);
             counters[4 * pix + 0] = xs;
             counters[4 * pix + 1] = xh;
             counters[4 * pix + 2] = xp;
@@ -342,25 +412,24 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
                                          const int32_t *__restrict__ nbr, float4 *accA, OwnGrad &o)
 {
     if (q == kEndNear) return;
-    float xpx = fmaf(tprime, R.dx, -g.ex), xpy = fmaf(tprime, R.dy, -g.ey),
-          xpz = fmaf(tprime, R.dz, -g.ez);   // x* - p_i
+    const float xpx = fmaf(tprime, R.dx, -g.ex), xpy = fmaf(tprime, R.dy, -g.ey),
+                xpz = fmaf(tprime, R.dz, -g.ez);   // x* - p_i
     if (q == kEndSphere) {
-        float f = __fdiv_rn(wgt, tprime);
+        const float f = __fdividef(wgt, tprime);
         o.px = fmaf(f, xpx, o.px);
         o.py = fmaf(f, xpy, o.py);
         o.pz = fmaf(f, xpz, o.pz);
         o.r = fmaf(f, rad, o.r);
         return;
     }
-    float f = __fdiv_rn(wgt, a);
+    const float f = __fdividef(wgt, a);
     o.px = fmaf(f, xpx, o.px);
     o.py = fmaf(f, xpy, o.py);
     o.pz = fmaf(f, xpz, o.pz);
     o.w = fmaf(0.5f, f, o.w);
-    float4 E = __ldg(edges + q);
-    int j = __ldg(nbr + q);
-    float4 gj = make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f);
-    atomicAdd(accA + j, gj);
+    const float4 E = __ldg(edges + q);
+    const int j = __ldg(nbr + q);
+    atomicAdd(accA + j, make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f));
 }
 
 }  // namespace
@@ -371,74 +440,78 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const float4 *__restrict__ grad_out, float4 *__restrict__ accA,
             float4 *__restrict__ accB, float *__restrict__ accC)
 {
-    __shared__ Stage S;
+    __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
-    const int tile = blockIdx.x;
-    const int lane = threadIdx.x & 31;
+    __shared__ WarpCtx WC[kWarps];
+    const int tile = blockIdx.x, lane = threadIdx.x & 31;
+    WarpStage &S = WS[threadIdx.x >> 5];
+    WarpCtx &W = WC[threadIdx.x >> 5];
     PixelSetup P;
-    setup_pixel(cam, tile, P, PR);
+    setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     bool done = !P.valid;
     float4 fin = make_float4(0, 0, 0, 1), G = make_float4(0, 0, 0, 0);
     if (P.valid) {
-        size_t pix = (size_t)P.y * cam.W + P.x;
+        const size_t pix = (size_t)P.y * cam.W + P.x;
         fin = saved[pix];
         G = grad_out[pix];
     }
     const float GT_Tfin = __fmul_rn(G.w, fin.w);
-    for (uint32_t base = rg.x; base < rg.y; base += 256) {
-        if (__syncthreads_count(!done) == 0) break;
-        const int nb = (int)min(256u, rg.y - base);
-        if ((int)threadIdx.x < nb) stage_cell(S, threadIdx.x, ds, vals[base + threadIdx.x], P.Q, P.d0);
-        __syncthreads();
-        for (int j = 0; j < nb; ++j) {
-            if (__all_sync(0xffffffffu, done)) break;
+    for (uint32_t base = rg.x; base < rg.y; base += 32) {
+        if (__all_sync(0xffffffffu, done)) break;
+        unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
             Seg g;
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
             clip_interval(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
-            bool seg = g.dt > 0.0f;
+            const bool seg = g.dt > 0.0f;
             if (!__any_sync(0xffffffffu, seg)) continue;
             OwnGrad o = {0, 0, 0, 0, 0};
             float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f;
             if (seg) {
                 const float sig = S.sig[j], cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
-                float Tk = T, alpha;
+                const float Tk = T;
+                float alpha;
                 composite_step(sig, g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
                 // T is now T_{k+1}; C is C_k; S_k = out_rgb - C_k
-                float Sr = __fsub_rn(fin.x, Cr), Sg = __fsub_rn(fin.y, Cg), Sb = __fsub_rn(fin.z, Cb);
+                const float Sr = __fsub_rn(fin.x, Cr), Sg = __fsub_rn(fin.y, Cg),
+                            Sb = __fsub_rn(fin.z, Cb);
                 float dtau = -GT_Tfin;
                 dtau = fmaf(G.x, fmaf(T, cr, -Sr), dtau);
                 dtau = fmaf(G.y, fmaf(T, cg, -Sg), dtau);
                 dtau = fmaf(G.z, fmaf(T, cb, -Sb), dtau);
-                float wa = __fmul_rn(Tk, alpha);
+                const float wa = __fmul_rn(Tk, alpha);
                 gR = wa * G.x;
                 gG = wa * G.y;
                 gB = wa * G.z;
                 gs = dtau * g.dt;
-                float gdt = dtau * sig;
+                const float gdt = dtau * sig;
                 if (gdt != 0.0f) {
                     const float rad = S.r[j];
-                    float tout = __fdiv_rn(g.hi_n, g.hi_d), tin = __fdiv_rn(g.lo_n, g.lo_d);
+                    const float tout = __fdividef(g.hi_n, g.hi_d), tin = __fdividef(g.lo_n, g.lo_d);
                     end_grad(P.R, g, g.hi_q, tout, g.hi_d, gdt, rad, ds.edges, ds.nbr_idx, accA, o);
                     end_grad(P.R, g, g.lo_q, tin, -g.lo_d, -gdt, rad, ds.edges, ds.nbr_idx, accA, o);
                 }
                 if (T < kTStop) done = true;
             }
             // own-cell terms: warp reduction, one lane issues the atomics
-            float v0 = warp_sum(o.px), v1 = warp_sum(o.py), v2 = warp_sum(o.pz), v3 = warp_sum(o.w);
-            float v4 = warp_sum(o.r), v5 = warp_sum(gs), v6 = warp_sum(gR), v7 = warp_sum(gG);
-            float v8 = warp_sum(gB);
+            const float v0 = warp_sum(o.px), v1 = warp_sum(o.py), v2 = warp_sum(o.pz);
+            const float v3 = warp_sum(o.w), v4 = warp_sum(o.r), v5 = warp_sum(gs);
+            const float v6 = warp_sum(gR), v7 = warp_sum(gG), v8 = warp_sum(gB);
             if (lane == 0) {
-                uint32_t cell = S.cell[j];
+                const uint32_t cell = S.cell[j];
                 atomicAdd(accA + cell, make_float4(v0, v1, v2, v3));
                 atomicAdd(accB + cell, make_float4(v4, v5, v6, v7));
                 atomicAdd(accC + cell, v8);
             }
+            if (__all_sync(0xffffffffu, done)) break;
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
