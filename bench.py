@@ -41,7 +41,7 @@ FP32_LANES_PER_SM = 128
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="train8_1m",
@@ -270,6 +270,7 @@ def main():
     l0 = r.launch_count()
     clk = ClockSampler(local)
     clk.start()
+    time.sleep(0.5)          # let the sampler take its first reading
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -277,6 +278,7 @@ def main():
         step()
     e1.record(stream)
     barrier()
+    time.sleep(0.25)
     clocks = clk.stop()
     launches = r.launch_count() - l0
     stages = r.stage_times()

@@ -394,8 +394,8 @@ int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t V, const floa
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)s->ds.N;
-    PF_CUDA(s->acc.reserve(N * (16 + 16 + 4)));
-    PF_CUDA(cudaMemsetAsync(s->acc.ptr, 0, N * (16 + 16 + 4), st));
+    PF_CUDA(s->acc.reserve(N * 48));   // 12 floats per cell (pf_raster.cu)
+    PF_CUDA(cudaMemsetAsync(s->acc.ptr, 0, N * 48, st));
     const size_t npix = (size_t)cams[0].width * cams[0].height;
     for (int v = 0; v < V; ++v) {
         pf::ViewState &vs = s->views[v];

@@ -80,10 +80,17 @@ struct WarpCtx {           // one per warp, in shared memory
 struct Seg {
     float s, tc;           // sphere half-chord, t_c (local frame origin)
     float ex, ey, ez;      // e = c - t_c d  (offset of the centre from the ray)
-    float lo_n, lo_d, hi_n, hi_d;   // t'_in = lo_n/lo_d, t'_out = hi_n/hi_d (d > 0)
-    int lo_q, hi_q;        // edge index of the binding plane, or kEndSphere / kEndNear
+    float lo, hi;          // t'_in, t'_out (local frame)
+    int lo_q, hi_q;        // binding constraint: edge index, or kEndSphere / kEndNear (K7 only)
     float dt;              // interval length (0 = empty)
 };
+
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // a8: ray-sphere test in the local frame: t_c = t0 + delta.c,
 // e = e0 - t0 delta - (delta.c) d,  h = r^2 - |e|^2;  hit iff h > 0 and the
@@ -129,56 +136,58 @@ __device__ __forceinline__ bool sphere_hit(const Ray &R, const WarpStage &S, int
     return __fadd_rn(g.tc, g.s) > R.tnear;
 }
 
-// one radical plane  a t' <= b,  a = d.n, b = k + n.e, branch free: the current
-// bound on the side of sign(a) is N/D (D > 0); the candidate b/a is tighter iff
-// b D < N a (strict: the first binding constraint wins).
-__device__ __forceinline__ void clip_plane(const Ray &R, const float4 E, int q, Seg &g, bool &empty)
+// one radical plane  a t' <= b,  a = d.n, b = k + n.e:  t = b/a bounds t' from
+// above if a > 0, from below if a < 0; a == +0 with b < 0 empties the interval
+// (rcp(+0) = +inf, so t = -inf lands on the upper bound).  K6 and K7
+// evaluate the identical instruction sequence (min/max of the same values), K7
+// additionally records which constraint binds (strict: the first one wins,
+// SURVEY C16).
+template <bool kTrack>
+__device__ __forceinline__ void clip_plane(const Ray &R, const float4 E, int q, Seg &g)
 {
     const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
-    const bool pos = a > 0.0f, neg = a < 0.0f;
-    const float N = pos ? g.hi_n : g.lo_n, D = pos ? g.hi_d : g.lo_d;
-    const bool tighter = __fmul_rn(b, D) < __fmul_rn(N, a);
-    const bool uh = pos && tighter, ul = neg && tighter;
-    g.hi_n = uh ? b : g.hi_n;
-    g.hi_d = uh ? a : g.hi_d;
-    g.hi_q = uh ? q : g.hi_q;
-    g.lo_n = ul ? -b : g.lo_n;
-    g.lo_d = ul ? -a : g.lo_d;
-    g.lo_q = ul ? q : g.lo_q;
-    empty |= (a == 0.0f) && (b < 0.0f);
+    const float t = __fmul_rn(b, rcp_approx(a));
+    const bool up = a >= 0.0f;
+    const float th = up ? t : __int_as_float(0x7f800000);
+    const float tl = up ? __int_as_float(0xff800000) : t;
+    const float nh = fminf(g.hi, th), nl = fmaxf(g.lo, tl);
+    if (kTrack) {
+        g.hi_q = (nh != g.hi) ? q : g.hi_q;
+        g.lo_q = (nl != g.lo) ? q : g.lo_q;
+    }
+    g.hi = nh;
+    g.lo = nl;
 }
 
 // a9: clip the chord [-s, s] by the near plane and every neighbour's radical
 // plane (P:228, P:577-585 with the weight sign of SURVEY C1).
+template <bool kTrack>
 __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__restrict__ edges,
                                               uint32_t eb, uint32_t deg, Seg &g, bool active)
 {
-    g.lo_n = -g.s;
-    g.lo_d = 1.0f;
+    g.lo = -g.s;
     g.lo_q = kEndSphere;
     const float tnl = __fsub_rn(R.tnear, g.tc);
-    if (tnl > g.lo_n) {
-        g.lo_n = tnl;
+    if (tnl > g.lo) {
+        g.lo = tnl;
         g.lo_q = kEndNear;
     }
-    g.hi_n = g.s;
-    g.hi_d = 1.0f;
+    g.hi = g.s;
     g.hi_q = kEndSphere;
-    bool empty = false;
     uint32_t q = eb;
     const uint32_t qe = eb + deg;
     for (; q + 4 <= qe; q += 4) {
         const float4 E0 = __ldg(edges + q), E1 = __ldg(edges + q + 1), E2 = __ldg(edges + q + 2),
                      E3 = __ldg(edges + q + 3);
-        clip_plane(R, E0, (int)q, g, empty);
-        clip_plane(R, E1, (int)q + 1, g, empty);
-        clip_plane(R, E2, (int)q + 2, g, empty);
-        clip_plane(R, E3, (int)q + 3, g, empty);
+        clip_plane<kTrack>(R, E0, (int)q, g);
+        clip_plane<kTrack>(R, E1, (int)q + 1, g);
+        clip_plane<kTrack>(R, E2, (int)q + 2, g);
+        clip_plane<kTrack>(R, E3, (int)q + 3, g);
     }
-    for (; q < qe; ++q) clip_plane(R, __ldg(edges + q), (int)q, g, empty);
-    const float dt = __fsub_rn(__fdividef(g.hi_n, g.hi_d), __fdividef(g.lo_n, g.lo_d));
-    g.dt = (active && !empty && dt > 0.0f) ? dt : 0.0f;
+    for (; q < qe; ++q) clip_plane<kTrack>(R, __ldg(edges + q), (int)q, g);
+    const float dt = __fsub_rn(g.hi, g.lo);
+    g.dt = (active && dt > 0.0f) ? dt : 0.0f;
 }
 
 // a10: one front-to-back compositing step (alpha = 1 - exp(-sigma dt))
@@ -333,7 +342,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
-            clip_interval(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
+            clip_interval<false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
             if (kCount && hit) {
                 ++xh;
                 xp += S.deg[j];
@@ -391,13 +400,6 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
 // ------------------------------------------------------------------------
 namespace {
 
-__device__ __forceinline__ float warp_sum(float v)
-{
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
 // d t_end / d theta times  w = +-dL/ddt  for one interval end:
 //   sphere end at t' = +-s:  dt/dp_i = (t' d - e)/t',  dt/dr = r/t'
 //   plane end (i,j), a = d.n: dt/dp_i = (t' d - e)/a, dt/dp_j = (n - t' d + e)/a,
@@ -407,9 +409,11 @@ struct OwnGrad {
     float px, py, pz, w, r;
 };
 
-__device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, float tprime, float a,
+// Accumulator layout: 12 floats per cell, acc[12 i + k]:
+//   k = 0..3 (p.x, p.y, p.z, w)  4..7 (r, sigma, R, G)  8 (B)  9..11 unused.
+__device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, float tprime,
                                          float wgt, float rad, const float4 *__restrict__ edges,
-                                         const int32_t *__restrict__ nbr, float4 *accA, OwnGrad &o)
+                                         const int32_t *__restrict__ nbr, float *acc, OwnGrad &o)
 {
     if (q == kEndNear) return;
     const float xpx = fmaf(tprime, R.dx, -g.ex), xpy = fmaf(tprime, R.dy, -g.ey),
@@ -422,14 +426,51 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
         o.r = fmaf(f, rad, o.r);
         return;
     }
+    const float4 E = __ldg(edges + q);
+    const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float f = __fdividef(wgt, a);
     o.px = fmaf(f, xpx, o.px);
     o.py = fmaf(f, xpy, o.py);
     o.pz = fmaf(f, xpz, o.pz);
     o.w = fmaf(0.5f, f, o.w);
-    const float4 E = __ldg(edges + q);
     const int j = __ldg(nbr + q);
-    atomicAdd(accA + j, make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f));
+    atomicAdd(reinterpret_cast<float4 *>(acc + 12 * (size_t)j),
+              make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f));
+}
+
+// Sum of 9 per-lane values over the warp by a transposing reduction (12 shuffles
+// instead of 45): after it, the lane with (lane & 1) == 0 and a valid slot holds
+// the warp total of value *idx and issues one atomic; 9 lanes, one instruction.
+__device__ __forceinline__ void warp_reduce9_atomic(float v[10], float *acc_cell, int lane)
+{
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    float u[6];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const float send = b4 ? v[k] : v[k + 5], keep = b4 ? v[k + 5] : v[k];
+        u[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    u[5] = 0.0f;
+    float w[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float send = b3 ? u[k] : u[k + 3], keep = b3 ? u[k + 3] : u[k];
+        w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    w[3] = 0.0f;
+    float x[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float send = b2 ? w[k] : w[k + 2], keep = b2 ? w[k + 2] : w[k];
+        x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    const float send = b1 ? x[0] : x[1], keep = b1 ? x[1] : x[0];
+    float y = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    y += __shfl_xor_sync(0xffffffffu, y, 1);
+    const int j = (b3 ? 3 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+    const int idx = (b4 ? 5 : 0) + j;
+    const bool valid = !(lane & 1) && (b3 ? j <= 4 : j <= 2) && idx < 9;
+    if (valid) atomicAdd(acc_cell + idx, y);
 }
 
 }  // namespace
@@ -437,8 +478,7 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
 __global__ void __launch_bounds__(256)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint32_t *__restrict__ vals, const float4 *__restrict__ saved,
-            const float4 *__restrict__ grad_out, float4 *__restrict__ accA,
-            float4 *__restrict__ accB, float *__restrict__ accC)
+            const float4 *__restrict__ grad_out, float *__restrict__ acc)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
@@ -468,7 +508,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
-            clip_interval(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
+            clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
             const bool seg = g.dt > 0.0f;
             if (!__any_sync(0xffffffffu, seg)) continue;
             OwnGrad o = {0, 0, 0, 0, 0};
@@ -493,21 +533,24 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 const float gdt = dtau * sig;
                 if (gdt != 0.0f) {
                     const float rad = S.r[j];
-                    const float tout = __fdividef(g.hi_n, g.hi_d), tin = __fdividef(g.lo_n, g.lo_d);
-                    end_grad(P.R, g, g.hi_q, tout, g.hi_d, gdt, rad, ds.edges, ds.nbr_idx, accA, o);
-                    end_grad(P.R, g, g.lo_q, tin, -g.lo_d, -gdt, rad, ds.edges, ds.nbr_idx, accA, o);
+                    end_grad(P.R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o);
+                    end_grad(P.R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o);
                 }
                 if (T < kTStop) done = true;
             }
-            // own-cell terms: warp reduction, one lane issues the atomics
-            const float v0 = warp_sum(o.px), v1 = warp_sum(o.py), v2 = warp_sum(o.pz);
-            const float v3 = warp_sum(o.w), v4 = warp_sum(o.r), v5 = warp_sum(gs);
-            const float v6 = warp_sum(gR), v7 = warp_sum(gG), v8 = warp_sum(gB);
-            if (lane == 0) {
-                const uint32_t cell = S.cell[j];
-                atomicAdd(accA + cell, make_float4(v0, v1, v2, v3));
-                atomicAdd(accB + cell, make_float4(v4, v5, v6, v7));
-                atomicAdd(accC + cell, v8);
+            // own-cell terms: one lane alone issues its atomics, else a
+            // transposing warp reduction then one 9-lane atomic instruction
+            float *accc = acc + 12 * (size_t)S.cell[j];
+            const unsigned sm = __ballot_sync(0xffffffffu, seg);
+            if (__popc(sm) == 1) {
+                if (seg) {
+                    atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
+                    atomicAdd(reinterpret_cast<float4 *>(accc) + 1, make_float4(o.r, gs, gR, gG));
+                    atomicAdd(accc + 8, gB);
+                }
+            } else {
+                float v[10] = {o.px, o.py, o.pz, o.w, o.r, gs, gR, gG, gB, 0.0f};
+                warp_reduce9_atomic(v, accc, lane);
             }
             if (__all_sync(0xffffffffu, done)) break;
         }
@@ -518,14 +561,10 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
 {
     int T = v.cam.tiles_x * v.cam.tiles_y;
-    int64_t N = s->ds.N;
-    float4 *accA = s->acc.as<float4>();
-    float4 *accB = accA + N;
-    float *accC = reinterpret_cast<float *>(accB + N);
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
     k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.vals.as<uint32_t>(),
-                                   v.saved.as<float4>(), (const float4 *)grad_out, accA, accB, accC);
+                                   v.saved.as<float4>(), (const float4 *)grad_out, s->acc.as<float>());
     ++s->launches;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();
@@ -535,13 +574,12 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
 // K8: add the packed accumulators into the caller's arrays (+=)
 // ------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
-k8_unpack(int64_t N, const float4 *__restrict__ accA, const float4 *__restrict__ accB,
-          const float *__restrict__ accC, float *gs, float *gw, float *gr, float *gd, float *gc)
+k8_unpack(int64_t N, const float4 *__restrict__ acc, float *gs, float *gw, float *gr, float *gd,
+          float *gc)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    float4 a = accA[i], b = accB[i];
-    float c = accC[i];
+    const float4 a = acc[3 * i], b = acc[3 * i + 1], c = acc[3 * i + 2];
     gs[3 * i + 0] += a.x;
     gs[3 * i + 1] += a.y;
     gs[3 * i + 2] += a.z;
@@ -550,19 +588,16 @@ k8_unpack(int64_t N, const float4 *__restrict__ accA, const float4 *__restrict__
     gd[i] += b.y;
     gc[3 * i + 0] += b.z;
     gc[3 * i + 1] += b.w;
-    gc[3 * i + 2] += c;
+    gc[3 * i + 2] += c.x;
 }
 
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
                           cudaStream_t st)
 {
     int64_t N = s->ds.N;
-    float4 *accA = s->acc.as<float4>();
-    float4 *accB = accA + N;
-    float *accC = reinterpret_cast<float *>(accB + N);
     cudaEvent_t ev;
     stage_begin(s, 8, st, &ev);
-    k8_unpack<<<ceil_div(N, 256), 256, 0, st>>>(N, accA, accB, accC, gs, gw, gr, gd, gc);
+    k8_unpack<<<ceil_div(N, 256), 256, 0, st>>>(N, s->acc.as<float4>(), gs, gw, gr, gd, gc);
     ++s->launches;
     stage_end(s, 8, st, ev);
     return cudaGetLastError();
