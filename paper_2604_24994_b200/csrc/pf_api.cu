@@ -105,7 +105,7 @@ int emit_sort_ranges(pf_scene *s, pf::ViewState &v, cudaStream_t st, uint64_t **
     PF_CUDA(v.ranges.reserve(sizeof(uint2) * (size_t)T));
     *keys_out = nullptr;
     if (P == 0) {
-        PF_CUDA(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(uint2) * (size_t)T, st));
+        PF_CUDA(pf::launch_ranges(s, v, nullptr, st));
         return PF_OK;
     }
     size_t p = (size_t)P;

@@ -56,6 +56,7 @@ struct ViewState {
     int64_t P = 0;
     DevBuf rect, count, keybits, offsets;   // binning of this view (N-sized)
     DevBuf vals, ranges;                     // sorted cell ids, per-tile [start,end)
+    DevBuf order;                            // tiles by decreasing list length (K6/K7 grid order)
     DevBuf saved;                            // float4[H*W] final (C + T bg, T)
 };
 

@@ -369,16 +369,49 @@ __global__ void __launch_bounds__(256) k5_ranges(const unsigned long long *__res
     if (q == P - 1 || (uint32_t)(keys[q + 1] >> 32) != t) ranges[t].y = (uint32_t)(q + 1);
 }
 
+// Grid order for K6/K7: tiles by decreasing list length (longest-processing-time
+// first, so the long tiles do not form the tail of the launch).  Order within a
+// length bucket is arbitrary: tiles are independent, results do not depend on it.
+__global__ void __launch_bounds__(1024) k5_tile_order(const uint2 *__restrict__ ranges, int T,
+                                                      uint32_t *__restrict__ order)
+{
+    __shared__ int hist[64], off[64];
+    if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+    __syncthreads();
+    auto bucket = [](uint32_t len) { return min(63, (int)(5.0f * __log2f((float)len + 1.0f))); };
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        atomicAdd(&hist[bucket(r.y - r.x)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 63; b >= 0; --b) {
+            off[b] = run;
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        order[atomicAdd(&off[bucket(r.y - r.x)], 1)] = (uint32_t)t;
+    }
+}
+
 cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaStream_t st)
 {
     int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaError_t err = cudaMemsetAsync(v.ranges.ptr, 0, sizeof(uint2) * (size_t)T, st);
     if (err != cudaSuccess) return err;
-    if (v.P == 0) return cudaSuccess;
+    if ((err = v.order.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
     cudaEvent_t ev;
     stage_begin(s, 5, st, &ev);
-    k5_ranges<<<ceil_div(v.P, 256), 256, 0, st>>>((const unsigned long long *)keys, v.P,
-                                                   v.ranges.as<uint2>());
+    if (v.P > 0) {
+        k5_ranges<<<ceil_div(v.P, 256), 256, 0, st>>>((const unsigned long long *)keys, v.P,
+                                                       v.ranges.as<uint2>());
+        ++s->launches;
+    }
+    k5_tile_order<<<1, 1024, 0, st>>>(v.ranges.as<uint2>(), T, v.order.as<uint32_t>());
     ++s->launches;
     stage_end(s, 5, st, ev);
     return cudaGetLastError();

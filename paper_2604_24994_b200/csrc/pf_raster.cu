@@ -304,6 +304,14 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
         S.eb[lane] = E.x;
         S.deg[lane] = E.y;
         S.cell[lane] = cell;
+        // pull the cell's edge records (and neighbour ids) towards L1 while the
+        // warp walks the earlier cells of the chunk
+        if (E.y) {
+            const float4 *ep = ds.edges + E.x;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(ep));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + (E.y - 1)));
+            if (E.y > 8) asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + (E.y >> 1)));
+        }
     }
     __syncwarp();
     return m;
@@ -317,13 +325,13 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
 template <bool kCount>
 __global__ void __launch_bounds__(256)
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
-           const uint32_t *__restrict__ vals, float4 *__restrict__ out, float4 *__restrict__ saved,
-           long long *__restrict__ counters)
+           const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
+           float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
-    const int tile = blockIdx.x, lane = threadIdx.x & 31;
+    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31;
     WarpStage &S = WS[threadIdx.x >> 5];
     WarpCtx &W = WC[threadIdx.x >> 5];
     PixelSetup P;
@@ -383,12 +391,12 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
     if (counters)
-        k6_forward<true><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.vals.as<uint32_t>(),
+        k6_forward<true><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
                                             (float4 *)out, v.saved.as<float4>(),
                                             (long long *)counters);
     else
         k6_forward<false><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(),
-                                             v.vals.as<uint32_t>(), (float4 *)out,
+                                             v.order.as<uint32_t>(), v.vals.as<uint32_t>(), (float4 *)out,
                                              v.saved.as<float4>(), nullptr);
     ++s->launches;
     stage_end(s, 6, st, ev);
@@ -475,15 +483,16 @@ __device__ __forceinline__ void warp_reduce9_atomic(float v[10], float *acc_cell
 
 }  // namespace
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
-            const uint32_t *__restrict__ vals, const float4 *__restrict__ saved,
+            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
+            const float4 *__restrict__ saved,
             const float4 *__restrict__ grad_out, float *__restrict__ acc)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
-    const int tile = blockIdx.x, lane = threadIdx.x & 31;
+    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31;
     WarpStage &S = WS[threadIdx.x >> 5];
     WarpCtx &W = WC[threadIdx.x >> 5];
     PixelSetup P;
@@ -563,7 +572,7 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
     int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.vals.as<uint32_t>(),
+    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
                                    v.saved.as<float4>(), (const float4 *)grad_out, s->acc.as<float>());
     ++s->launches;
     stage_end(s, 7, st, ev);
