@@ -165,11 +165,9 @@ def run_reference(args):
     cams = workload_cameras(wl, nv, 1, 0)
     res = cpu_baseline(sc, cams[0], args.cpu_seconds, train=wl != "mip360_1m")
     steps = []
-    for _ in range(max(args.warmup, 0)):
-        pass
     for _ in range(args.steps):
         r = cpu_baseline(sc, cams[0], args.cpu_seconds / max(args.steps, 1), train=wl != "mip360_1m",
-                         calib=res)
+                         calib=res["calib"])
         steps.append(r["value"])
     val = float(np.median(steps)) if steps else res["value"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 0,
@@ -184,16 +182,19 @@ def run_reference(args):
 
 
 def cpu_baseline(sc, cam, seconds, train=True, calib=None):
-    """Times the oracle (O3 tile-list mode, double, OpenMP over pixels) on a
-    bounded sample of pixel rows of one view; extrapolates to frames/s."""
+    """Times the oracle (O3 tile-list mode, double, OpenMP over all host cores) on
+    a bounded sample of pixel rows of one view and extrapolates to frames/s.
+    Each oracle call rebuilds its own fp32 binning (a fixed per-frame cost A), so
+    two samples of different size give A and the per-pixel cost B:
+    frame time = A + B * W * H  (forward + backward when train)."""
     import oracle
     import pf_synth
     H, W = cam.height, cam.width
     g = pf_synth.make_grad_out(1, H, W, seed=12)[0]
 
     def run(rows):
-        y = np.arange(rows) * max(H // max(rows, 1), 1)
-        y = y[y < H][:rows]
+        y = (np.arange(rows) * max(H // max(rows, 1), 1))[:rows]
+        y = y[y < H]
         pix = np.stack(np.meshgrid(np.arange(W), y), -1).reshape(-1, 2)
         t0 = time.perf_counter()
         oracle.render(sc, cam, mode=oracle.O3, pixels=pix)
@@ -203,17 +204,35 @@ def cpu_baseline(sc, cam, seconds, train=True, calib=None):
 
     if calib is None:
         t1, n1 = run(2)
-        per_px = max(t1 / n1, 1e-9)
-    else:
-        per_px = calib["per_px"]
-    rows = int(max(1, min(H, seconds / per_px / W)))
+        t1b, n1b = run(8)
+        B = max((t1b - t1) / max(n1b - n1, 1), 1e-9)
+        A = max(t1 - B * n1, 0.0)
+        calib = {"A": A, "B": B}
+    A, B = calib["A"], calib["B"]
+    rows = int(max(4, min(H, (seconds - A) / B / W)))
     t, n = run(rows)
-    frac = n / float(H * W)
-    fps = frac / t
-    return {"value": fps, "per_px": t / n, "cores": oracle.num_threads(),
-            "sample": f"{n} pixels ({rows} rows) of one {W}x{H} view, O3 "
-                      f"{'forward+backward' if train else 'forward'} incl. its own binning, "
-                      f"{t:.1f}s; frames/s extrapolated from the pixel fraction"}
+    # refine the per-pixel cost with the big sample (A from the calibration)
+    B2 = max((t - A) / n, 1e-12)
+    frame = A + B2 * W * H
+    return {"value": 1.0 / frame, "calib": {"A": A, "B": B2}, "cores": oracle.num_threads(),
+            "sample": f"{n} pixels ({rows} rows) of one {W}x{H} view, oracle O3 "
+                      f"{'forward+backward' if train else 'forward'} in {t:.1f}s; "
+                      f"per-frame fixed cost (own fp32 binning) {A:.2f}s + {B2 * 1e6:.2f}us/pixel "
+                      f"-> {frame:.1f}s per frame"}
+
+
+def load_traffic(kernel_tag):
+    """DRAM bytes per launch of a kernel from the newest committed ncu export."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        if kernel_tag in d:
+            return d[kernel_tag]["traffic_bytes"], d[kernel_tag]["source"]
+    return None, None
 
 
 # ----------------------------------------------------------------------------
@@ -248,13 +267,13 @@ def main():
     out = torch.empty((nv, H, W, 4), device=dev, dtype=torch.float32)
     stream = torch.cuda.current_stream()
 
+    from paper_2604_24994_b200 import dist as pfd
+
     def step():
-        r.forward(cams, out=out)
         if train:
-            flat.zero_()
-            r.backward(cams, grad_out, flat)
-            if ws > 1:
-                dist.all_reduce(flat)
+            pfd.train_step(r, cams, grad_out, flat, out=out)   # fwd, bwd, NCCL all-reduce
+        else:
+            r.forward(cams, out=out)
 
     def barrier():
         if ws > 1:
@@ -307,18 +326,19 @@ def main():
     # ---------------- end to end: host buffers through the public API -------
     e2e = None
     if not args.no_e2e:
-        g_host = grad_out.cpu().pin_memory()
-        grad_host = torch.empty(9 * N, dtype=torch.float32).pin_memory()
+        g_host = grad_out.cpu().pin_memory() if train else None
+        res_host = (torch.empty(9 * N, dtype=torch.float32) if train
+                    else torch.empty(out.shape, dtype=torch.float32)).pin_memory()
         g_dev = torch.empty_like(grad_out)
 
         def e2e_step():
-            g_dev.copy_(g_host, non_blocking=True)
-            r.forward(cams, out=out)
-            flat.zero_()
-            r.backward(cams, g_dev, flat)
-            if ws > 1:
-                dist.all_reduce(flat)
-            grad_host.copy_(flat, non_blocking=True)
+            if train:   # the step's dL/dimage arrives from the host, grads go back
+                g_dev.copy_(g_host, non_blocking=True)
+                pfd.train_step(r, cams, g_dev, flat, out=out)
+                res_host.copy_(flat, non_blocking=True)
+            else:       # forward-only: the rendered images go back to the host
+                r.forward(cams, out=out)
+                res_host.copy_(out, non_blocking=True)
 
         for _ in range(2):
             e2e_step()
@@ -333,10 +353,11 @@ def main():
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": ws * nv / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(g_host.numel() * 4),
-               "d2h_bytes_per_step": int(grad_host.numel() * 4),
-               "note": "H2D of the step's dL/dimage from pinned host + fwd + bwd "
-                       "(+ all-reduce) + D2H of the per-cell gradients, every step"}
+               "h2d_bytes_per_step": int(g_host.numel() * 4) if train else 64 * nv,
+               "d2h_bytes_per_step": int(res_host.numel() * 4),
+               "note": ("H2D of the step's dL/dimage from pinned host + fwd + bwd "
+                        "(+ all-reduce) + D2H of the per-cell gradients, every step") if train
+               else "fwd through the C-ABI (host cameras) + D2H of the rendered images, every step"}
 
     # ---------------- counters -> algorithmic flops, roofline ----------------
     cnt = np.zeros(4)
@@ -354,9 +375,11 @@ def main():
     d_avg = d_ms / max(d_n, 1)
     d_flops = f_bwd if dom == "K7_backward" else f_fwd
     achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
+    traffic, traffic_src = load_traffic("k7" if dom == "K7_backward" else "k6")
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
-                "traffic": None,
+                "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write)",
+                "traffic_source": traffic_src,
                 "peak_note": f"FP32 = {SM_COUNT} SM x {FP32_LANES_PER_SM} lanes x 2 x "
                              f"{sm_max:.0f} MHz (guide unit counts; no tensor-core path)",
                 "avg_launch_ms": d_avg,
