@@ -58,8 +58,10 @@ enum {
 enum {
     PF_VALIDATE = 1u << 0,     /* check the scene on the device at creation (finite values,
                                   r > 0, sigma >= 0, neighbour ids in [0,N) and != i) */
-    PF_STATIC_SCENE = 1u << 1  /* parameters never change after creation: the edge records
+    PF_STATIC_SCENE = 1u << 1, /* parameters never change after creation: the edge records
                                   (K0) are built once in pf_create_scene, not per forward */
+    PF_INFERENCE = 1u << 2     /* forward only: no per-view state is saved for a backward
+                                  (pf_render_backward then returns PF_ERR_STATE) */
 };
 
 /*

@@ -16,10 +16,11 @@ import torch
 from . import _build
 
 __all__ = ["PFError", "Renderer", "render", "load_library", "PF_VALIDATE", "PF_STATIC_SCENE",
-           "STAGES"]
+           "PF_INFERENCE", "STAGES"]
 
 PF_VALIDATE = 1
 PF_STATIC_SCENE = 2
+PF_INFERENCE = 4
 STAGES = ["K0_edge_records", "K1_preprocess", "K2_scan", "K3_emit", "K4_sort", "K5_ranges",
           "K6_forward", "K7_backward", "K8_unpack"]
 _STATUS = {0: "PF_OK", 1: "PF_ERR_INVALID_ARGUMENT", 2: "PF_ERR_CUDA",
@@ -59,6 +60,9 @@ def load_library(build_if_missing: bool = True):
     if _lib is not None:
         return _lib
     path = _build.LIB
+    if os.environ.get("PF_LIBRARY_PATH"):      # A/B variant of the same sources
+        path = os.environ["PF_LIBRARY_PATH"]
+        build_if_missing = False
     if build_if_missing:
         try:
             path = _build.build()

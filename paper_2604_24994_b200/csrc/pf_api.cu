@@ -331,8 +331,23 @@ int pf_destroy(pf_scene *s)
         v.vals.release();
         v.ranges.release();
         v.saved.release();
+        v.order.release();
+        v.chunk_off.release();
+        v.desc.release();
+        v.wdone.release();
+        v.rec.release();
     }
+    s->debug_view.rect.release();
+    s->debug_view.count.release();
+    s->debug_view.keybits.release();
+    s->debug_view.offsets.release();
+    s->debug_view.vals.release();
+    s->debug_view.ranges.release();
+    s->debug_view.order.release();
+    s->debug_view.chunk_off.release();
+    s->rec_used.release();
     if (s->pinned) cudaFreeHost(s->pinned);
+    if (s->pinned_rec) cudaFreeHost(s->pinned_rec);
     for (auto &e : s->events) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -366,16 +381,53 @@ int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
     int rc = bin_views(s, V, st);
     if (rc) return rc;
     const size_t npix = (size_t)cams[0].width * cams[0].height;
+    const bool record = !(s->flags & PF_INFERENCE);
+    if (record) {
+        // adapt the record-arena size to what the previous forward used
+        if (s->rec_seen_views > 0) {
+            for (int v = 0; v < s->rec_seen_views; ++v) {
+                const pf::ViewState &pv = s->views[v];
+                const uint32_t used = s->pinned_rec[v];
+                if (pv.P > 0 && used > 0)
+                    s->rec_ratio = fmax(s->rec_ratio * 0.98, 1.3 * (double)used / (double)pv.P);
+            }
+        }
+        PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * (size_t)V));
+        PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * (size_t)V, st));
+    }
     for (int v = 0; v < V; ++v) {
         pf::ViewState &vs = s->views[v];
         uint64_t *ks = nullptr;
         rc = emit_sort_ranges(s, vs, st, &ks);
         if (rc) return rc;
-        PF_CUDA(vs.saved.reserve(16 * npix));
-        PF_CUDA(pf::launch_forward(s, vs, out + 4 * npix * (size_t)v, nullptr, st));
+        uint32_t *used = nullptr;
+        if (record) {
+            const int T = vs.cam.tiles_x * vs.cam.tiles_y;
+            PF_CUDA(vs.saved.reserve(16 * npix));
+            const size_t chunks = (size_t)(vs.P / 32 + T + 1);
+            PF_CUDA(vs.desc.reserve(sizeof(uint2) * 8 * chunks));
+            PF_CUDA(vs.wdone.reserve(sizeof(uint32_t) * 8 * (size_t)T));
+            vs.rec_cap = (int64_t)(s->rec_ratio * (double)vs.P) + 1024;
+            if (vs.rec_cap > (int64_t)0xFFFFFFF0ll) vs.rec_cap = 0xFFFFFFF0ll;
+            PF_CUDA(vs.rec.reserve(72 * (size_t)vs.rec_cap));
+            used = s->rec_used.as<uint32_t>() + v;
+        }
+        PF_CUDA(pf::launch_forward(s, vs, out + 4 * npix * (size_t)v, nullptr, used, st));
+    }
+    if (record) {
+        if (s->pinned_rec_n < V) {
+            if (s->pinned_rec) cudaFreeHost(s->pinned_rec);
+            s->pinned_rec = nullptr;
+            s->pinned_rec_n = 0;
+            PF_CUDA(cudaMallocHost(&s->pinned_rec, sizeof(uint32_t) * (size_t)(V + 16)));
+            s->pinned_rec_n = V + 16;
+        }
+        PF_CUDA(cudaMemcpyAsync(s->pinned_rec, s->rec_used.ptr, sizeof(uint32_t) * (size_t)V,
+                                cudaMemcpyDeviceToHost, st));
+        s->rec_seen_views = V;   // read at the next forward, after its sync
     }
     s->fwd_cams.assign(cams, cams + V);
-    s->fwd_views = V;
+    s->fwd_views = record ? V : 0;
     return PF_OK;
 }
 
@@ -478,7 +530,7 @@ int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_s
     rc = emit_sort_ranges(s, vs, st, &ks);
     if (rc) return rc;
     PF_CUDA(cudaMemsetAsync(counters, 0, 32 * (size_t)cam->width * cam->height, st));
-    PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, st));
+    PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, nullptr, st));
     PF_CUDA(cudaStreamSynchronize(st));
     return PF_OK;
 }

@@ -57,6 +57,11 @@ struct ViewState {
     DevBuf rect, count, keybits, offsets;   // binning of this view (N-sized)
     DevBuf vals, ranges;                     // sorted cell ids, per-tile [start,end)
     DevBuf order;                            // tiles by decreasing list length (K6/K7 grid order)
+    DevBuf chunk_off;                        // first 32-entry chunk of each tile
+    // K6 -> K7 segment records (see pf_raster.cu): per (warp, chunk) descriptor
+    // (first record, count | kOverflow), chunks walked per warp, the record arena
+    DevBuf desc, wdone, rec;
+    int64_t rec_cap = 0;                     // records the arena holds
     DevBuf saved;                            // float4[H*W] final (C + T bg, T)
 };
 
@@ -76,6 +81,10 @@ struct pf_scene {
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
     pf::DevBuf acc;                 // backward packed accumulators
+    pf::DevBuf rec_used;            // u32[V] records used per view (K6 atomics)
+    double rec_ratio = 3.0;         // arena capacity in records per (tile, cell) pair
+    uint32_t *pinned_rec = nullptr; // host copy of rec_used from the previous forward
+    int pinned_rec_n = 0, rec_seen_views = 0;
     std::vector<pf::ViewState> views;
     pf::ViewState debug_view;       // pf_debug_* scratch (leaves the forward state intact)
     std::vector<pf_camera> fwd_cams;
@@ -102,7 +111,7 @@ cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64
                              cudaStream_t st);
 cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaStream_t st);
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           cudaStream_t st);
+                           uint32_t *rec_used, cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
                           cudaStream_t st);

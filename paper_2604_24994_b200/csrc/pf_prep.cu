@@ -372,11 +372,28 @@ __global__ void __launch_bounds__(256) k5_ranges(const unsigned long long *__res
 // Grid order for K6/K7: tiles by decreasing list length (longest-processing-time
 // first, so the long tiles do not form the tail of the launch).  Order within a
 // length bucket is arbitrary: tiles are independent, results do not depend on it.
+// Also writes chunk_off[t] = sum_{t' < t} ceil(len_t' / 32): the first 32-entry
+// chunk of tile t in the per-view chunk-descriptor table of the K6 -> K7 records.
 __global__ void __launch_bounds__(1024) k5_tile_order(const uint2 *__restrict__ ranges, int T,
-                                                      uint32_t *__restrict__ order)
+                                                      uint32_t *__restrict__ order,
+                                                      uint32_t *__restrict__ chunk_off)
 {
     __shared__ int hist[64], off[64];
+    __shared__ long long sw[33];
     if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+    long long carry = 0;
+    for (int base = 0; base < T; base += 1024) {
+        const int t = base + threadIdx.x;
+        long long c = 0;
+        if (t < T) {
+            const uint2 r = ranges[t];
+            c = (r.y - r.x + 31) / 32;
+        }
+        long long tot;
+        const long long ex = block_excl_scan<long long>(c, sw, &tot);
+        if (t < T) chunk_off[t] = (uint32_t)(carry + ex);
+        carry += tot;
+    }
     __syncthreads();
     auto bucket = [](uint32_t len) { return min(63, (int)(5.0f * __log2f((float)len + 1.0f))); };
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
@@ -411,7 +428,9 @@ cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaS
                                                        v.ranges.as<uint2>());
         ++s->launches;
     }
-    k5_tile_order<<<1, 1024, 0, st>>>(v.ranges.as<uint2>(), T, v.order.as<uint32_t>());
+    if ((err = v.chunk_off.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
+    k5_tile_order<<<1, 1024, 0, st>>>(v.ranges.as<uint2>(), T, v.order.as<uint32_t>(),
+                                      v.chunk_off.as<uint32_t>());
     ++s->launches;
     stage_end(s, 5, st, ev);
     return cudaGetLastError();

@@ -254,6 +254,46 @@ __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, Pixe
     __syncwarp();
 }
 
+// Stage cell `cell` into slot `slot` with the warp-centred frame (fp64 -> fp32).
+__device__ __forceinline__ void stage_slot(WarpStage &S, int slot, const DeviceScene &ds,
+                                           uint32_t cell, const float4 A, double c0, double c1,
+                                           double c2, double t, const WarpCtx &W)
+{
+    const float4 B = __ldg(ds.cellB + cell);
+    const uint2 E = __ldg(ds.cellE + cell);
+    S.t0[slot] = __double2float_rn(t);
+    S.e0x[slot] = __double2float_rn(__fma_rn(-t, W.wx, c0));
+    S.e0y[slot] = __double2float_rn(__fma_rn(-t, W.wy, c1));
+    S.e0z[slot] = __double2float_rn(__fma_rn(-t, W.wz, c2));
+    S.cx[slot] = __double2float_rn(c0);
+    S.cy[slot] = __double2float_rn(c1);
+    S.cz[slot] = __double2float_rn(c2);
+    S.r[slot] = A.w;
+    S.sig[slot] = B.x;
+    S.cr[slot] = B.y;
+    S.cg[slot] = B.z;
+    S.cb[slot] = B.w;
+    S.eb[slot] = E.x;
+    S.deg[slot] = E.y;
+    S.cell[slot] = cell;
+    // pull the cell's edge records towards L1 while the warp walks earlier cells
+    if (E.y) {
+        const float4 *ep = ds.edges + E.x;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ep));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + (E.y - 1)));
+        if (E.y > 8) asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + (E.y >> 1)));
+    }
+}
+
+__device__ __forceinline__ double cell_offset(const CamParams &cam, const float4 A, const WarpCtx &W,
+                                              double &c0, double &c1, double &c2)
+{
+    c0 = __dsub_rn((double)A.x, (double)cam.M[3]);
+    c1 = __dsub_rn((double)A.y, (double)cam.M[7]);
+    c2 = __dsub_rn((double)A.z, (double)cam.M[11]);
+    return __fma_rn(W.wx, c0, __fma_rn(W.wy, c1, __dmul_rn(W.wz, c2)));
+}
+
 // Lane `lane` takes list entry e (if < end): conservative sphere-vs-warp-cone
 // test in fp64; survivors are staged in slot `lane`.  Returns the ballot.
 // Cone test: the sphere (c, r) meets the cone (axis d_w, half-angle th) iff
@@ -271,10 +311,7 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
     if (e < end) {
         cell = __ldg(vals + e);
         A = __ldg(ds.cellA + cell);
-        c0 = __dsub_rn((double)A.x, (double)cam.M[3]);
-        c1 = __dsub_rn((double)A.y, (double)cam.M[7]);
-        c2 = __dsub_rn((double)A.z, (double)cam.M[11]);
-        t = __fma_rn(W.wx, c0, __fma_rn(W.wy, c1, __dmul_rn(W.wz, c2)));
+        t = cell_offset(cam, A, W, c0, c1, c2);
         const double cc = __fma_rn(c0, c0, __fma_rn(c1, c1, __dmul_rn(c2, c2)));
         const double rr = (double)A.w;
         const double r2 = __dmul_rn(rr, rr);
@@ -286,35 +323,38 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
         }
     }
     const unsigned m = __ballot_sync(0xffffffffu, pass);
-    if (pass) {
-        const float4 B = __ldg(ds.cellB + cell);
-        const uint2 E = __ldg(ds.cellE + cell);
-        S.t0[lane] = __double2float_rn(t);
-        S.e0x[lane] = __double2float_rn(__fma_rn(-t, W.wx, c0));
-        S.e0y[lane] = __double2float_rn(__fma_rn(-t, W.wy, c1));
-        S.e0z[lane] = __double2float_rn(__fma_rn(-t, W.wz, c2));
-        S.cx[lane] = __double2float_rn(c0);
-        S.cy[lane] = __double2float_rn(c1);
-        S.cz[lane] = __double2float_rn(c2);
-        S.r[lane] = A.w;
-        S.sig[lane] = B.x;
-        S.cr[lane] = B.y;
-        S.cg[lane] = B.z;
-        S.cb[lane] = B.w;
-        S.eb[lane] = E.x;
-        S.deg[lane] = E.y;
-        S.cell[lane] = cell;
-        // pull the cell's edge records (and neighbour ids) towards L1 while the
-        // warp walks the earlier cells of the chunk
-        if (E.y) {
-            const float4 *ep = ds.edges + E.x;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(ep));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + (E.y - 1)));
-            if (E.y > 8) asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + (E.y >> 1)));
-        }
-    }
+    if (pass) stage_slot(S, lane, ds, cell, A, c0, c1, c2, t, W);
     __syncwarp();
     return m;
+}
+
+// ---------------------------------------------------------------------------
+// K6 -> K7 segment records.  For every 32-entry chunk of its tile list a warp
+// walked, K6 writes a descriptor (first record, count); for every chunk entry
+// that produced a non-empty segment in at least one lane it writes a 72-byte
+// record: the lane mask, the entry's position in the chunk, and per lane the
+// binding constraints of the interval (lo, hi) coded in one byte each
+// (0 sphere, 1 near, 2+k plane k of the cell's list, 255 = not codable).  K7
+// then replays only those entries and evaluates only the binding planes: the
+// interval values are bit-identical (fminf/fmaxf return one of their inputs,
+// and the winning input is recomputed with the same instructions).
+// The arena is sized from the pair count; a chunk whose records do not fit is
+// marked kOverflow and K7 recomputes it in full.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kOverflow = 0xffffffffu;
+constexpr int kRecWords = 18;   // mask, pos, 32 x u16 codes
+
+struct WarpRec {
+    uint32_t mask[32], pos[32];
+    uint32_t code[32][16];      // 32 lanes x u16, as 16 words
+};
+
+__device__ __forceinline__ uint32_t end_code(int q, uint32_t eb, bool lo)
+{
+    if (q == kEndSphere) return 0u;
+    if (lo && q == kEndNear) return 1u;
+    const uint32_t k = (uint32_t)q - eb;
+    return k < 253u ? k + 2u : 255u;
 }
 
 }  // namespace
@@ -322,27 +362,40 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
 // ------------------------------------------------------------------------
 // K6 forward
 // ------------------------------------------------------------------------
-template <bool kCount>
-__global__ void __launch_bounds__(256)
+#ifndef PF_K6_MINB
+#define PF_K6_MINB 4
+#endif
+#ifndef PF_K7_MINB
+#define PF_K7_MINB 4
+#endif
+template <bool kCount, bool kRecord>
+__global__ void __launch_bounds__(256, PF_K6_MINB)
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
-           float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters)
+           float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
+           const uint32_t *__restrict__ chunk_off, uint2 *__restrict__ desc,
+           uint32_t *__restrict__ wdone, uint32_t *__restrict__ rec, uint32_t *__restrict__ rec_used,
+           uint32_t rec_cap)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
-    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31;
-    WarpStage &S = WS[threadIdx.x >> 5];
-    WarpCtx &W = WC[threadIdx.x >> 5];
+    __shared__ WarpRec WR[kRecord ? kWarps : 1];
+    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpStage &S = WS[warp];
+    WarpCtx &W = WC[warp];
+    WarpRec &Rb = WR[kRecord ? warp : 0];
     PixelSetup P;
     setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     bool done = !P.valid;
     long long xs = 0, xh = 0, xp = 0, xc = 0;
-    for (uint32_t base = rg.x; base < rg.y; base += 32) {
+    uint32_t chunks = 0;
+    for (uint32_t base = rg.x; base < rg.y; base += 32, ++chunks) {
         if (__all_sync(0xffffffffu, done)) break;
         unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
+        int nrec = 0;
         while (m) {
             const int j = __ffs(m) - 1;
             m &= m - 1;
@@ -350,12 +403,27 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
-            clip_interval<false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
+            clip_interval<kRecord>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
             if (kCount && hit) {
                 ++xh;
                 xp += S.deg[j];
             }
-            if (g.dt > 0.0f) {
+            const bool seg = g.dt > 0.0f;
+            if (kRecord) {
+                const unsigned sm = __ballot_sync(0xffffffffu, seg);
+                if (sm) {
+                    const uint32_t eb = S.eb[j];
+                    const uint32_t c = seg ? (end_code(g.lo_q, eb, true) |
+                                              (end_code(g.hi_q, eb, false) << 8)) : 0u;
+                    reinterpret_cast<uint16_t *>(Rb.code[nrec])[lane] = (uint16_t)c;
+                    if (lane == 0) {
+                        Rb.mask[nrec] = sm;
+                        Rb.pos[nrec] = (uint32_t)j;
+                    }
+                    ++nrec;
+                }
+            }
+            if (seg) {
                 float alpha;
                 composite_step(S.sig[j], g.dt, S.cr[j], S.cg[j], S.cb[j], T, Cr, Cg, Cb, alpha);
                 if (kCount) ++xc;
@@ -366,8 +434,30 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             }
             if (__all_sync(0xffffffffu, done)) break;
         }
+        if (kRecord) {
+            __syncwarp();
+            uint2 d = make_uint2(0u, 0u);
+            if (nrec) {
+                uint32_t b0 = 0;
+                if (lane == 0) b0 = atomicAdd(rec_used, (uint32_t)nrec);
+                b0 = __shfl_sync(0xffffffffu, b0, 0);
+                if ((uint64_t)b0 + nrec <= rec_cap) {
+                    for (int w = lane; w < nrec * kRecWords; w += 32) {
+                        const int k = w / kRecWords, o = w - k * kRecWords;
+                        const uint32_t v = o == 0 ? Rb.mask[k] : (o == 1 ? Rb.pos[k] : Rb.code[k][o - 2]);
+                        rec[(size_t)(b0 + k) * kRecWords + o] = v;
+                    }
+                    d = make_uint2(b0, (uint32_t)nrec);
+                } else {
+                    d = make_uint2(0u, kOverflow);
+                }
+            }
+            if (lane == 0) desc[(size_t)(chunk_off[tile] + chunks) * kWarps + warp] = d;
+            __syncwarp();
+        }
         __syncwarp();
     }
+    if (kRecord && lane == 0) wdone[(size_t)tile * kWarps + warp] = chunks;
     if (P.valid) {
         const float4 o = make_float4(fmaf(T, ds.bg[0], Cr), fmaf(T, ds.bg[1], Cg),
                                      fmaf(T, ds.bg[2], Cb), T);
@@ -385,19 +475,26 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
 }
 
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           cudaStream_t st)
+                           uint32_t *rec_used, cudaStream_t st)
 {
-    int T = v.cam.tiles_x * v.cam.tiles_y;
+    const int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
     if (counters)
-        k6_forward<true><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
-                                            (float4 *)out, v.saved.as<float4>(),
-                                            (long long *)counters);
+        k6_forward<true, false><<<T, 256, 0, st>>>(
+            s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
+            (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
+            nullptr, 0u);
+    else if (rec_used)
+        k6_forward<false, true><<<T, 256, 0, st>>>(
+            s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
+            (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off.as<uint32_t>(),
+            v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
+            (uint32_t)v.rec_cap);
     else
-        k6_forward<false><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(),
-                                             v.order.as<uint32_t>(), v.vals.as<uint32_t>(), (float4 *)out,
-                                             v.saved.as<float4>(), nullptr);
+        k6_forward<false, false><<<T, 256, 0, st>>>(
+            s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
+            (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u);
     ++s->launches;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();
@@ -448,7 +545,7 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
 
 // Sum of 9 per-lane values over the warp by a transposing reduction (12 shuffles
 // instead of 45): after it, the lane with (lane & 1) == 0 and a valid slot holds
-// the warp total of value *idx and issues one atomic; 9 lanes, one instruction.
+// the warp total of one value and issues one atomic; 9 lanes, one instruction.
 __device__ __forceinline__ void warp_reduce9_atomic(float v[10], float *acc_cell, int lane)
 {
     const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
@@ -481,87 +578,174 @@ __device__ __forceinline__ void warp_reduce9_atomic(float v[10], float *acc_cell
     if (valid) atomicAdd(acc_cell + idx, y);
 }
 
+// value of one interval end from its recorded constraint code (see end_code)
+__device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restrict__ edges,
+                                           uint32_t eb, uint32_t code, bool lo, const Seg &g,
+                                           int &q)
+{
+    if (code == 0u) {
+        q = kEndSphere;
+        return lo ? -g.s : g.s;
+    }
+    if (lo && code == 1u) {
+        q = kEndNear;
+        return __fsub_rn(R.tnear, g.tc);
+    }
+    q = (int)(eb + code - 2u);
+    const float4 E = __ldg(edges + q);
+    const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
+    const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
+    return __fmul_rn(b, rcp_approx(a));
+}
+
+// Backward of one segment (lanes with seg) + scatter of the cell's gradients.
+struct BwdPixel {
+    float T, Cr, Cg, Cb;
+    float4 fin, G;
+    float GT_Tfin;
+};
+
+__device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, bool seg,
+                                                 const WarpStage &S, int j, BwdPixel &px,
+                                                 const DeviceScene &ds, float *acc, int lane)
+{
+    OwnGrad o = {0, 0, 0, 0, 0};
+    float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f;
+    if (seg) {
+        const float sig = S.sig[j], cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
+        const float Tk = px.T;
+        float alpha;
+        composite_step(sig, g.dt, cr, cg, cb, px.T, px.Cr, px.Cg, px.Cb, alpha);
+        // px.T is now T_{k+1}; C is C_k; S_k = out_rgb - C_k
+        const float Sr = __fsub_rn(px.fin.x, px.Cr), Sg = __fsub_rn(px.fin.y, px.Cg),
+                    Sb = __fsub_rn(px.fin.z, px.Cb);
+        float dtau = -px.GT_Tfin;
+        dtau = fmaf(px.G.x, fmaf(px.T, cr, -Sr), dtau);
+        dtau = fmaf(px.G.y, fmaf(px.T, cg, -Sg), dtau);
+        dtau = fmaf(px.G.z, fmaf(px.T, cb, -Sb), dtau);
+        const float wa = __fmul_rn(Tk, alpha);
+        gR = wa * px.G.x;
+        gG = wa * px.G.y;
+        gB = wa * px.G.z;
+        gs = dtau * g.dt;
+        const float gdt = dtau * sig;
+        if (gdt != 0.0f) {
+            const float rad = S.r[j];
+            end_grad(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o);
+            end_grad(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o);
+        }
+    }
+    // own-cell terms: one lane alone issues its atomics, else a transposing warp
+    // reduction then one 9-lane atomic instruction
+    float *accc = acc + 12 * (size_t)S.cell[j];
+    const unsigned sm = __ballot_sync(0xffffffffu, seg);
+    if (__popc(sm) == 1) {
+        if (seg) {
+            atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
+            atomicAdd(reinterpret_cast<float4 *>(accc) + 1, make_float4(o.r, gs, gR, gG));
+            atomicAdd(accc + 8, gB);
+        }
+    } else {
+        float v[10] = {o.px, o.py, o.pz, o.w, o.r, gs, gR, gG, gB, 0.0f};
+        warp_reduce9_atomic(v, accc, lane);
+    }
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, PF_K7_MINB)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
-            const float4 *__restrict__ saved,
-            const float4 *__restrict__ grad_out, float *__restrict__ acc)
+            const float4 *__restrict__ saved, const float4 *__restrict__ grad_out,
+            float *__restrict__ acc, const uint32_t *__restrict__ chunk_off,
+            const uint2 *__restrict__ desc, const uint32_t *__restrict__ wdone,
+            const uint32_t *__restrict__ rec)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
-    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31;
-    WarpStage &S = WS[threadIdx.x >> 5];
-    WarpCtx &W = WC[threadIdx.x >> 5];
+    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpStage &S = WS[warp];
+    WarpCtx &W = WC[warp];
     PixelSetup P;
     setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
-    float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
+    BwdPixel px;
+    px.T = 1.0f;
+    px.Cr = px.Cg = px.Cb = 0.0f;
     bool done = !P.valid;
-    float4 fin = make_float4(0, 0, 0, 1), G = make_float4(0, 0, 0, 0);
+    px.fin = make_float4(0, 0, 0, 1);
+    px.G = make_float4(0, 0, 0, 0);
     if (P.valid) {
         const size_t pix = (size_t)P.y * cam.W + P.x;
-        fin = saved[pix];
-        G = grad_out[pix];
+        px.fin = saved[pix];
+        px.G = grad_out[pix];
     }
-    const float GT_Tfin = __fmul_rn(G.w, fin.w);
-    for (uint32_t base = rg.x; base < rg.y; base += 32) {
-        if (__all_sync(0xffffffffu, done)) break;
-        unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1;
+    px.GT_Tfin = __fmul_rn(px.G.w, px.fin.w);
+    const uint32_t nchunks = wdone[(size_t)tile * kWarps + warp];
+    const uint32_t c0 = chunk_off[tile];
+    for (uint32_t c = 0; c < nchunks; ++c) {
+        const uint2 d = desc[(size_t)(c0 + c) * kWarps + warp];
+        if (d.y == 0u) continue;
+        const uint32_t base = rg.x + 32u * c;
+        if (d.y == kOverflow) {
+            // records did not fit: full replay of this chunk (same code as K6)
+            unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                Seg g;
+                bool hit = false;
+                if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
+                if (!__any_sync(0xffffffffu, hit)) continue;
+                clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
+                const bool seg = g.dt > 0.0f;
+                if (!__any_sync(0xffffffffu, seg)) continue;
+                segment_backward(P.R, g, seg, S, j, px, ds, acc, lane);
+                if (seg && px.T < kTStop) done = true;
+            }
+            __syncwarp();
+            continue;
+        }
+        // recorded entries only: stage them (lane k <-> record k)
+        const uint32_t nrec = d.y;
+        const uint32_t *R0 = rec + (size_t)d.x * kRecWords;
+        if (lane < (int)nrec) {
+            const uint32_t pos = __ldg(R0 + (size_t)lane * kRecWords + 1);
+            const uint32_t cell = __ldg(vals + base + pos);
+            const float4 A = __ldg(ds.cellA + cell);
+            double x0, x1, x2;
+            const double t = cell_offset(cam, A, W, x0, x1, x2);
+            stage_slot(S, lane, ds, cell, A, x0, x1, x2, t, W);
+        }
+        __syncwarp();
+        for (uint32_t k = 0; k < nrec; ++k) {
+            const uint32_t *Rk = R0 + (size_t)k * kRecWords;
+            const uint32_t mask = __ldg(Rk);
+            const uint32_t code = __ldg(reinterpret_cast<const uint16_t *>(Rk + 2) + lane);
+            const bool seg = (mask >> lane) & 1u;
+            const int j = (int)k;
             Seg g;
-            bool hit = false;
-            if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
-            if (!__any_sync(0xffffffffu, hit)) continue;
-            clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
-            const bool seg = g.dt > 0.0f;
-            if (!__any_sync(0xffffffffu, seg)) continue;
-            OwnGrad o = {0, 0, 0, 0, 0};
-            float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f;
+            g.dt = 0.0f;
             if (seg) {
-                const float sig = S.sig[j], cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
-                const float Tk = T;
-                float alpha;
-                composite_step(sig, g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
-                // T is now T_{k+1}; C is C_k; S_k = out_rgb - C_k
-                const float Sr = __fsub_rn(fin.x, Cr), Sg = __fsub_rn(fin.y, Cg),
-                            Sb = __fsub_rn(fin.z, Cb);
-                float dtau = -GT_Tfin;
-                dtau = fmaf(G.x, fmaf(T, cr, -Sr), dtau);
-                dtau = fmaf(G.y, fmaf(T, cg, -Sg), dtau);
-                dtau = fmaf(G.z, fmaf(T, cb, -Sb), dtau);
-                const float wa = __fmul_rn(Tk, alpha);
-                gR = wa * G.x;
-                gG = wa * G.y;
-                gB = wa * G.z;
-                gs = dtau * g.dt;
-                const float gdt = dtau * sig;
-                if (gdt != 0.0f) {
-                    const float rad = S.r[j];
-                    end_grad(P.R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o);
-                    end_grad(P.R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o);
-                }
-                if (T < kTStop) done = true;
+                sphere_hit(P.R, S, j, g, ds, cam, PR);   // identical to K6 (recorded hit)
+                const uint32_t eb = S.eb[j];
+                g.lo = coded_end(P.R, ds.edges, eb, code & 0xffu, true, g, g.lo_q);
+                g.hi = coded_end(P.R, ds.edges, eb, code >> 8, false, g, g.hi_q);
             }
-            // own-cell terms: one lane alone issues its atomics, else a
-            // transposing warp reduction then one 9-lane atomic instruction
-            float *accc = acc + 12 * (size_t)S.cell[j];
-            const unsigned sm = __ballot_sync(0xffffffffu, seg);
-            if (__popc(sm) == 1) {
-                if (seg) {
-                    atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
-                    atomicAdd(reinterpret_cast<float4 *>(accc) + 1, make_float4(o.r, gs, gR, gG));
-                    atomicAdd(accc + 8, gB);
+            const bool full = seg && (((code & 0xffu) == 255u) || ((code >> 8) == 255u));
+            if (__any_sync(0xffffffffu, full)) {
+                Seg h = g;
+                if (full) {
+                    clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], h, true);
+                    g = h;
+                } else {
+                    clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], h, false);
                 }
-            } else {
-                float v[10] = {o.px, o.py, o.pz, o.w, o.r, gs, gR, gG, gB, 0.0f};
-                warp_reduce9_atomic(v, accc, lane);
             }
-            if (__all_sync(0xffffffffu, done)) break;
+            if (seg) g.dt = __fsub_rn(g.hi, g.lo);
+            segment_backward(P.R, g, seg, S, j, px, ds, acc, lane);
+            if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();
     }
@@ -572,8 +756,11 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
     int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
-                                   v.saved.as<float4>(), (const float4 *)grad_out, s->acc.as<float>());
+    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(),
+                                   v.vals.as<uint32_t>(), v.saved.as<float4>(),
+                                   (const float4 *)grad_out, s->acc.as<float>(),
+                                   v.chunk_off.as<uint32_t>(), v.desc.as<uint2>(),
+                                   v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
     ++s->launches;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();
