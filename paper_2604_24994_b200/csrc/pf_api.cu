@@ -2,6 +2,7 @@
 // checks, grow-only workspaces, per-view saved state, error strings, stage timing.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -248,6 +249,11 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
         return fail(PF_ERR_CUDA, "no current CUDA device");
     }
     s->flags = d->flags;
+    if (const char *r = getenv("PF_REC_RATIO")) {   // debug knob: K6->K7 record arena size
+        const double v = atof(r);
+        if (v > 0.0) s->rec_ratio = v;
+        s->rec_ratio_fixed = v > 0.0;
+    }
     pf::DeviceScene &ds = s->ds;
     ds.N = d->num_cells;
     ds.E = d->num_edges;
@@ -384,7 +390,7 @@ int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
     const bool record = !(s->flags & PF_INFERENCE);
     if (record) {
         // adapt the record-arena size to what the previous forward used
-        if (s->rec_seen_views > 0) {
+        if (s->rec_seen_views > 0 && !s->rec_ratio_fixed) {
             for (int v = 0; v < s->rec_seen_views; ++v) {
                 const pf::ViewState &pv = s->views[v];
                 const uint32_t used = s->pinned_rec[v];
@@ -407,7 +413,7 @@ int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
             const size_t chunks = (size_t)(vs.P / 32 + T + 1);
             PF_CUDA(vs.desc.reserve(sizeof(uint2) * 8 * chunks));
             PF_CUDA(vs.wdone.reserve(sizeof(uint32_t) * 8 * (size_t)T));
-            vs.rec_cap = (int64_t)(s->rec_ratio * (double)vs.P) + 1024;
+            vs.rec_cap = (int64_t)(s->rec_ratio * (double)vs.P) + (s->rec_ratio_fixed ? 0 : 1024);
             if (vs.rec_cap > (int64_t)0xFFFFFFF0ll) vs.rec_cap = 0xFFFFFFF0ll;
             PF_CUDA(vs.rec.reserve(72 * (size_t)vs.rec_cap));
             used = s->rec_used.as<uint32_t>() + v;

@@ -200,6 +200,41 @@ def test_backward_large_sampled_pixels(name):
     r.close()
 
 
+def test_inference_forward_equals_training_forward():
+    import paper_2604_24994_b200 as pf
+    sc, cams = case("small360")
+    r = renderer(sc)
+    ri = renderer(sc, flags=pf.PF_INFERENCE)
+    a = r.forward(cams).cpu().numpy()
+    b = ri.forward(cams).cpu().numpy()
+    assert np.array_equal(a, b)
+    g = torch.zeros((len(cams), cams[0].height, cams[0].width, 4), device="cuda")
+    with pytest.raises(pf.PFError) as e:
+        ri.backward(cams, g)
+    assert e.value.status == 4
+    r.close()
+    ri.close()
+
+
+def test_backward_record_overflow_fallback(monkeypatch):
+    """K6->K7 record arena too small: overflowed chunks are recomputed in full by
+    K7; gradients must be unchanged (parity with the oracle)."""
+    monkeypatch.setenv("PF_REC_RATIO", "0.02")
+    sc, cams = case("small360")
+    r = renderer(sc)
+    cams = cams[:2]
+    H, W = cams[0].height, cams[0].width
+    g = pf_synth.make_grad_out(len(cams), H, W, seed=11)
+    r.forward(cams)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    ref = None
+    for v, cam in enumerate(cams):
+        o = oracle.backward(sc, cam, g[v], mode=oracle.O3)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+
+
 def test_backward_requires_matching_forward():
     import paper_2604_24994_b200 as pf
     sc, cams = case("tiny")
