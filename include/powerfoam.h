@@ -150,6 +150,8 @@ PF_API const char *pf_last_error(void);
  *   keys u64[P], vals u32[P] (sorted), ranges u32[T,2] ([start,end), (0,0) empty).
  * *num_pairs (host) receives P.  If keys == NULL only rect/count/keybits and P
  * are produced (so the caller can size keys/vals).  Synchronizes the stream.
+ * The debug exports reuse the forward's sorted-pair workspace: a following
+ * pf_render_backward returns PF_ERR_STATE until the next pf_render_forward.
  */
 PF_API int pf_debug_binning(pf_scene *s, const pf_camera *cam, int32_t *rect, int32_t *count,
                      uint32_t *keybits, uint64_t *keys, uint32_t *vals, uint32_t *ranges,

@@ -97,31 +97,51 @@ int reserve_view_bins(pf_scene *s, pf::ViewState &v)
     return PF_OK;
 }
 
-// K3..K5 of one view whose K1/K2 already ran and whose v.P is known.
-// Leaves the sorted keys in *keys_out (scratch) and the sorted values in v.vals.
-int emit_sort_ranges(pf_scene *s, pf::ViewState &v, cudaStream_t st, uint64_t **keys_out)
+// K3..K5 for views [0, V) of this call (K1/K2 ran, every v.P is known): the pairs
+// of all views are emitted into one array with the view id above the tile bits,
+// sorted once, and split into per-view tile ranges.  Leaves the sorted keys in
+// *keys_out (scratch) and the sorted cell ids in s->vals_all.
+int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
+                     uint64_t **keys_out)
 {
-    const int64_t P = v.P;
-    const int T = v.cam.tiles_x * v.cam.tiles_y;
-    PF_CUDA(v.ranges.reserve(sizeof(uint2) * (size_t)T));
-    *keys_out = nullptr;
-    if (P == 0) {
-        PF_CUDA(pf::launch_ranges(s, v, nullptr, st));
-        return PF_OK;
+    const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
+    const int tb = tile_bits(T);
+    int vb = 0;
+    while ((1 << vb) < V) ++vb;
+    if (32 + tb + vb > 64) return fail(PF_ERR_INVALID_ARGUMENT, "too many views for 64-bit keys");
+    int64_t Ptot = 0;
+    for (int v = 0; v < V; ++v) {
+        views[v].pair_off = Ptot;
+        Ptot += views[v].P;
     }
-    size_t p = (size_t)P;
+    if (Ptot >= (int64_t)0xFFFFFFFFll)
+        return fail(PF_ERR_OUT_OF_MEMORY, "pair count of one call exceeds 2^32");
+    const size_t p = (size_t)(Ptot > 0 ? Ptot : 1);
     PF_CUDA(s->keys0.reserve(8 * p));
     PF_CUDA(s->keys1.reserve(8 * p));
     PF_CUDA(s->vals1.reserve(4 * p));
-    PF_CUDA(v.vals.reserve(4 * p));
+    PF_CUDA(s->vals_all.reserve(4 * p));
+    PF_CUDA(s->ranges_all.reserve(sizeof(uint2) * (size_t)T * V));
     uint64_t *k0 = s->keys0.as<uint64_t>(), *k1 = s->keys1.as<uint64_t>();
-    uint32_t *v0 = v.vals.as<uint32_t>(), *v1 = s->vals1.as<uint32_t>();
-    PF_CUDA(pf::launch_emit(s, v, k0, v0, st));
+    uint32_t *v0 = s->vals_all.as<uint32_t>(), *v1 = s->vals1.as<uint32_t>();
+    for (int v = 0; v < V; ++v) {
+        if (views[v].P == 0) continue;
+        PF_CUDA(pf::launch_emit(s, views[v], k0 + views[v].pair_off, v0 + views[v].pair_off,
+                                (uint64_t)v << (32 + tb), st));
+    }
     bool alt = false;
-    PF_CUDA(pf::radix_sort_pairs(s, k0, v0, k1, v1, P, 32 + tile_bits(T), &alt, st));
-    if (alt) PF_CUDA(cudaMemcpyAsync(v0, v1, 4 * p, cudaMemcpyDeviceToDevice, st));
+    if (Ptot > 0) {
+        PF_CUDA(pf::radix_sort_pairs(s, k0, v0, k1, v1, Ptot, 32 + tb + vb, &alt, st));
+        if (alt) PF_CUDA(cudaMemcpyAsync(v0, v1, 4 * (size_t)Ptot, cudaMemcpyDeviceToDevice, st));
+    }
     uint64_t *ks = alt ? k1 : k0;
-    PF_CUDA(pf::launch_ranges(s, v, ks, st));
+    uint2 *rall = s->ranges_all.as<uint2>();
+    PF_CUDA(pf::launch_ranges(s, ks, Ptot, T, tb, rall, V, st));
+    for (int v = 0; v < V; ++v) {
+        views[v].vals_p = v0;
+        views[v].ranges_p = rall + (size_t)v * T;
+        PF_CUDA(pf::launch_tile_order(s, views[v], st));
+    }
     *keys_out = ks;
     return PF_OK;
 }
@@ -334,8 +354,6 @@ int pf_destroy(pf_scene *s)
         v.count.release();
         v.keybits.release();
         v.offsets.release();
-        v.vals.release();
-        v.ranges.release();
         v.saved.release();
         v.order.release();
         v.chunk_off.release();
@@ -347,8 +365,8 @@ int pf_destroy(pf_scene *s)
     s->debug_view.count.release();
     s->debug_view.keybits.release();
     s->debug_view.offsets.release();
-    s->debug_view.vals.release();
-    s->debug_view.ranges.release();
+    s->vals_all.release();
+    s->ranges_all.release();
     s->debug_view.order.release();
     s->debug_view.chunk_off.release();
     s->rec_used.release();
@@ -401,11 +419,11 @@ int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
         PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * (size_t)V));
         PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * (size_t)V, st));
     }
+    uint64_t *ks_all = nullptr;
+    rc = emit_sort_ranges(s, s->views.data(), V, st, &ks_all);
+    if (rc) return rc;
     for (int v = 0; v < V; ++v) {
         pf::ViewState &vs = s->views[v];
-        uint64_t *ks = nullptr;
-        rc = emit_sort_ranges(s, vs, st, &ks);
-        if (rc) return rc;
         uint32_t *used = nullptr;
         if (record) {
             const int T = vs.cam.tiles_x * vs.cam.tiles_y;
@@ -473,8 +491,8 @@ int pf_debug_binning(pf_scene *s, const pf_camera *cam, int32_t *rect, int32_t *
     if (rc) return rc;
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)stream;
-    // use a dedicated view slot so the forward's saved state is untouched
     pf::ViewState &vs = s->debug_view;
+    s->fwd_views = 0;   // the debug pass reuses the call's sorted-pair arrays
     vs.cam = cam_params(*cam);
     int64_t *d_tot;
     PF_CUDA(s->scan_totals.reserve(sizeof(int64_t)));
@@ -494,14 +512,14 @@ int pf_debug_binning(pf_scene *s, const pf_camera *cam, int32_t *rect, int32_t *
     if (keybits) PF_CUDA(cudaMemcpyAsync(keybits, vs.keybits.ptr, 4 * N, cudaMemcpyDeviceToDevice, st));
     if (keys) {
         uint64_t *ks = nullptr;
-        rc = emit_sort_ranges(s, vs, st, &ks);
+        rc = emit_sort_ranges(s, &vs, 1, st, &ks);
         if (rc) return rc;
         if (P > 0) {
             PF_CUDA(cudaMemcpyAsync(keys, ks, 8 * (size_t)P, cudaMemcpyDeviceToDevice, st));
-            if (vals) PF_CUDA(cudaMemcpyAsync(vals, vs.vals.ptr, 4 * (size_t)P, cudaMemcpyDeviceToDevice, st));
+            if (vals) PF_CUDA(cudaMemcpyAsync(vals, vs.vals_p, 4 * (size_t)P, cudaMemcpyDeviceToDevice, st));
         }
         if (ranges)
-            PF_CUDA(cudaMemcpyAsync(ranges, vs.ranges.ptr,
+            PF_CUDA(cudaMemcpyAsync(ranges, vs.ranges_p,
                                     sizeof(uint2) * (size_t)vs.cam.tiles_x * vs.cam.tiles_y,
                                     cudaMemcpyDeviceToDevice, st));
     }
@@ -521,6 +539,7 @@ int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_s
         s->edges_built = true;
     }
     pf::ViewState &vs = s->debug_view;
+    s->fwd_views = 0;   // the debug pass reuses the call's sorted-pair arrays
     vs.cam = cam_params(*cam);
     PF_CUDA(s->scan_totals.reserve(sizeof(int64_t)));
     int64_t *d_tot = s->scan_totals.as<int64_t>();
@@ -533,7 +552,7 @@ int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_s
     PF_CUDA(cudaStreamSynchronize(st));
     vs.P = P;
     uint64_t *ks;
-    rc = emit_sort_ranges(s, vs, st, &ks);
+    rc = emit_sort_ranges(s, &vs, 1, st, &ks);
     if (rc) return rc;
     PF_CUDA(cudaMemsetAsync(counters, 0, 32 * (size_t)cam->width * cam->height, st));
     PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, nullptr, st));

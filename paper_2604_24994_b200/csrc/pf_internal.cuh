@@ -55,7 +55,9 @@ struct ViewState {
     CamParams cam{};
     int64_t P = 0;
     DevBuf rect, count, keybits, offsets;   // binning of this view (N-sized)
-    DevBuf vals, ranges;                     // sorted cell ids, per-tile [start,end)
+    uint32_t *vals_p = nullptr;              // sorted cell ids (the call's shared array)
+    uint2 *ranges_p = nullptr;               // this view's per-tile [start,end) into vals_p
+    int64_t pair_off = 0;                    // first pair of this view in the shared arrays
     DevBuf order;                            // tiles by decreasing list length (K6/K7 grid order)
     DevBuf chunk_off;                        // first 32-entry chunk of each tile
     // K6 -> K7 segment records (see pf_raster.cu): per (warp, chunk) descriptor
@@ -80,6 +82,7 @@ struct pf_scene {
     bool edges_built = false;
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
+    pf::DevBuf vals_all, ranges_all;   // sorted pairs of all views of the last call
     pf::DevBuf acc;                 // backward packed accumulators
     pf::DevBuf rec_used;            // u32[V] records used per view (K6 atomics)
     double rec_ratio = 3.0;         // arena capacity in records per (tile, cell) pair
@@ -106,11 +109,13 @@ cudaError_t launch_validate(pf_scene *s, int *d_flag, cudaStream_t st);
 cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st);
 cudaError_t launch_scan_counts(pf_scene *s, ViewState &v, int64_t *d_total, cudaStream_t st);
 cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
-                        cudaStream_t st);
+                        uint64_t view_key, cudaStream_t st);
 cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                              uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
                              cudaStream_t st);
-cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaStream_t st);
+cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, int tile_bits,
+                          uint2 *ranges_all, int V, cudaStream_t st);
+cudaError_t launch_tile_order(pf_scene *s, ViewState &v, cudaStream_t st);
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
                            uint32_t *rec_used, cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);

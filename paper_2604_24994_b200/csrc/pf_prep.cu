@@ -307,7 +307,8 @@ cudaError_t launch_scan_counts(pf_scene *s, ViewState &v, int64_t *d_total, cuda
 __global__ void __launch_bounds__(256)
 k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__restrict__ count,
         const uint32_t *__restrict__ keybits, const uint32_t *__restrict__ offs,
-        unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals)
+        unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+        unsigned long long view_key)
 {
     const int lane = threadIdx.x & 31;
     int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
@@ -337,20 +338,21 @@ k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__rest
         for (int q = lane; q < c; q += 32) {
             int dy = q / w, dx = q - dy * w;
             unsigned long long tile = (unsigned long long)((y0 + dy) * tiles_x + (x0 + dx));
-            keys[o + q] = (tile << 32) | k;
+            keys[o + q] = view_key | (tile << 32) | k;
             vals[o + q] = cell;
         }
     }
 }
 
 cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
-                        cudaStream_t st)
+                        uint64_t view_key, cudaStream_t st)
 {
     cudaEvent_t ev;
     stage_begin(s, 3, st, &ev);
     k3_emit<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
         s->ds.N, v.cam.tiles_x, v.rect.as<int4>(), v.count.as<int>(), v.keybits.as<uint32_t>(),
-        v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals);
+        v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals,
+        (unsigned long long)view_key);
     ++s->launches;
     stage_end(s, 3, st, ev);
     return cudaGetLastError();
@@ -359,14 +361,19 @@ cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *val
 // ------------------------------------------------------------------------
 // K5: per-tile ranges [start, end) of the sorted pairs ((0,0) for empty tiles)
 // ------------------------------------------------------------------------
+// keys of all views of a call: (view << (32 + tile_bits)) | (tile << 32) | keybits;
+// ranges[view * T + tile] = [start, end) in the call's sorted arrays.
 __global__ void __launch_bounds__(256) k5_ranges(const unsigned long long *__restrict__ keys,
-                                                 int64_t P, uint2 *__restrict__ ranges)
+                                                 int64_t P, int T, int tile_bits,
+                                                 uint2 *__restrict__ ranges)
 {
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= P) return;
-    uint32_t t = (uint32_t)(keys[q] >> 32);
-    if (q == 0 || (uint32_t)(keys[q - 1] >> 32) != t) ranges[t].x = (uint32_t)q;
-    if (q == P - 1 || (uint32_t)(keys[q + 1] >> 32) != t) ranges[t].y = (uint32_t)(q + 1);
+    const unsigned long long vt = keys[q] >> 32;   // (view << tile_bits) | tile
+    const uint32_t idx = (uint32_t)(vt >> tile_bits) * (uint32_t)T +
+                         (uint32_t)(vt & ((1ull << tile_bits) - 1ull));
+    if (q == 0 || (keys[q - 1] >> 32) != vt) ranges[idx].x = (uint32_t)q;
+    if (q == P - 1 || (keys[q + 1] >> 32) != vt) ranges[idx].y = (uint32_t)(q + 1);
 }
 
 // Grid order for K6/K7: tiles by decreasing list length (longest-processing-time
@@ -415,21 +422,30 @@ __global__ void __launch_bounds__(1024) k5_tile_order(const uint2 *__restrict__ 
     }
 }
 
-cudaError_t launch_ranges(pf_scene *s, ViewState &v, const uint64_t *keys, cudaStream_t st)
+cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, int tile_bits,
+                          uint2 *ranges_all, int V, cudaStream_t st)
 {
-    int T = v.cam.tiles_x * v.cam.tiles_y;
-    cudaError_t err = cudaMemsetAsync(v.ranges.ptr, 0, sizeof(uint2) * (size_t)T, st);
+    cudaError_t err = cudaMemsetAsync(ranges_all, 0, sizeof(uint2) * (size_t)T * V, st);
     if (err != cudaSuccess) return err;
-    if ((err = v.order.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
+    if (P == 0) return cudaSuccess;
     cudaEvent_t ev;
     stage_begin(s, 5, st, &ev);
-    if (v.P > 0) {
-        k5_ranges<<<ceil_div(v.P, 256), 256, 0, st>>>((const unsigned long long *)keys, v.P,
-                                                       v.ranges.as<uint2>());
-        ++s->launches;
-    }
+    k5_ranges<<<ceil_div(P, 256), 256, 0, st>>>((const unsigned long long *)keys, P, T, tile_bits,
+                                                 ranges_all);
+    ++s->launches;
+    stage_end(s, 5, st, ev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_order(pf_scene *s, ViewState &v, cudaStream_t st)
+{
+    const int T = v.cam.tiles_x * v.cam.tiles_y;
+    cudaError_t err;
+    if ((err = v.order.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
     if ((err = v.chunk_off.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
-    k5_tile_order<<<1, 1024, 0, st>>>(v.ranges.as<uint2>(), T, v.order.as<uint32_t>(),
+    cudaEvent_t ev;
+    stage_begin(s, 5, st, &ev);
+    k5_tile_order<<<1, 1024, 0, st>>>(v.ranges_p, T, v.order.as<uint32_t>(),
                                       v.chunk_off.as<uint32_t>());
     ++s->launches;
     stage_end(s, 5, st, ev);

@@ -482,18 +482,18 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
     stage_begin(s, 6, st, &ev);
     if (counters)
         k6_forward<true, false><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
+            s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(), v.vals_p,
             (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
             nullptr, 0u);
     else if (rec_used)
         k6_forward<false, true><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
+            s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(), v.vals_p,
             (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off.as<uint32_t>(),
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
             (uint32_t)v.rec_cap);
     else
         k6_forward<false, false><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(), v.vals.as<uint32_t>(),
+            s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(), v.vals_p,
             (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u);
     ++s->launches;
     stage_end(s, 6, st, ev);
@@ -710,8 +710,11 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
         // recorded entries only: stage them (lane k <-> record k)
         const uint32_t nrec = d.y;
         const uint32_t *R0 = rec + (size_t)d.x * kRecWords;
+        uint32_t my_mask = 0;
         if (lane < (int)nrec) {
-            const uint32_t pos = __ldg(R0 + (size_t)lane * kRecWords + 1);
+            const uint2 mp = __ldg(reinterpret_cast<const uint2 *>(R0 + (size_t)lane * kRecWords));
+            my_mask = mp.x;
+            const uint32_t pos = mp.y;
             const uint32_t cell = __ldg(vals + base + pos);
             const float4 A = __ldg(ds.cellA + cell);
             double x0, x1, x2;
@@ -720,9 +723,8 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
         }
         __syncwarp();
         for (uint32_t k = 0; k < nrec; ++k) {
-            const uint32_t *Rk = R0 + (size_t)k * kRecWords;
-            const uint32_t mask = __ldg(Rk);
-            const uint32_t code = __ldg(reinterpret_cast<const uint16_t *>(Rk + 2) + lane);
+            const uint32_t mask = __shfl_sync(0xffffffffu, my_mask, (int)k);
+            const uint32_t code = __ldg(reinterpret_cast<const uint16_t *>(R0 + (size_t)k * kRecWords + 2) + lane);
             const bool seg = (mask >> lane) & 1u;
             const int j = (int)k;
             Seg g;
@@ -756,8 +758,8 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
     int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges.as<uint2>(), v.order.as<uint32_t>(),
-                                   v.vals.as<uint32_t>(), v.saved.as<float4>(),
+    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(),
+                                   v.vals_p, v.saved.as<float4>(),
                                    (const float4 *)grad_out, s->acc.as<float>(),
                                    v.chunk_off.as<uint32_t>(), v.desc.as<uint2>(),
                                    v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
