@@ -137,11 +137,16 @@ int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
     uint64_t *ks = alt ? k1 : k0;
     uint2 *rall = s->ranges_all.as<uint2>();
     PF_CUDA(pf::launch_ranges(s, ks, Ptot, T, tb, rall, V, st));
+    PF_CUDA(s->order_all.reserve(sizeof(uint32_t) * (size_t)T * V));
+    PF_CUDA(s->chunk_off_all.reserve(sizeof(uint32_t) * (size_t)T * V));
     for (int v = 0; v < V; ++v) {
         views[v].vals_p = v0;
         views[v].ranges_p = rall + (size_t)v * T;
-        PF_CUDA(pf::launch_tile_order(s, views[v], st));
+        views[v].order = s->order_all.as<uint32_t>() + (size_t)v * T;
+        views[v].chunk_off = s->chunk_off_all.as<uint32_t>() + (size_t)v * T;
     }
+    PF_CUDA(pf::launch_tile_order(s, rall, T, V, s->order_all.as<uint32_t>(),
+                                  s->chunk_off_all.as<uint32_t>(), st));
     *keys_out = ks;
     return PF_OK;
 }
@@ -355,8 +360,6 @@ int pf_destroy(pf_scene *s)
         v.keybits.release();
         v.offsets.release();
         v.saved.release();
-        v.order.release();
-        v.chunk_off.release();
         v.desc.release();
         v.wdone.release();
         v.rec.release();
@@ -367,8 +370,8 @@ int pf_destroy(pf_scene *s)
     s->debug_view.offsets.release();
     s->vals_all.release();
     s->ranges_all.release();
-    s->debug_view.order.release();
-    s->debug_view.chunk_off.release();
+    s->order_all.release();
+    s->chunk_off_all.release();
     s->rec_used.release();
     if (s->pinned) cudaFreeHost(s->pinned);
     if (s->pinned_rec) cudaFreeHost(s->pinned_rec);

@@ -58,8 +58,8 @@ struct ViewState {
     uint32_t *vals_p = nullptr;              // sorted cell ids (the call's shared array)
     uint2 *ranges_p = nullptr;               // this view's per-tile [start,end) into vals_p
     int64_t pair_off = 0;                    // first pair of this view in the shared arrays
-    DevBuf order;                            // tiles by decreasing list length (K6/K7 grid order)
-    DevBuf chunk_off;                        // first 32-entry chunk of each tile
+    uint32_t *order = nullptr;               // tiles by decreasing list length (K6/K7 grid order)
+    uint32_t *chunk_off = nullptr;           // first 32-entry chunk of each tile
     // K6 -> K7 segment records (see pf_raster.cu): per (warp, chunk) descriptor
     // (first record, count | kOverflow), chunks walked per warp, the record arena
     DevBuf desc, wdone, rec;
@@ -83,6 +83,7 @@ struct pf_scene {
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
     pf::DevBuf vals_all, ranges_all;   // sorted pairs of all views of the last call
+    pf::DevBuf order_all, chunk_off_all;  // per-view tile orders / chunk offsets (V x T)
     pf::DevBuf acc;                 // backward packed accumulators
     pf::DevBuf rec_used;            // u32[V] records used per view (K6 atomics)
     double rec_ratio = 3.0;         // arena capacity in records per (tile, cell) pair
@@ -115,7 +116,8 @@ cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64
                              cudaStream_t st);
 cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, int tile_bits,
                           uint2 *ranges_all, int V, cudaStream_t st);
-cudaError_t launch_tile_order(pf_scene *s, ViewState &v, cudaStream_t st);
+cudaError_t launch_tile_order(pf_scene *s, const uint2 *ranges_all, int T, int V,
+                              uint32_t *order_all, uint32_t *chunk_off_all, cudaStream_t st);
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
                            uint32_t *rec_used, cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);

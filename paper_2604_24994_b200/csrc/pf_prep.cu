@@ -17,22 +17,53 @@ namespace pf {
 // ------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k0_edge_records(DeviceScene ds)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ds.N) return;
-    float px = ds.sites[3 * i], py = ds.sites[3 * i + 1], pz = ds.sites[3 * i + 2];
-    float wi = ds.weights[i];
-    int64_t b = ds.nbr_off[i], e = ds.nbr_off[i + 1];
-    ds.cellA[i] = make_float4(px, py, pz, ds.radii[i]);
-    ds.cellB[i] = make_float4(ds.density[i], ds.rgb[3 * i], ds.rgb[3 * i + 1], ds.rgb[3 * i + 2]);
-    ds.cellE[i] = make_uint2((uint32_t)b, (uint32_t)(e - b));
-    for (int64_t q = b; q < e; ++q) {
-        int j = ds.nbr_idx[q];
-        float nx = ds.sites[3 * j] - px, ny = ds.sites[3 * j + 1] - py,
-              nz = ds.sites[3 * j + 2] - pz;
-        float nn = nx * nx + ny * ny + nz * nz;
-        // pow(x,i) <= pow(x,j)  <=>  (x - p_i).n <= 0.5 (|n|^2 - (w_j - w_i))
-        float k = 0.5f * (nn - (ds.weights[j] - wi));
-        ds.edges[q] = make_float4(nx, ny, nz, k);
+    // cell records: one thread per cell.  Edge records: the warp's 32 cells own
+    // the contiguous CSR range [off[i0], off[i0+32]); the warp walks it 32 edges
+    // at a time (coalesced index reads and record writes), each lane finding its
+    // edge's source cell by a binary search over the lanes' offsets (shuffles).
+    const int lane = threadIdx.x & 31;
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
+    const int64_t i = i0 + lane;
+    if (i0 >= ds.N) return;
+    float px = 0.f, py = 0.f, pz = 0.f, wi = 0.f;
+    int64_t ob = 0, oe = 0;
+    if (i < ds.N) {
+        px = ds.sites[3 * i];
+        py = ds.sites[3 * i + 1];
+        pz = ds.sites[3 * i + 2];
+        wi = ds.weights[i];
+        ob = ds.nbr_off[i];
+        oe = ds.nbr_off[i + 1];
+        ds.cellA[i] = make_float4(px, py, pz, ds.radii[i]);
+        ds.cellB[i] = make_float4(ds.density[i], ds.rgb[3 * i], ds.rgb[3 * i + 1], ds.rgb[3 * i + 2]);
+        ds.cellE[i] = make_uint2((uint32_t)ob, (uint32_t)(oe - ob));
+    }
+    const int64_t base = __shfl_sync(0xffffffffu, ob, 0);
+    const int last = (int)min((int64_t)31, ds.N - 1 - i0);
+    const int64_t end = __shfl_sync(0xffffffffu, oe, last);
+    const uint32_t rel = (i < ds.N) ? (uint32_t)(ob - base) : 0xffffffffu;
+    const uint32_t total = (uint32_t)(end - base);
+    for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        int src = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int cand = src + step;
+            const uint32_t r = __shfl_sync(0xffffffffu, rel, cand & 31);
+            if (cand < 32 && r <= e) src = cand;
+        }
+        const float sx = __shfl_sync(0xffffffffu, px, src), sy = __shfl_sync(0xffffffffu, py, src),
+                    sz = __shfl_sync(0xffffffffu, pz, src), sw = __shfl_sync(0xffffffffu, wi, src);
+        if (e < total) {
+            const int64_t q = base + e;
+            const int j = ds.nbr_idx[q];
+            const float nx = ds.sites[3 * j] - sx, ny = ds.sites[3 * j + 1] - sy,
+                        nz = ds.sites[3 * j + 2] - sz;
+            const float nn = nx * nx + ny * ny + nz * nz;
+            // pow(x,i) <= pow(x,j)  <=>  (x - p_i).n <= 0.5 (|n|^2 - (w_j - w_i))
+            const float k = 0.5f * (nn - (ds.weights[j] - sw));
+            ds.edges[q] = make_float4(nx, ny, nz, k);
+        }
     }
 }
 
@@ -310,36 +341,55 @@ k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__rest
         unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
         unsigned long long view_key)
 {
+    // A warp owns 32 consecutive cells, whose pairs occupy one contiguous output
+    // range [off[i0], off[i0] + total).  It writes that range 32 positions at a
+    // time (coalesced); position p finds its source lane by a 5-step binary
+    // search over the lanes' offsets (shuffles), so big rectangles are balanced.
     const int lane = threadIdx.x & 31;
-    int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
-    int64_t i = i0 + lane;
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
+    const int64_t i = i0 + lane;
     int cnt = 0;
-    int4 rc = make_int4(0, 0, 0, 0);
+    int4 rc = make_int4(0, 0, 1, 0);
     uint32_t kb = 0, off = 0;
     if (i < N) {
         cnt = count[i];
+        off = offs[i];
         if (cnt) {
             rc = rect[i];
             kb = keybits[i];
-            off = offs[i];
         }
     }
-    unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);
-    while (todo) {
-        int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        int c = __shfl_sync(0xffffffffu, cnt, src);
-        int x0 = __shfl_sync(0xffffffffu, rc.x, src);
-        int y0 = __shfl_sync(0xffffffffu, rc.y, src);
-        int w = __shfl_sync(0xffffffffu, rc.z, src) - x0;
-        uint32_t k = __shfl_sync(0xffffffffu, kb, src);
-        uint32_t o = __shfl_sync(0xffffffffu, off, src);
-        uint32_t cell = (uint32_t)(i0 + src);
-        for (int q = lane; q < c; q += 32) {
-            int dy = q / w, dx = q - dy * w;
-            unsigned long long tile = (unsigned long long)((y0 + dy) * tiles_x + (x0 + dx));
-            keys[o + q] = view_key | (tile << 32) | k;
-            vals[o + q] = cell;
+    // exclusive prefix of the counts inside the warp (offs is the global one)
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t base = __shfl_sync(0xffffffffu, off, 0) ;
+    const int w = rc.z - rc.x;
+    for (int p0 = 0; p0 < total; p0 += 32) {
+        const int p = p0 + lane;
+        int src = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int cand = src + step;
+            const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+            if (cand < 32 && ex <= p) src = cand;
+        }
+        const int ex = __shfl_sync(0xffffffffu, excl, src);
+        const int x0 = __shfl_sync(0xffffffffu, rc.x, src);
+        const int y0 = __shfl_sync(0xffffffffu, rc.y, src);
+        const int ww = __shfl_sync(0xffffffffu, w, src);
+        const uint32_t k = __shfl_sync(0xffffffffu, kb, src);
+        if (p < total) {
+            const int q = p - ex;
+            const int dy = q / ww, dx = q - dy * ww;
+            const unsigned long long tile = (unsigned long long)((y0 + dy) * tiles_x + (x0 + dx));
+            keys[base + p] = view_key | (tile << 32) | k;
+            vals[base + p] = (uint32_t)(i0 + src);
         }
     }
 }
@@ -381,10 +431,14 @@ __global__ void __launch_bounds__(256) k5_ranges(const unsigned long long *__res
 // length bucket is arbitrary: tiles are independent, results do not depend on it.
 // Also writes chunk_off[t] = sum_{t' < t} ceil(len_t' / 32): the first 32-entry
 // chunk of tile t in the per-view chunk-descriptor table of the K6 -> K7 records.
-__global__ void __launch_bounds__(1024) k5_tile_order(const uint2 *__restrict__ ranges, int T,
-                                                      uint32_t *__restrict__ order,
-                                                      uint32_t *__restrict__ chunk_off)
+__global__ void __launch_bounds__(1024) k5_tile_order(const uint2 *__restrict__ ranges_all, int T,
+                                                      uint32_t *__restrict__ order_all,
+                                                      uint32_t *__restrict__ chunk_off_all)
 {
+    // one block per view
+    const uint2 *ranges = ranges_all + (size_t)blockIdx.x * T;
+    uint32_t *order = order_all + (size_t)blockIdx.x * T;
+    uint32_t *chunk_off = chunk_off_all + (size_t)blockIdx.x * T;
     __shared__ int hist[64], off[64];
     __shared__ long long sw[33];
     if (threadIdx.x < 64) hist[threadIdx.x] = 0;
@@ -437,16 +491,12 @@ cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_tile_order(pf_scene *s, ViewState &v, cudaStream_t st)
+cudaError_t launch_tile_order(pf_scene *s, const uint2 *ranges_all, int T, int V,
+                              uint32_t *order_all, uint32_t *chunk_off_all, cudaStream_t st)
 {
-    const int T = v.cam.tiles_x * v.cam.tiles_y;
-    cudaError_t err;
-    if ((err = v.order.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
-    if ((err = v.chunk_off.reserve(sizeof(uint32_t) * (size_t)T)) != cudaSuccess) return err;
     cudaEvent_t ev;
     stage_begin(s, 5, st, &ev);
-    k5_tile_order<<<1, 1024, 0, st>>>(v.ranges_p, T, v.order.as<uint32_t>(),
-                                      v.chunk_off.as<uint32_t>());
+    k5_tile_order<<<V, 1024, 0, st>>>(ranges_all, T, order_all, chunk_off_all);
     ++s->launches;
     stage_end(s, 5, st, ev);
     return cudaGetLastError();

@@ -482,18 +482,18 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
     stage_begin(s, 6, st, &ev);
     if (counters)
         k6_forward<true, false><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(), v.vals_p,
+            s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
             nullptr, 0u);
     else if (rec_used)
         k6_forward<false, true><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(), v.vals_p,
-            (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off.as<uint32_t>(),
+            s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
+            (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
             (uint32_t)v.rec_cap);
     else
         k6_forward<false, false><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(), v.vals_p,
+            s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u);
     ++s->launches;
     stage_end(s, 6, st, ev);
@@ -758,10 +758,10 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
     int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order.as<uint32_t>(),
+    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order,
                                    v.vals_p, v.saved.as<float4>(),
                                    (const float4 *)grad_out, s->acc.as<float>(),
-                                   v.chunk_off.as<uint32_t>(), v.desc.as<uint2>(),
+                                   v.chunk_off, v.desc.as<uint2>(),
                                    v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
     ++s->launches;
     stage_end(s, 7, st, ev);
