@@ -54,14 +54,14 @@ def lib():
         L.oracle_emit_sort.argtypes = [i64, P, P, P, C.c_int32, P, P]
         L.oracle_emit_sort.restype = i64
         L.oracle_tile_ranges.argtypes = [i64, P, C.c_int32, P]
-        L.oracle_render.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, i64, P, P, P, P,
-                                    P, P, C.c_int]
-        L.oracle_backward.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, i64, P, P,
-                                      P, P, P, P, P, C.c_int]
-        L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, i64, P, P,
+        L.oracle_render.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P, P,
+                                    P, P, P, C.c_int]
+        L.oracle_backward.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P,
+                                      P, P, P, P, P, P, C.c_int]
+        L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, P, i64, P, P,
                                            C.c_double, P, P]
-        L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, C.c_int32,
-                                             C.c_int32, P, i64]
+        L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P,
+                                             C.c_int32, C.c_int32, P, i64]
         L.oracle_pixel_segments.restype = i64
         L.oracle_pixel_ray.argtypes = [P, C.c_int32, C.c_int32, P, P, P]
         L.oracle_composite.argtypes = [i64, P, P, P, P, P]
@@ -102,10 +102,12 @@ class _SceneArrays:
         if self.idx.size == 0:
             self.idx = np.zeros(1, np.int32)
         self.bg = np.asarray(sc.background, np.float32)
+        nrm = getattr(sc, "normals", None)
+        self.normals = None if nrm is None else _c(nrm, np.float32)
 
     def args(self):
         return [self.N, _p(self.sites), _p(self.weights), _p(self.radii), _p(self.density),
-                _p(self.rgb), _p(self.off), _p(self.idx), _p(self.bg)]
+                _p(self.rgb), _p(self.off), _p(self.idx), _p(self.bg), _p(self.normals)]
 
 
 # ---------------------------------------------------------------------------
@@ -182,9 +184,13 @@ def backward(sc, cam, grad_out, mode=O3, pixels=None, nthreads=0):
     N = A.N
     gs = np.zeros((N, 3)); gw = np.zeros(N); gr = np.zeros(N); gsig = np.zeros(N)
     grgb = np.zeros((N, 3))
+    gn = np.zeros((N, 3)) if A.normals is not None else None
     lib().oracle_backward(mode, *A.args(), C.byref(oc), n, _p(pix), _p(g), _p(gs), _p(gw),
-                          _p(gr), _p(gsig), _p(grgb), nthreads)
-    return dict(sites=gs, weights=gw, radii=gr, density=gsig, rgb=grgb)
+                          _p(gr), _p(gsig), _p(grgb), _p(gn), nthreads)
+    out = dict(sites=gs, weights=gw, radii=gr, density=gsig, rgb=grgb)
+    if gn is not None:
+        out["normals"] = gn
+    return out
 
 
 def cell_interval(sc, i, Q, d, t_near=0.0, mode=O2):
@@ -195,14 +201,14 @@ def cell_interval(sc, i, Q, d, t_near=0.0, mode=O2):
     res = np.zeros(2)
     kinds = np.zeros(4, np.int32)
     hit = lib().oracle_cell_interval(mode, A.N, _p(A.sites), _p(A.weights), _p(A.radii),
-                                     _p(A.off), _p(A.idx), int(i), _p(Qa), _p(da),
+                                     _p(A.off), _p(A.idx), _p(A.normals), int(i), _p(Qa), _p(da),
                                      float(t_near), _p(res), _p(kinds))
     return bool(hit), float(res[0]), float(res[1]), kinds
 
 
 def pixel_segments(sc, cam, x, y, mode=O3, cap=4096):
     """Composited segments of pixel (x,y): list of dicts (cell, t_in, t_out, kin, kout,
-    jin, jout, list_pos); kinds 0 sphere, 1 near, 2 plane."""
+    jin, jout, list_pos); kinds 0 sphere, 1 near, 2 plane, 3 dipole."""
     A = _SceneArrays(sc)
     oc = make_camera(cam)
     buf = np.zeros((cap, 8))

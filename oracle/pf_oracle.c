@@ -40,6 +40,11 @@
  *            "global sort by depths ... similar to 3DGS"); planes from lists.
  *      O1 == O2 == O3 on shared pixels is itself a test.
  *
+ *      Dipoles (NEXT-1): with per-cell normals n_i the cell is an
+ *      oriented point whose occupied half is (x - p_i).n_i <= 0 (SPEC S:242:
+ *      the side the normal points away from); the other half has zero density,
+ *      so I_i is further intersected with that half-space.
+ *
  *  (2) The backward pass: the exact derivative of (1) for a fixed active set
  *      and termination index, L = sum_pixels <grad_out, out> (
  *      endpoint derivatives of the sphere and the radical plane).
@@ -82,6 +87,7 @@ typedef struct {
     const int64_t *nbr_off;
     const int32_t *nbr_idx;
     double bg[3];
+    const float *normals; /* dipole normals n_i [N,3] or NULL (NEXT-1) */
 } oc_scene;
 
 #define O1_ALL_PAIRS 1
@@ -258,6 +264,7 @@ static void pixel_ray(const oc_camera *cam, double px, double py, double Q[3], d
 #define END_SPHERE 0
 #define END_NEAR 1
 #define END_PLANE 2
+#define END_DIPOLE 3 /* the cell's internal oriented face (NEXT-1) */
 
 typedef struct {
     double t_in, t_out;
@@ -338,6 +345,32 @@ static int cell_interval(const oc_scene *S, int mode, int64_t i, const double Q[
             }
         } else if (B < 0.0) {
             empty = 1; /* ray parallel to the plane, on j's side (C14) */
+        }
+    }
+    if (S->normals) {
+        /* oriented-point dipole: only the half-space the normal points
+         * away from is occupied, (x - p_i).n_i <= 0 (SPEC S:242 convention);
+         * (x(t) - p_i).n_i = (Q - p_i).n_i + t d.n_i  ->  A t <= B */
+        const float *n = S->normals + 3 * i;
+        double A = d[0] * n[0] + d[1] * n[1] + d[2] * n[2];
+        double B = ((double)p[0] - Q[0]) * n[0] + ((double)p[1] - Q[1]) * n[1] +
+                   ((double)p[2] - Q[2]) * n[2];
+        if (A > 0.0) {
+            double t = B / A;
+            if (t < s->t_out) {
+                s->t_out = t;
+                s->kout = END_DIPOLE;
+                s->jout = -1;
+            }
+        } else if (A < 0.0) {
+            double t = B / A;
+            if (t > s->t_in) {
+                s->t_in = t;
+                s->kin = END_DIPOLE;
+                s->jin = -1;
+            }
+        } else if (B < 0.0) {
+            empty = 1;
         }
     }
     if (empty) s->t_out = s->t_in;
@@ -500,8 +533,10 @@ static void pixel_counters(const oc_scene *S, const oc_bins *B, int x, int y, co
 
 static void make_scene(oc_scene *S, int64_t N, const float *sites, const float *weights,
                        const float *radii, const float *density, const float *rgb,
-                       const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg)
+                       const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
+                       const float *normals)
 {
+    S->normals = normals;
     S->N = N;
     S->sites = sites;
     S->weights = weights;
@@ -523,12 +558,12 @@ static void make_scene(oc_scene *S, int64_t N, const float *sites, const float *
 int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
                   const float *radii, const float *density, const float *rgb,
                   const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                  const oc_camera *cam, int64_t npix, const int32_t *pix_xy, double *out,
+                  const float *normals, const oc_camera *cam, int64_t npix, const int32_t *pix_xy, double *out,
                   int64_t *counters, uint64_t *sig, int64_t *nseg_out, int64_t *viol,
                   int nthreads)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS || counters) build_bins(&S, cam, &B);
@@ -586,12 +621,26 @@ int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
  * Adds sgn * gdt * (those) into the gradient arrays. */
 static void end_grad(const oc_scene *S, int kind, int64_t i, int64_t j, double t,
                      const double Q[3], const double d[3], double sgn_gdt, double *g_sites,
-                     double *g_w, double *g_r)
+                     double *g_w, double *g_r, double *g_normals)
 {
     if (kind == END_NEAR) return;
     const float *p = S->sites + 3 * i;
     double x[3] = {Q[0] + t * d[0], Q[1] + t * d[1], Q[2] + t * d[2]};
     double xp[3] = {x[0] - p[0], x[1] - p[1], x[2] - p[2]};
+    if (kind == END_DIPOLE) {
+        /* t* = (p - Q).n / (d.n):  dt/dp_i = n/a,  dt/dn_i = (p_i - x*)/a,  a = d.n */
+        const float *n = S->normals + 3 * i;
+        double a = d[0] * n[0] + d[1] * n[1] + d[2] * n[2];
+        for (int m = 0; m < 3; ++m) {
+#pragma omp atomic
+            g_sites[3 * i + m] += sgn_gdt * (double)n[m] / a;
+            if (g_normals) {
+#pragma omp atomic
+                g_normals[3 * i + m] -= sgn_gdt * xp[m] / a;
+            }
+        }
+        return;
+    }
     if (kind == END_SPHERE) {
         double den = d[0] * xp[0] + d[1] * xp[1] + d[2] * xp[2];
         for (int m = 0; m < 3; ++m) {
@@ -629,12 +678,12 @@ static void end_grad(const oc_scene *S, int kind, int64_t i, int64_t j, double t
 int oracle_backward(int mode, int64_t N, const float *sites, const float *weights,
                     const float *radii, const float *density, const float *rgb,
                     const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                    const oc_camera *cam, int64_t npix, const int32_t *pix_xy,
-                    const float *grad_out, double *g_sites, double *g_w, double *g_r,
-                    double *g_sigma, double *g_rgb, int nthreads)
+                    const float *normals, const oc_camera *cam, int64_t npix,
+                    const int32_t *pix_xy, const float *grad_out, double *g_sites, double *g_w,
+                    double *g_r, double *g_sigma, double *g_rgb, double *g_normals, int nthreads)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
@@ -697,8 +746,10 @@ int oracle_backward(int mode, int64_t N, const float *sites, const float *weight
                 g_sigma[i] += dtau * dt;
                 double gdt = dtau * sig;
                 if (gdt != 0.0) {
-                    end_grad(&S, s->kout, i, s->jout, s->t_out, Q, d, gdt, g_sites, g_w, g_r);
-                    end_grad(&S, s->kin, i, s->jin, s->t_in, Q, d, -gdt, g_sites, g_w, g_r);
+                    end_grad(&S, s->kout, i, s->jout, s->t_out, Q, d, gdt, g_sites, g_w, g_r,
+                             g_normals);
+                    end_grad(&S, s->kin, i, s->jin, s->t_in, Q, d, -gdt, g_sites, g_w, g_r,
+                             g_normals);
                 }
             }
         }
@@ -719,11 +770,11 @@ int oracle_backward(int mode, int64_t N, const float *sites, const float *weight
  * Returns 1 on a sphere hit, 0 otherwise. */
 int oracle_cell_interval(int mode, int64_t N, const float *sites, const float *weights,
                          const float *radii, const int64_t *nbr_off, const int32_t *nbr_idx,
-                         int64_t i, const double *Q, const double *d, double t_near,
-                         double *res, int32_t *kinds)
+                         const float *normals, int64_t i, const double *Q, const double *d,
+                         double t_near, double *res, int32_t *kinds)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, NULL, NULL, nbr_off, nbr_idx, NULL);
+    make_scene(&S, N, sites, weights, radii, NULL, NULL, nbr_off, nbr_idx, NULL, normals);
     oc_seg s;
     int64_t np = 0;
     int hit = cell_interval(&S, mode, i, Q, d, t_near, &s, &np);
@@ -743,11 +794,11 @@ int oracle_cell_interval(int mode, int64_t N, const float *sites, const float *w
 int64_t oracle_pixel_segments(int mode, int64_t N, const float *sites, const float *weights,
                               const float *radii, const float *density, const float *rgb,
                               const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                              const oc_camera *cam, int32_t x, int32_t y, double *seg,
-                              int64_t cap)
+                              const float *normals, const oc_camera *cam, int32_t x, int32_t y,
+                              double *seg, int64_t cap)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);

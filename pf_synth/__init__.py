@@ -61,6 +61,7 @@ class Scene:
     background: tuple = (0.0, 0.0, 0.0)
     name: str = ""
     meta: dict = field(default_factory=dict)
+    normals: np.ndarray | None = None   # f32[N,3] dipole normals (NEXT-1), or None
 
     @property
     def num_cells(self) -> int:
@@ -74,7 +75,8 @@ class Scene:
         return Scene(self.sites.copy(), self.weights.copy(), self.radii.copy(),
                      self.density.copy(), self.rgb.copy(),
                      self.nbr_offsets.copy(), self.nbr_indices.copy(),
-                     tuple(self.background), self.name, dict(self.meta))
+                     tuple(self.background), self.name, dict(self.meta),
+                     None if self.normals is None else self.normals.copy())
 
 
 # --------------------------------------------------------------------------
@@ -321,9 +323,30 @@ PRESETS = {
 }
 
 
+def add_dipoles(sc: Scene, seed: int = 77, toward=(0.0, 0.0, 0.0)) -> Scene:
+    """Oriented-point dipoles (NEXT-1): a unit normal per cell.
+    Normals are random unit vectors biased away from `toward` (so most occupied
+    halves face inward, as a trained surface would), seeded."""
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=(sc.num_cells, 3))
+    out = sc.sites.astype(np.float64) - np.asarray(toward, np.float64)[None, :]
+    out /= np.maximum(np.linalg.norm(out, axis=1, keepdims=True), 1e-9)
+    n = v / np.linalg.norm(v, axis=1, keepdims=True) + 1.5 * out
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    sc.normals = n.astype(np.float32)
+    sc.meta["dipoles"] = seed
+    return sc
+
+
 def make_scene(preset: str, seed: int | None = None, variant: str | None = None,
-               num_cells: int | None = None) -> Scene:
-    """Deterministic scene for a preset."""
+               num_cells: int | None = None, dipoles: bool = False) -> Scene:
+    """Deterministic scene for a preset; dipoles=True adds
+    seeded dipole normals (NEXT-1)."""
+    sc = _make_scene(preset, seed, variant, num_cells)
+    return add_dipoles(sc) if dipoles else sc
+
+
+def _make_scene(preset, seed, variant, num_cells):
     if preset == "tiny":
         return _scene_tiny(0 if seed is None else seed, variant or "sym8")
     if preset == "small":   # test-size nerfsynth-shaped foam
