@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--workload", default="train8_1m",
                     choices=["train8_1m", "mip360_1m", "nerfsynth200k", "sweep64_3m", "small360"])
     ap.add_argument("--views", type=int, default=None, help="views per GPU (default: preset)")
+    ap.add_argument("--dipoles", action="store_true",
+                    help="oriented-point dipole cells (NEXT-1) on the workload's foam")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -255,17 +257,17 @@ def main():
     wl = args.workload
     nv = args.views or default_views(wl)
     t_gen = time.perf_counter()
-    sc = pf_synth.make_scene(wl)
+    sc = pf_synth.make_scene(wl, dipoles=args.dipoles)
     cams = workload_cameras(wl, nv, ws, rank)
     t_gen = time.perf_counter() - t_gen
     H, W = cams[0].height, cams[0].width
     train = wl != "mip360_1m"
     r = pf.Renderer.from_scene(sc, dev, flags=0 if train else pf.PF_INFERENCE)
     # render-only handle on the same tensors (no backward state saved)
-    r_inf = pf.Renderer(*r._tensors, background=sc.background, flags=pf.PF_INFERENCE)
+    r_inf = r.sibling(pf.PF_INFERENCE)
     N = sc.num_cells
     grad_out = torch.from_numpy(pf_synth.make_grad_out(nv, H, W, seed=12 + rank)).to(dev)
-    flat = torch.zeros(9 * N, device=dev, dtype=torch.float32)
+    flat = torch.zeros(r.grad_size, device=dev, dtype=torch.float32)
     out = torch.empty((nv, H, W, 4), device=dev, dtype=torch.float32)
     stream = torch.cuda.current_stream()
 
@@ -331,7 +333,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         g_host = grad_out.cpu().pin_memory() if train else None
-        res_host = (torch.empty(9 * N, dtype=torch.float32) if train
+        res_host = (torch.empty(r.grad_size, dtype=torch.float32) if train
                     else torch.empty(out.shape, dtype=torch.float32)).pin_memory()
         g_dev = torch.empty_like(grad_out)
 
@@ -391,8 +393,11 @@ def main():
     sort_ms, sort_n = stages["K4_sort"]
     pairs = r.pair_counts(nv)
     P = float(np.mean(pairs))
-    passes = math.ceil((32 + math.ceil(math.log2((W + 15) // 16 * ((H + 15) // 16)))) / 8)
-    sort_bytes = 32.0 * P * passes
+    # one radix sort per call over all views' pairs: key bits = 32 + tile + view bits;
+    # algorithmic bytes per pass = 8 (histogram key read) + 12 read + 12 write per pair
+    vbits = math.ceil(math.log2(nv)) if nv > 1 else 0
+    passes = math.ceil((32 + math.ceil(math.log2((W + 15) // 16 * ((H + 15) // 16))) + vbits) / 8)
+    sort_bytes = 32.0 * P * nv * passes
     sort_gbs = sort_bytes / (sort_ms / max(sort_n, 1) / 1e3) / 1e9 if sort_ms > 0 else None
     hbm = float(peaks.get("hbm_gbs", 6650.0))
 
@@ -412,7 +417,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (pf_synth seeded generator, random-init foam)",
-            "config": {"workload": wl, "cells": N, "edges": sc.num_edges, "views_per_gpu": nv,
+            "config": {"workload": wl + ("+dipoles" if args.dipoles else ""), "cells": N,
+                       "edges": sc.num_edges, "views_per_gpu": nv,
                        "global_batch_views": nv * ws, "width": W, "height": H,
                        "pass": "fwd+bwd" if train else "fwd",
                        "parallelism": f"dp{ws} (views sharded, per-cell grad all-reduce)",
@@ -425,8 +431,8 @@ def main():
             "stage_launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
             "pairs_per_view": P, "counters_per_view": {"X_s": cnt[0], "X_h": cnt[1],
                                                        "X_p": cnt[2], "X_c": cnt[3]},
-            "sort": {"ms_per_view": sort_ms / max(sort_n, 1), "passes": passes,
-                     "bytes_per_view": sort_bytes, "achieved_gbs": sort_gbs,
+            "sort": {"ms_per_launch": sort_ms / max(sort_n, 1), "pairs_per_launch": P * nv,
+                     "passes": passes, "bytes_per_launch": sort_bytes, "achieved_gbs": sort_gbs,
                      "hbm_frac": (sort_gbs / hbm) if sort_gbs else None},
             "peaks_source": peaks_kind, "scene_gen_s": t_gen,
         }

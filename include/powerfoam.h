@@ -87,7 +87,11 @@ typedef struct {
     const int64_t *nbr_offsets; /* device i64[N+1] CSR offsets, nbr_offsets[0] = 0 */
     const int32_t *nbr_indices; /* device i32[E]   neighbour ids */
     float background[3];        /* constant background radiance */
-    uint32_t flags;             /* PF_VALIDATE | PF_STATIC_SCENE */
+    uint32_t flags;             /* PF_VALIDATE | PF_STATIC_SCENE | PF_INFERENCE */
+    const float *normals;       /* device f32[N,3] or NULL.  Oriented-point dipoles (P:238-249,
+                                   NEXT-1): cell i is occupied only on the side its normal points
+                                   away from, (x - p_i).n_i <= 0; the other half has
+                                   zero density.  Non-zero, finite (not required to be unit). */
 } pf_scene_desc;
 
 /* Pinhole camera, OpenCV axes (x right, y down, z forward).
@@ -133,6 +137,20 @@ PF_API int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t num_vi
                        const float *grad_out, float *grad_sites, float *grad_weights,
                        float *grad_radii, float *grad_density, float *grad_rgb,
                        pf_stream_t stream);
+
+/* Gradient outputs of pf_render_backward_ex (device arrays, accumulated +=). */
+typedef struct {
+    float *sites;    /* [N,3] */
+    float *weights;  /* [N]   */
+    float *radii;    /* [N]   */
+    float *density;  /* [N]   */
+    float *rgb;      /* [N,3] */
+    float *normals;  /* [N,3] dL/dn_i of the dipole normals, or NULL (ignored without dipoles) */
+} pf_grads;
+
+/* pf_render_backward with the gradient arrays in a struct (adds dL/d normals). */
+PF_API int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t num_views,
+                                 const float *grad_out, const pf_grads *grads, pf_stream_t stream);
 
 /* Frees everything the handle owns (not the caller's arrays).  NULL is a no-op. */
 PF_API int pf_destroy(pf_scene *s);

@@ -26,7 +26,8 @@ STAGES = ["K0_edge_records", "K1_preprocess", "K2_scan", "K3_emit", "K4_sort", "
 _STATUS = {0: "PF_OK", 1: "PF_ERR_INVALID_ARGUMENT", 2: "PF_ERR_CUDA",
            3: "PF_ERR_OUT_OF_MEMORY", 4: "PF_ERR_STATE"}
 
-EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_backward", "pf_destroy",
+EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_backward",
+           "pf_render_backward_ex", "pf_destroy",
            "pf_last_error", "pf_debug_binning", "pf_debug_counters", "pf_launch_count",
            "pf_set_profiling", "pf_stage_times", "pf_last_pair_counts"]
 
@@ -48,7 +49,12 @@ class _SceneDesc(C.Structure):
                 ("sites", C.c_void_p), ("weights", C.c_void_p), ("radii", C.c_void_p),
                 ("density", C.c_void_p), ("rgb", C.c_void_p), ("nbr_offsets", C.c_void_p),
                 ("nbr_indices", C.c_void_p), ("background", C.c_float * 3),
-                ("flags", C.c_uint32)]
+                ("flags", C.c_uint32), ("normals", C.c_void_p)]
+
+
+class _Grads(C.Structure):
+    _fields_ = [("sites", C.c_void_p), ("weights", C.c_void_p), ("radii", C.c_void_p),
+                ("density", C.c_void_p), ("rgb", C.c_void_p), ("normals", C.c_void_p)]
 
 
 _lib = None
@@ -76,6 +82,7 @@ def load_library(build_if_missing: bool = True):
     L.pf_create_scene.argtypes = [C.POINTER(_SceneDesc), C.POINTER(C.c_void_p), P]
     L.pf_render_forward.argtypes = [P, C.POINTER(_Camera), i32, P, P]
     L.pf_render_backward.argtypes = [P, C.POINTER(_Camera), i32, P, P, P, P, P, P, P]
+    L.pf_render_backward_ex.argtypes = [P, C.POINTER(_Camera), i32, P, C.POINTER(_Grads), P]
     L.pf_destroy.argtypes = [P]
     L.pf_last_error.restype = C.c_char_p
     L.pf_debug_binning.argtypes = [P, C.POINTER(_Camera), P, P, P, P, P, P, C.POINTER(i64), P]
@@ -136,12 +143,13 @@ class Renderer:
 
     def __init__(self, sites, weights, radii, density, rgb, nbr_offsets, nbr_indices,
                  background=(0.0, 0.0, 0.0), flags: int = 0, num_edges: int | None = None,
-                 stream=None):
+                 stream=None, normals=None):
         L = load_library()
         self.N = int(sites.shape[0])
         self.device = sites.device
-        self._tensors = (sites, weights, radii, density, rgb, nbr_offsets, nbr_indices)
-        for t in (sites, weights, radii, density, rgb):
+        self.has_normals = normals is not None
+        self._tensors = (sites, weights, radii, density, rgb, nbr_offsets, nbr_indices, normals)
+        for t in (sites, weights, radii, density, rgb) + ((normals,) if self.has_normals else ()):
             _dev_f32(t)
         if nbr_offsets.dtype != torch.int64 or nbr_indices.dtype != torch.int32:
             raise TypeError("nbr_offsets must be int64 and nbr_indices int32")
@@ -158,6 +166,9 @@ class Renderer:
         for c in range(3):
             d.background[c] = float(background[c])
         d.flags = int(flags)
+        d.normals = normals.data_ptr() if self.has_normals else None
+        self.background = tuple(float(b) for b in background)
+        self.flags = int(flags)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _check(L.pf_create_scene(C.byref(d), C.byref(h), _stream(stream)))
@@ -169,10 +180,22 @@ class Renderer:
         """Uploads a pf_synth.Scene-like object (numpy arrays) and wraps it."""
         dev = torch.device(device)
         t = lambda a, dt: torch.as_tensor(a).to(device=dev, dtype=dt).contiguous()
+        nrm = getattr(sc, "normals", None)
         return cls(t(sc.sites, torch.float32), t(sc.weights, torch.float32),
                    t(sc.radii, torch.float32), t(sc.density, torch.float32),
                    t(sc.rgb, torch.float32), t(sc.nbr_offsets, torch.int64),
-                   t(sc.nbr_indices, torch.int32), background=sc.background, flags=flags)
+                   t(sc.nbr_indices, torch.int32), background=sc.background, flags=flags,
+                   normals=None if nrm is None else t(nrm, torch.float32))
+
+    def sibling(self, flags: int):
+        """Another handle on the same tensors (e.g. a PF_INFERENCE renderer)."""
+        s, w, r, d, c, o, i, n = self._tensors
+        return Renderer(s, w, r, d, c, o, i, background=self.background, flags=flags, normals=n)
+
+    @property
+    def grad_size(self) -> int:
+        """Length of the flat gradient buffer: 9N, or 12N with dipole normals."""
+        return (12 if self.has_normals else 9) * self.N
 
     # -------------------------------------------------------------- hot path
     def forward(self, cams, out=None, stream=None):
@@ -186,24 +209,31 @@ class Renderer:
         return out
 
     def backward(self, cams, grad_out, grads=None, stream=None):
-        """Accumulates dL/dparams into `grads` (dict or flat f32[9N] tensor; zeros if None)."""
+        """Accumulates dL/dparams into `grads` (dict or flat f32[grad_size] tensor;
+        zeros if None)."""
         arr, V = _cams(cams)
         H, W = arr[0].height, arr[0].width
         _dev_f32(grad_out, (V, H, W, 4))
         if grads is None:
-            grads = torch.zeros(9 * self.N, device=self.device, dtype=torch.float32)
+            grads = torch.zeros(self.grad_size, device=self.device, dtype=torch.float32)
         views = self.grad_views(grads) if isinstance(grads, torch.Tensor) else grads
-        ptrs = [_dev_f32(views[k]) for k in ("sites", "weights", "radii", "density", "rgb")]
-        _check(self._L.pf_render_backward(self._h, arr, V, C.c_void_p(grad_out.data_ptr()),
-                                          *ptrs, _stream(stream)))
+        g = _Grads()
+        for k in ("sites", "weights", "radii", "density", "rgb"):
+            setattr(g, k, _dev_f32(views[k]).value)
+        g.normals = _dev_f32(views["normals"]).value if "normals" in views else None
+        _check(self._L.pf_render_backward_ex(self._h, arr, V, C.c_void_p(grad_out.data_ptr()),
+                                             C.byref(g), _stream(stream)))
         return views
 
     def grad_views(self, flat):
-        """Views of a flat f32[9N] gradient buffer as the five arrays (one NCCL buffer)."""
+        """Views of a flat gradient buffer as the parameter arrays (one NCCL buffer)."""
         N = self.N
-        return {"sites": flat[0:3 * N].view(N, 3), "weights": flat[3 * N:4 * N],
-                "radii": flat[4 * N:5 * N], "density": flat[5 * N:6 * N],
-                "rgb": flat[6 * N:9 * N].view(N, 3)}
+        out = {"sites": flat[0:3 * N].view(N, 3), "weights": flat[3 * N:4 * N],
+               "radii": flat[4 * N:5 * N], "density": flat[5 * N:6 * N],
+               "rgb": flat[6 * N:9 * N].view(N, 3)}
+        if self.has_normals and flat.numel() >= 12 * N:
+            out["normals"] = flat[9 * N:12 * N].view(N, 3)
+        return out
 
     # ----------------------------------------------------------- debug / stats
     def debug_binning(self, cam, stream=None):
@@ -269,19 +299,20 @@ class _RenderFn(torch.autograd.Function):
     neighbour lists and cameras are non-differentiable context."""
 
     @staticmethod
-    def forward(ctx, renderer, cams, sites, weights, radii, density, rgb):
+    def forward(ctx, renderer, cams, sites, weights, radii, density, rgb, normals):
         ctx.renderer, ctx.cams = renderer, cams
         return renderer.forward(cams)
 
     @staticmethod
     def backward(ctx, grad_out):
         r = ctx.renderer
-        g = torch.zeros(9 * r.N, device=r.device, dtype=torch.float32)
+        g = torch.zeros(r.grad_size, device=r.device, dtype=torch.float32)
         v = r.backward(ctx.cams, grad_out.contiguous(), g)
-        return None, None, v["sites"], v["weights"], v["radii"], v["density"], v["rgb"]
+        return (None, None, v["sites"], v["weights"], v["radii"], v["density"], v["rgb"],
+                v.get("normals"))
 
 
 def render(renderer: Renderer, cams):
     """Autograd-aware forward over the renderer's parameter tensors."""
-    s, w, r, d, c = renderer._tensors[:5]
-    return _RenderFn.apply(renderer, cams, s, w, r, d, c)
+    s, w, r, d, c, _, _, n = renderer._tensors
+    return _RenderFn.apply(renderer, cams, s, w, r, d, c, n)

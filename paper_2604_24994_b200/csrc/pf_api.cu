@@ -289,6 +289,7 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
     ds.rgb = d->rgb;
     ds.nbr_off = d->nbr_offsets;
     ds.nbr_idx = d->nbr_indices;
+    ds.normals = d->normals;
     for (int c = 0; c < 3; ++c) ds.bg[c] = d->background[c];
     int rc = PF_OK;
     do {
@@ -298,6 +299,10 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
         if ((e = s->cellB.reserve(16 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellB"); break; }
         if ((e = s->cellE.reserve(8 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellE"); break; }
         if ((e = s->edges.reserve(16 * E)) != cudaSuccess) { rc = cuda_fail(e, "alloc edges"); break; }
+        if (ds.normals) {
+            if ((e = s->cellN.reserve(16 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellN"); break; }
+            ds.cellN = s->cellN.as<float4>();
+        }
         ds.cellA = s->cellA.as<float4>();
         ds.cellB = s->cellB.as<float4>();
         ds.cellE = s->cellE.as<uint2>();
@@ -321,6 +326,7 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
                 if (host & 16) why += " density not finite/non-negative;";
                 if (host & 32) why += " bad neighbour offsets;";
                 if (host & 64) why += " neighbour index out of range or self loop;";
+                if (host & 128) why += " dipole normal zero or non-finite;";
                 rc = fail(PF_ERR_INVALID_ARGUMENT, why);
                 break;
             }
@@ -347,6 +353,7 @@ int pf_destroy(pf_scene *s)
     s->cellB.release();
     s->cellE.release();
     s->edges.release();
+    s->cellN.release();
     s->keys0.release();
     s->keys1.release();
     s->vals1.release();
@@ -462,15 +469,22 @@ int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t V, const floa
                        float *grad_sites, float *grad_weights, float *grad_radii,
                        float *grad_density, float *grad_rgb, pf_stream_t stream)
 {
+    pf_grads g = {grad_sites, grad_weights, grad_radii, grad_density, grad_rgb, nullptr};
+    return pf_render_backward_ex(s, cams, V, grad_out, &g, stream);
+}
+
+int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const float *grad_out,
+                          const pf_grads *g, pf_stream_t stream)
+{
     if (!s) return fail(PF_ERR_INVALID_ARGUMENT, "scene handle is NULL");
-    if (!cams || V < 1 || !grad_out)
-        return fail(PF_ERR_INVALID_ARGUMENT, "need cameras and grad_out");
-    if (!grad_sites || !grad_weights || !grad_radii || !grad_density || !grad_rgb)
+    if (!cams || V < 1 || !grad_out || !g)
+        return fail(PF_ERR_INVALID_ARGUMENT, "need cameras, grad_out and gradient arrays");
+    if (!g->sites || !g->weights || !g->radii || !g->density || !g->rgb)
         return fail(PF_ERR_INVALID_ARGUMENT, "a gradient array pointer is NULL");
     if (V != s->fwd_views || (int)s->fwd_cams.size() < V ||
         memcmp(cams, s->fwd_cams.data(), sizeof(pf_camera) * (size_t)V) != 0)
         return fail(PF_ERR_STATE, "backward needs the immediately preceding forward with the same cameras");
-    DeviceGuard g(s->device);
+    DeviceGuard dg(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)s->ds.N;
     PF_CUDA(s->acc.reserve(N * 48));   // 12 floats per cell (pf_raster.cu)
@@ -481,7 +495,8 @@ int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t V, const floa
         if (vs.P == 0) continue;
         PF_CUDA(pf::launch_backward(s, vs, grad_out + 4 * npix * (size_t)v, st));
     }
-    PF_CUDA(pf::launch_unpack(s, grad_sites, grad_weights, grad_radii, grad_density, grad_rgb, st));
+    PF_CUDA(pf::launch_unpack(s, g->sites, g->weights, g->radii, g->density, g->rgb,
+                              s->ds.cellN ? g->normals : nullptr, st));
     return PF_OK;
 }
 

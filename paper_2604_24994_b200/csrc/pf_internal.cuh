@@ -40,6 +40,8 @@ struct DeviceScene {
     float bg[3] = {0, 0, 0};
     float4 *cellA = nullptr, *cellB = nullptr, *edges = nullptr;
     uint2 *cellE = nullptr;
+    const float *normals = nullptr;   // caller's dipole normals [N,3] or null
+    float4 *cellN = nullptr;          // (n_i, 0) when dipoles are present
 };
 
 // grow-only device buffer
@@ -78,7 +80,7 @@ struct pf_scene {
     int device = 0;
     uint32_t flags = 0;
     pf::DeviceScene ds;
-    pf::DevBuf cellA, cellB, cellE, edges;
+    pf::DevBuf cellA, cellB, cellE, edges, cellN;
     bool edges_built = false;
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
@@ -122,7 +124,7 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
                            uint32_t *rec_used, cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
-                          cudaStream_t st);
+                          float *gn, cudaStream_t st);
 
 // stage timing helpers (pf_api.cu)
 void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev);

@@ -37,6 +37,9 @@ __global__ void __launch_bounds__(256) k0_edge_records(DeviceScene ds)
         ds.cellA[i] = make_float4(px, py, pz, ds.radii[i]);
         ds.cellB[i] = make_float4(ds.density[i], ds.rgb[3 * i], ds.rgb[3 * i + 1], ds.rgb[3 * i + 2]);
         ds.cellE[i] = make_uint2((uint32_t)ob, (uint32_t)(oe - ob));
+        if (ds.normals)
+            ds.cellN[i] = make_float4(ds.normals[3 * i], ds.normals[3 * i + 1],
+                                      ds.normals[3 * i + 2], 0.0f);
     }
     const int64_t base = __shfl_sync(0xffffffffu, ob, 0);
     const int last = (int)min((int64_t)31, ds.N - 1 - i0);
@@ -92,6 +95,11 @@ __global__ void k_validate(DeviceScene ds, int *flag)
     bad |= !isfinite(ds.weights[i]) ? 4 : 0;
     bad |= !(ds.radii[i] > 0.0f) || !isfinite(ds.radii[i]) ? 8 : 0;
     bad |= !(ds.density[i] >= 0.0f) || !isfinite(ds.density[i]) ? 16 : 0;
+    if (ds.normals) {
+        const float nx = ds.normals[3 * i], ny = ds.normals[3 * i + 1], nz = ds.normals[3 * i + 2];
+        if (!isfinite(nx) || !isfinite(ny) || !isfinite(nz) || (nx == 0.f && ny == 0.f && nz == 0.f))
+            bad |= 128;
+    }
     int64_t b = ds.nbr_off[i], e = ds.nbr_off[i + 1];
     if (b < 0 || e < b || e > ds.E) bad |= 32;
     else

@@ -22,7 +22,7 @@ namespace pf {
 
 namespace {
 
-constexpr int kEndSphere = -1, kEndNear = -2;
+constexpr int kEndSphere = -1, kEndNear = -2, kEndDipole = -3;
 
 struct Ray {
     float dx, dy, dz;      // unit direction
@@ -62,6 +62,7 @@ constexpr int kWarps = 8;
 struct WarpStage {
     float t0[32], e0x[32], e0y[32], e0z[32], cx[32], cy[32], cz[32], r[32];
     float sig[32], cr[32], cg[32], cb[32];
+    float4 *nrm;                    // dipole normals (NEXT-1) of the slots: separate smem, or null
     uint32_t eb[32], deg[32], cell[32];
 };
 
@@ -162,9 +163,10 @@ __device__ __forceinline__ void clip_plane(const Ray &R, const float4 E, int q, 
 
 // a9: clip the chord [-s, s] by the near plane and every neighbour's radical
 // plane (P:228, P:577-585 with the weight sign of SURVEY C1).
-template <bool kTrack>
+template <bool kTrack, bool kDipole>
 __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__restrict__ edges,
-                                              uint32_t eb, uint32_t deg, Seg &g, bool active)
+                                              uint32_t eb, uint32_t deg, Seg &g, bool active,
+                                              const WarpStage &S, int j)
 {
     g.lo = -g.s;
     g.lo_q = kEndSphere;
@@ -186,6 +188,8 @@ __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__rest
         clip_plane<kTrack>(R, E3, (int)q + 3, g);
     }
     for (; q < qe; ++q) clip_plane<kTrack>(R, __ldg(edges + q), (int)q, g);
+    if (kDipole)  // the occupied half (x - p_i).n_i <= 0: a plane through p_i with k = 0
+        clip_plane<kTrack>(R, S.nrm[j], kEndDipole, g);
     const float dt = __fsub_rn(g.hi, g.lo);
     g.dt = (active && dt > 0.0f) ? dt : 0.0f;
 }
@@ -255,6 +259,7 @@ __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, Pixe
 }
 
 // Stage cell `cell` into slot `slot` with the warp-centred frame (fp64 -> fp32).
+template <bool kDipole>
 __device__ __forceinline__ void stage_slot(WarpStage &S, int slot, const DeviceScene &ds,
                                            uint32_t cell, const float4 A, double c0, double c1,
                                            double c2, double t, const WarpCtx &W)
@@ -276,6 +281,10 @@ __device__ __forceinline__ void stage_slot(WarpStage &S, int slot, const DeviceS
     S.eb[slot] = E.x;
     S.deg[slot] = E.y;
     S.cell[slot] = cell;
+    if (kDipole) {
+        const float4 Nn = __ldg(ds.cellN + cell);
+        S.nrm[slot] = make_float4(Nn.x, Nn.y, Nn.z, 0.0f);
+    }
     // pull the cell's edge records towards L1 while the warp walks earlier cells
     if (E.y) {
         const float4 *ep = ds.edges + E.x;
@@ -299,6 +308,7 @@ __device__ __forceinline__ double cell_offset(const CamParams &cam, const float4
 // Cone test: the sphere (c, r) meets the cone (axis d_w, half-angle th) iff
 // the angle between c and d_w is <= th + asin(r/|c|), i.e. (|c| > r)
 // d_w.c >= cos(th) sqrt(|c|^2 - r^2) - sin(th) r;  always if |c| <= r.
+template <bool kDipole>
 __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene &ds,
                                                 const CamParams &cam,
                                                 const uint32_t *__restrict__ vals, uint32_t e,
@@ -323,7 +333,7 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
         }
     }
     const unsigned m = __ballot_sync(0xffffffffu, pass);
-    if (pass) stage_slot(S, lane, ds, cell, A, c0, c1, c2, t, W);
+    if (pass) stage_slot<kDipole>(S, lane, ds, cell, A, c0, c1, c2, t, W);
     __syncwarp();
     return m;
 }
@@ -334,7 +344,8 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
 // that produced a non-empty segment in at least one lane it writes a 72-byte
 // record: the lane mask, the entry's position in the chunk, and per lane the
 // binding constraints of the interval (lo, hi) coded in one byte each
-// (0 sphere, 1 near, 2+k plane k of the cell's list, 255 = not codable).  K7
+// (0 sphere, 1 near, 2+k plane k of the cell's list, 254 dipole face,
+// 255 = not codable).  K7
 // then replays only those entries and evaluates only the binding planes: the
 // interval values are bit-identical (fminf/fmaxf return one of their inputs,
 // and the winning input is recomputed with the same instructions).
@@ -353,8 +364,9 @@ __device__ __forceinline__ uint32_t end_code(int q, uint32_t eb, bool lo)
 {
     if (q == kEndSphere) return 0u;
     if (lo && q == kEndNear) return 1u;
+    if (q == kEndDipole) return 254u;
     const uint32_t k = (uint32_t)q - eb;
-    return k < 253u ? k + 2u : 255u;
+    return k < 252u ? k + 2u : 255u;
 }
 
 }  // namespace
@@ -368,7 +380,7 @@ __device__ __forceinline__ uint32_t end_code(int q, uint32_t eb, bool lo)
 #ifndef PF_K7_MINB
 #define PF_K7_MINB 4
 #endif
-template <bool kCount, bool kRecord>
+template <bool kCount, bool kRecord, bool kDipole>
 __global__ void __launch_bounds__(256, PF_K6_MINB)
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
@@ -381,8 +393,10 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
     __shared__ WarpRec WR[kRecord ? kWarps : 1];
+    __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
     const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
+    if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
     WarpRec &Rb = WR[kRecord ? warp : 0];
     PixelSetup P;
@@ -394,7 +408,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     uint32_t chunks = 0;
     for (uint32_t base = rg.x; base < rg.y; base += 32, ++chunks) {
         if (__all_sync(0xffffffffu, done)) break;
-        unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
+        unsigned m = stage_chunk<kDipole>(S, ds, cam, vals, base + lane, rg.y, W, lane);
         int nrec = 0;
         while (m) {
             const int j = __ffs(m) - 1;
@@ -403,7 +417,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
-            clip_interval<kRecord>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
+            clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, S, j);
             if (kCount && hit) {
                 ++xh;
                 xp += S.deg[j];
@@ -474,27 +488,37 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     }
 }
 
-cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           uint32_t *rec_used, cudaStream_t st)
+template <bool kDipole>
+static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *counters,
+                             uint32_t *rec_used, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
-    cudaEvent_t ev;
-    stage_begin(s, 6, st, &ev);
     if (counters)
-        k6_forward<true, false><<<T, 256, 0, st>>>(
+        k6_forward<true, false, kDipole><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
             nullptr, 0u);
     else if (rec_used)
-        k6_forward<false, true><<<T, 256, 0, st>>>(
+        k6_forward<false, true, kDipole><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
             (uint32_t)v.rec_cap);
     else
-        k6_forward<false, false><<<T, 256, 0, st>>>(
+        k6_forward<false, false, kDipole><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u);
+}
+
+cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
+                           uint32_t *rec_used, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 6, st, &ev);
+    if (s->ds.cellN)
+        launch_forward_t<true>(s, v, out, counters, rec_used, st);
+    else
+        launch_forward_t<false>(s, v, out, counters, rec_used, st);
     ++s->launches;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();
@@ -511,18 +535,34 @@ namespace {
 //                             dt/dw_i = 1/(2a), dt/dw_j = -1/(2a)
 //   near end: 0
 struct OwnGrad {
-    float px, py, pz, w, r;
+    float px, py, pz, w, r, nx, ny, nz;
 };
 
 // Accumulator layout: 12 floats per cell, acc[12 i + k]:
-//   k = 0..3 (p.x, p.y, p.z, w)  4..7 (r, sigma, R, G)  8 (B)  9..11 unused.
+//   k = 0..3 (p.x, p.y, p.z, w)  4..7 (r, sigma, R, G)  8 (B)  9..11 dipole normal.
+template <bool kDipole>
 __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, float tprime,
                                          float wgt, float rad, const float4 *__restrict__ edges,
-                                         const int32_t *__restrict__ nbr, float *acc, OwnGrad &o)
+                                         const int32_t *__restrict__ nbr, float *acc, OwnGrad &o,
+                                         const WarpStage &S, int jslot)
 {
     if (q == kEndNear) return;
     const float xpx = fmaf(tprime, R.dx, -g.ex), xpy = fmaf(tprime, R.dy, -g.ey),
                 xpz = fmaf(tprime, R.dz, -g.ez);   // x* - p_i
+    if (kDipole && q == kEndDipole) {
+        // dipole face t* = (p - Q).n / (d.n): dt/dp_i = n/a, dt/dn_i = (p_i - x*)/a
+        const float4 Nn = S.nrm[jslot];
+        const float nx = Nn.x, ny = Nn.y, nz = Nn.z;
+        const float a = fmaf(R.dx, nx, fmaf(R.dy, ny, __fmul_rn(R.dz, nz)));
+        const float f = __fdividef(wgt, a);
+        o.px = fmaf(f, nx, o.px);
+        o.py = fmaf(f, ny, o.py);
+        o.pz = fmaf(f, nz, o.pz);
+        o.nx = fmaf(-f, xpx, o.nx);
+        o.ny = fmaf(-f, xpy, o.ny);
+        o.nz = fmaf(-f, xpz, o.nz);
+        return;
+    }
     if (q == kEndSphere) {
         const float f = __fdividef(wgt, tprime);
         o.px = fmaf(f, xpx, o.px);
@@ -578,10 +618,30 @@ __device__ __forceinline__ void warp_reduce9_atomic(float v[10], float *acc_cell
     if (valid) atomicAdd(acc_cell + idx, y);
 }
 
+// Same for up to 16 values (slots padded to 16): 16 shuffles; lane (lane & 1) == 0
+// ends with the total of value ((lane >> 1) & 15).
+template <int K>
+__device__ __forceinline__ void warp_reduce16_atomic(float v[16], float *acc_cell, int lane)
+{
+#pragma unroll
+    for (int half = 8; half >= 1; half >>= 1) {
+        const bool up = lane & (2 * half);   // lane bit log2(2*half): keeps the upper half
+#pragma unroll
+        for (int k = 0; k < half; ++k) {
+            const float send = up ? v[k] : v[k + half], keep = up ? v[k + half] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * half);
+        }
+    }
+    float y = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int idx = (lane >> 1) & 15;
+    if (!(lane & 1) && idx < K) atomicAdd(acc_cell + idx, y);
+}
+
 // value of one interval end from its recorded constraint code (see end_code)
+template <bool kDipole>
 __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restrict__ edges,
                                            uint32_t eb, uint32_t code, bool lo, const Seg &g,
-                                           int &q)
+                                           int &q, const WarpStage &S, int j)
 {
     if (code == 0u) {
         q = kEndSphere;
@@ -591,8 +651,14 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
         q = kEndNear;
         return __fsub_rn(R.tnear, g.tc);
     }
-    q = (int)(eb + code - 2u);
-    const float4 E = __ldg(edges + q);
+    float4 E;
+    if (kDipole && code == 254u) {
+        q = kEndDipole;
+        E = S.nrm[j];
+    } else {
+        q = (int)(eb + code - 2u);
+        E = __ldg(edges + q);
+    }
     const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
     return __fmul_rn(b, rcp_approx(a));
@@ -605,11 +671,13 @@ struct BwdPixel {
     float GT_Tfin;
 };
 
+template <bool kDipole>
 __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, bool seg,
                                                  const WarpStage &S, int j, BwdPixel &px,
                                                  const DeviceScene &ds, float *acc, int lane)
 {
-    OwnGrad o = {0, 0, 0, 0, 0};
+    constexpr bool dipole = kDipole;
+    OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
     float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f;
     if (seg) {
         const float sig = S.sig[j], cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
@@ -631,8 +699,8 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
         const float gdt = dtau * sig;
         if (gdt != 0.0f) {
             const float rad = S.r[j];
-            end_grad(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o);
-            end_grad(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o);
+            end_grad<kDipole>(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o, S, j);
+            end_grad<kDipole>(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o, S, j);
         }
     }
     // own-cell terms: one lane alone issues its atomics, else a transposing warp
@@ -642,9 +710,15 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
     if (__popc(sm) == 1) {
         if (seg) {
             atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
+            if (dipole)
+                atomicAdd(reinterpret_cast<float4 *>(accc) + 2, make_float4(gB, o.nx, o.ny, o.nz));
+            else
+                atomicAdd(accc + 8, gB);
             atomicAdd(reinterpret_cast<float4 *>(accc) + 1, make_float4(o.r, gs, gR, gG));
-            atomicAdd(accc + 8, gB);
         }
+    } else if (dipole) {
+        float v[16] = {o.px, o.py, o.pz, o.w, o.r, gs, gR, gG, gB, o.nx, o.ny, o.nz, 0, 0, 0, 0};
+        warp_reduce16_atomic<12>(v, accc, lane);
     } else {
         float v[10] = {o.px, o.py, o.pz, o.w, o.r, gs, gR, gG, gB, 0.0f};
         warp_reduce9_atomic(v, accc, lane);
@@ -653,6 +727,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
 
 }  // namespace
 
+template <bool kDipole>
 __global__ void __launch_bounds__(256, PF_K7_MINB)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
@@ -664,8 +739,10 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
+    __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
     const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
+    if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
     PixelSetup P;
     setup_pixel(cam, tile, P, PR, W);
@@ -690,7 +767,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
         const uint32_t base = rg.x + 32u * c;
         if (d.y == kOverflow) {
             // records did not fit: full replay of this chunk (same code as K6)
-            unsigned m = stage_chunk(S, ds, cam, vals, base + lane, rg.y, W, lane);
+            unsigned m = stage_chunk<kDipole>(S, ds, cam, vals, base + lane, rg.y, W, lane);
             while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
@@ -698,10 +775,10 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 bool hit = false;
                 if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
                 if (!__any_sync(0xffffffffu, hit)) continue;
-                clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit);
+                clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, S, j);
                 const bool seg = g.dt > 0.0f;
                 if (!__any_sync(0xffffffffu, seg)) continue;
-                segment_backward(P.R, g, seg, S, j, px, ds, acc, lane);
+                segment_backward<kDipole>(P.R, g, seg, S, j, px, ds, acc, lane);
                 if (seg && px.T < kTStop) done = true;
             }
             __syncwarp();
@@ -719,7 +796,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const float4 A = __ldg(ds.cellA + cell);
             double x0, x1, x2;
             const double t = cell_offset(cam, A, W, x0, x1, x2);
-            stage_slot(S, lane, ds, cell, A, x0, x1, x2, t, W);
+            stage_slot<kDipole>(S, lane, ds, cell, A, x0, x1, x2, t, W);
         }
         __syncwarp();
         for (uint32_t k = 0; k < nrec; ++k) {
@@ -732,21 +809,21 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             if (seg) {
                 sphere_hit(P.R, S, j, g, ds, cam, PR);   // identical to K6 (recorded hit)
                 const uint32_t eb = S.eb[j];
-                g.lo = coded_end(P.R, ds.edges, eb, code & 0xffu, true, g, g.lo_q);
-                g.hi = coded_end(P.R, ds.edges, eb, code >> 8, false, g, g.hi_q);
+                g.lo = coded_end<kDipole>(P.R, ds.edges, eb, code & 0xffu, true, g, g.lo_q, S, j);
+                g.hi = coded_end<kDipole>(P.R, ds.edges, eb, code >> 8, false, g, g.hi_q, S, j);
             }
             const bool full = seg && (((code & 0xffu) == 255u) || ((code >> 8) == 255u));
             if (__any_sync(0xffffffffu, full)) {
                 Seg h = g;
                 if (full) {
-                    clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], h, true);
+                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], h, true, S, j);
                     g = h;
                 } else {
-                    clip_interval<true>(P.R, ds.edges, S.eb[j], S.deg[j], h, false);
+                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], h, false, S, j);
                 }
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
-            segment_backward(P.R, g, seg, S, j, px, ds, acc, lane);
+            segment_backward<kDipole>(P.R, g, seg, S, j, px, ds, acc, lane);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();
@@ -758,11 +835,16 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
     int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    k7_backward<<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order,
-                                   v.vals_p, v.saved.as<float4>(),
-                                   (const float4 *)grad_out, s->acc.as<float>(),
-                                   v.chunk_off, v.desc.as<uint2>(),
-                                   v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
+    if (s->ds.cellN)
+        k7_backward<true><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
+                                             v.saved.as<float4>(), (const float4 *)grad_out,
+                                             s->acc.as<float>(), v.chunk_off, v.desc.as<uint2>(),
+                                             v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
+    else
+        k7_backward<false><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
+                                              v.saved.as<float4>(), (const float4 *)grad_out,
+                                              s->acc.as<float>(), v.chunk_off, v.desc.as<uint2>(),
+                                              v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
     ++s->launches;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();
@@ -773,7 +855,7 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
 // ------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 k8_unpack(int64_t N, const float4 *__restrict__ acc, float *gs, float *gw, float *gr, float *gd,
-          float *gc)
+          float *gc, float *gn)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
@@ -787,15 +869,20 @@ k8_unpack(int64_t N, const float4 *__restrict__ acc, float *gs, float *gw, float
     gc[3 * i + 0] += b.z;
     gc[3 * i + 1] += b.w;
     gc[3 * i + 2] += c.x;
+    if (gn) {
+        gn[3 * i + 0] += c.y;
+        gn[3 * i + 1] += c.z;
+        gn[3 * i + 2] += c.w;
+    }
 }
 
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
-                          cudaStream_t st)
+                          float *gn, cudaStream_t st)
 {
     int64_t N = s->ds.N;
     cudaEvent_t ev;
     stage_begin(s, 8, st, &ev);
-    k8_unpack<<<ceil_div(N, 256), 256, 0, st>>>(N, s->acc.as<float4>(), gs, gw, gr, gd, gc);
+    k8_unpack<<<ceil_div(N, 256), 256, 0, st>>>(N, s->acc.as<float4>(), gs, gw, gr, gd, gc, gn);
     ++s->launches;
     stage_end(s, 8, st, ev);
     return cudaGetLastError();

@@ -41,6 +41,10 @@ def case(name, variant=None):
         elif name == "train8_1m":
             sc = pf_synth.make_scene("train8_1m")
             cams = pf_synth.make_cameras("train8_1m")
+        elif name.endswith("+dipoles"):
+            base, bcams = case(name[:-len("+dipoles")], variant)
+            sc = pf_synth.add_dipoles(base.copy())
+            cams = bcams
         else:
             raise KeyError(name)
         _cache[key] = (sc, cams)
@@ -54,7 +58,9 @@ def renderer(sc, flags=None):
 
 def grad_check(gpu, ref, tol=GRAD_TOL):
     msgs = []
-    for k in ("sites", "weights", "radii", "density", "rgb"):
+    keys = ("sites", "weights", "radii", "density", "rgb") + (("normals",) if "normals" in ref
+                                                               else ())
+    for k in keys:
         a = gpu[k].detach().cpu().numpy().astype(np.float64).reshape(-1)
         b = ref[k].reshape(-1)
         nb = np.linalg.norm(b)
@@ -278,3 +284,62 @@ def test_abi_argument_errors():
     with pytest.raises(pf.PFError):
         r.forward([c])
     r.close()
+
+
+# --------------------------------------------------------------- dipoles (NEXT-1)
+
+@pytest.mark.parametrize("name,variant", [("tiny+dipoles", "outside"), ("tiny+dipoles", "inside"),
+                                          ("small+dipoles", None), ("small360+dipoles", None)])
+def test_dipole_forward_and_backward_full_image(name, variant):
+    sc, cams = case(name, variant)
+    r = renderer(sc)
+    cams = cams[:2]
+    H, W = cams[0].height, cams[0].width
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    mode = oracle.O1 if name.startswith("tiny") else oracle.O3
+    for v, cam in enumerate(cams):
+        ref = oracle.render(sc, cam, mode=mode)["out"]
+        assert np.abs(out[v] - ref).max() <= IMG_TOL
+    g = pf_synth.make_grad_out(len(cams), H, W, seed=13)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    assert "normals" in got
+    ref = None
+    for v, cam in enumerate(cams):
+        o = oracle.backward(sc, cam, g[v], mode=mode)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+
+
+def test_dipole_large_sampled_pixels():
+    sc, cams = case("nerfsynth200k+dipoles")
+    r = renderer(sc, flags=0)
+    H, W = cams[0].height, cams[0].width
+    rng = np.random.default_rng(2)
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    g = np.zeros((len(cams), H, W, 4), np.float32)
+    pix = {}
+    for v in (0, len(cams) - 1):
+        p = np.unique(np.stack([rng.integers(0, W, 1500), rng.integers(0, H, 1500)], 1), axis=0)
+        pix[v] = p
+        ref = oracle.render(sc, cams[v], mode=oracle.O3, pixels=p)["out"]
+        assert np.abs(out[v][p[:, 1], p[:, 0]] - ref).max() <= IMG_TOL
+        g[v, p[:, 1], p[:, 0]] = rng.standard_normal((p.shape[0], 4)).astype(np.float32)
+    r.forward(cams)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    ref = None
+    for v, p in pix.items():
+        o = oracle.backward(sc, cams[v], g[v, p[:, 1], p[:, 0]], mode=oracle.O3, pixels=p)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+
+
+def test_dipole_validation_rejects_zero_normal():
+    import paper_2604_24994_b200 as pf
+    sc, _ = case("tiny+dipoles", "outside")
+    bad = sc.copy()
+    bad.normals[5] = 0.0
+    with pytest.raises(pf.PFError) as e:
+        renderer(bad)
+    assert e.value.status == 1
