@@ -58,6 +58,8 @@ def lib():
                                     P, P, P, C.c_int]
         L.oracle_backward.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P,
                                       P, P, P, P, P, P, C.c_int]
+        L.oracle_cell_stats.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P,
+                                         P, C.c_int]
         L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, P, i64, P, P,
                                            C.c_double, P, P]
         L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P,
@@ -191,6 +193,24 @@ def backward(sc, cam, grad_out, mode=O3, pixels=None, nthreads=0):
     if gn is not None:
         out["normals"] = gn
     return out
+
+
+def cell_stats(sc, cam, mode=O3, pixels=None, nthreads=0):
+    """Per-cell forward by-products: contrib = sum T_k alpha_k (L_sparse / pruning),
+    normal = sum T_k alpha_k max(n.d, 0)^2 (L_normal; dipole scenes only)."""
+    A = _SceneArrays(sc)
+    oc = make_camera(cam)
+    if pixels is None:
+        n = cam.width * cam.height
+        pix = None
+    else:
+        pix = _c(np.asarray(pixels).reshape(-1, 2), np.int32)
+        n = pix.shape[0]
+    contrib = np.zeros(A.N)
+    normal = np.zeros(A.N) if A.normals is not None else None
+    lib().oracle_cell_stats(mode, *A.args(), C.byref(oc), n, _p(pix), _p(contrib), _p(normal),
+                            nthreads)
+    return dict(contrib=contrib, normal=normal)
 
 
 def cell_interval(sc, i, Q, d, t_near=0.0, mode=O2):

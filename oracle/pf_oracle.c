@@ -609,6 +609,64 @@ int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
     return 0;
 }
 
+/*
+ * Per-cell by-products of the forward (NEXT-1; P:308 pruning statistic, P:728
+ * L_sparse, P:718 L_normal): over the given pixels and their composited
+ * segments k (termination as in composite()),
+ *   contrib[i]     += T_k alpha_k
+ *   normal_term[i] += T_k alpha_k max(n_i . d, 0)^2      (needs dipole normals)
+ * Accumulates (+=) into double arrays; normal_term may be NULL.
+ */
+int oracle_cell_stats(int mode, int64_t N, const float *sites, const float *weights,
+                      const float *radii, const float *density, const float *rgb,
+                      const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
+                      const float *normals, const oc_camera *cam, int64_t npix,
+                      const int32_t *pix_xy, double *contrib, double *normal_term, int nthreads)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
+    oc_bins B;
+    memset(&B, 0, sizeof(B));
+    if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
+    if (!pix_xy) npix = (int64_t)cam->width * cam->height;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel
+    {
+        oc_scratch scr = {NULL, 0};
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t q = 0; q < npix; ++q) {
+            int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
+            int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
+            double Q[3], d[3], tn, out[4];
+            pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+            int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL);
+            int64_t K = composite(&S, scr.segs, n, out);
+            double T = 1.0;
+            for (int64_t k = 0; k < K; ++k) {
+                const oc_seg *sg = scr.segs + k;
+                int64_t i = sg->cell;
+                double tau = (double)S.density[i] * (sg->t_out - sg->t_in);
+                double w = T * (1.0 - exp(-tau));
+#pragma omp atomic
+                contrib[i] += w;
+                if (normal_term && normals) {
+                    const float *nn = normals + 3 * i;
+                    double nd = nn[0] * d[0] + nn[1] * d[1] + nn[2] * d[2];
+                    double m = nd > 0.0 ? nd : 0.0;
+#pragma omp atomic
+                    normal_term[i] += w * m * m;
+                }
+                T *= exp(-tau);
+            }
+        }
+        free(scr.segs);
+    }
+    if (B.vals) free_bins(&B);
+    return 0;
+}
+
 /* ======================================================================== */
 /* (2) backward                                                             */
 /* ======================================================================== */

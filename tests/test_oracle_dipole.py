@@ -147,3 +147,26 @@ def test_dipole_modes_agree_and_theorem2():
     r3 = oracle.render(sc, cam, mode=oracle.O3, pixels=pix)
     assert np.abs(r1["out"] - r3["out"]).max() < 1e-12
     assert oracle.render(sc, cam, mode=oracle.O3)["viol"] == 0
+
+
+def test_cell_stats_telescoping_and_closed_form():
+    """sum_i contrib_i = sum_pixels (1 - T_final) (the weights T_k alpha_k telescope);
+    single cell on the optical axis: contrib = 1 - e^{-sigma L}, normal term =
+    contrib * max(n.d, 0)^2 (P:718, P:728)."""
+    sc = pf_synth.make_scene("tiny", dipoles=True)
+    cam = pf_synth.make_cameras("tiny")[0]
+    st = oracle.cell_stats(sc, cam, mode=oracle.O2)
+    img = oracle.render(sc, cam, mode=oracle.O2)["out"]
+    assert st["contrib"].sum() == pytest.approx((1.0 - img[..., 3]).sum(), rel=1e-12)
+    assert np.all(st["normal"] <= st["contrib"] + 1e-15) and st["normal"].sum() > 0
+    nrm = np.array([0.0, 0.6, 0.8], np.float32)   # n.d = 0.8 > 0 on the axis
+    one = _one(nrm, r=0.5)
+    one.density = np.array([2.0], np.float32)
+    cam1 = camera(W=3, H=3, f=50.0)            # pixel (1,1): the optical axis (+z)
+    s1 = oracle.cell_stats(one, cam1, mode=oracle.O1, pixels=np.array([[1, 1]]))
+    Q, d, _ = ray_np(cam1, 1, 1)
+    hit, tin, tout, _ = oracle.cell_interval(one, 0, Q, d, mode=oracle.O1)
+    a = 1 - math.exp(-2.0 * (tout - tin))
+    assert s1["contrib"][0] == pytest.approx(a, rel=1e-12)
+    nd = max(float(nrm.astype(np.float64) @ d), 0.0)
+    assert nd > 0.5 and s1["normal"][0] == pytest.approx(a * nd * nd, rel=1e-12)
