@@ -125,6 +125,21 @@ PF_API int pf_create_scene(const pf_scene_desc *desc, pf_scene **out, pf_stream_
 PF_API int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t num_views, float *out,
                       pf_stream_t stream);
 
+/* Optional per-cell by-products of a forward (NEXT-1), accumulated (+=) over the
+ * pixels of all views of the call; device f32[N] arrays, or NULL:
+ *   contrib[i]     += sum over composited segments of cell i of T_k alpha_k
+ *                     (the pruning statistic, and L_sparse)
+ *   normal_term[i] += sum of T_k alpha_k max(n_i . d, 0)^2  (L_normal, P:718;
+ *                     only with dipole normals). */
+typedef struct {
+    float *contrib;
+    float *normal_term;
+} pf_forward_extras;
+
+/* pf_render_forward plus the by-products above (ex may be NULL). */
+PF_API int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t num_views, float *out,
+                                const pf_forward_extras *ex, pf_stream_t stream);
+
 /*
  * Backward of the immediately preceding pf_render_forward with the same cameras
  * (else PF_ERR_STATE).  grad_out: device f32[V,H,W,4] = dL/d(out) (channel 3 =

@@ -26,7 +26,7 @@ STAGES = ["K0_edge_records", "K1_preprocess", "K2_scan", "K3_emit", "K4_sort", "
 _STATUS = {0: "PF_OK", 1: "PF_ERR_INVALID_ARGUMENT", 2: "PF_ERR_CUDA",
            3: "PF_ERR_OUT_OF_MEMORY", 4: "PF_ERR_STATE"}
 
-EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_backward",
+EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_forward_ex", "pf_render_backward",
            "pf_render_backward_ex", "pf_destroy",
            "pf_last_error", "pf_debug_binning", "pf_debug_counters", "pf_launch_count",
            "pf_set_profiling", "pf_stage_times", "pf_last_pair_counts"]
@@ -81,6 +81,7 @@ def load_library(build_if_missing: bool = True):
     P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
     L.pf_create_scene.argtypes = [C.POINTER(_SceneDesc), C.POINTER(C.c_void_p), P]
     L.pf_render_forward.argtypes = [P, C.POINTER(_Camera), i32, P, P]
+    L.pf_render_forward_ex.argtypes = [P, C.POINTER(_Camera), i32, P, P, P]
     L.pf_render_backward.argtypes = [P, C.POINTER(_Camera), i32, P, P, P, P, P, P, P]
     L.pf_render_backward_ex.argtypes = [P, C.POINTER(_Camera), i32, P, C.POINTER(_Grads), P]
     L.pf_destroy.argtypes = [P]
@@ -198,14 +199,22 @@ class Renderer:
         return (12 if self.has_normals else 9) * self.N
 
     # -------------------------------------------------------------- hot path
-    def forward(self, cams, out=None, stream=None):
+    def forward(self, cams, out=None, stream=None, stats=None):
+        """Renders the views into out f32[V,H,W,4].  stats: optional dict with
+        f32[N] tensors 'contrib' (+= sum T alpha) and 'normal' (+= sum T alpha
+        max(n.d,0)^2, dipole scenes)."""
         arr, V = _cams(cams)
         H, W = arr[0].height, arr[0].width
         if out is None:
             out = torch.empty((V, H, W, 4), device=self.device, dtype=torch.float32)
         _dev_f32(out, (V, H, W, 4))
-        _check(self._L.pf_render_forward(self._h, arr, V, C.c_void_p(out.data_ptr()),
-                                         _stream(stream)))
+        ex = None
+        if stats is not None:
+            ex = (C.c_void_p * 2)(_dev_f32(stats["contrib"], (self.N,)).value,
+                                  _dev_f32(stats["normal"], (self.N,)).value
+                                  if stats.get("normal") is not None else None)
+        _check(self._L.pf_render_forward_ex(self._h, arr, V, C.c_void_p(out.data_ptr()),
+                                            ex, _stream(stream)))
         return out
 
     def backward(self, cams, grad_out, grads=None, stream=None):

@@ -394,6 +394,12 @@ int pf_destroy(pf_scene *s)
 int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
                       pf_stream_t stream)
 {
+    return pf_render_forward_ex(s, cams, V, out, nullptr, stream);
+}
+
+int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
+                         const pf_forward_extras *ex, pf_stream_t stream)
+{
     if (!s) return fail(PF_ERR_INVALID_ARGUMENT, "scene handle is NULL");
     if (!cams || V < 1) return fail(PF_ERR_INVALID_ARGUMENT, "need >= 1 camera");
     if (!out) return fail(PF_ERR_INVALID_ARGUMENT, "out is NULL");
@@ -446,7 +452,8 @@ int pf_render_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out,
             PF_CUDA(vs.rec.reserve(72 * (size_t)vs.rec_cap));
             used = s->rec_used.as<uint32_t>() + v;
         }
-        PF_CUDA(pf::launch_forward(s, vs, out + 4 * npix * (size_t)v, nullptr, used, st));
+        PF_CUDA(pf::launch_forward(s, vs, out + 4 * npix * (size_t)v, nullptr, used,
+                                   ex ? ex->contrib : nullptr, ex ? ex->normal_term : nullptr, st));
     }
     if (record) {
         if (s->pinned_rec_n < V) {
@@ -573,7 +580,7 @@ int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_s
     rc = emit_sort_ranges(s, &vs, 1, st, &ks);
     if (rc) return rc;
     PF_CUDA(cudaMemsetAsync(counters, 0, 32 * (size_t)cam->width * cam->height, st));
-    PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, nullptr, st));
+    PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, nullptr, nullptr, nullptr, st));
     PF_CUDA(cudaStreamSynchronize(st));
     return PF_OK;
 }

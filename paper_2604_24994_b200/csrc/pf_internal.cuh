@@ -121,7 +121,8 @@ cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, i
 cudaError_t launch_tile_order(pf_scene *s, const uint2 *ranges_all, int T, int V,
                               uint32_t *order_all, uint32_t *chunk_off_all, cudaStream_t st);
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           uint32_t *rec_used, cudaStream_t st);
+                           uint32_t *rec_used, float *st_contrib, float *st_normal,
+                           cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
                           float *gn, cudaStream_t st);

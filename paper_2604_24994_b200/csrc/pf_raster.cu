@@ -387,7 +387,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
            const uint32_t *__restrict__ chunk_off, uint2 *__restrict__ desc,
            uint32_t *__restrict__ wdone, uint32_t *__restrict__ rec, uint32_t *__restrict__ rec_used,
-           uint32_t rec_cap)
+           uint32_t rec_cap, float *__restrict__ st_contrib, float *__restrict__ st_normal)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
@@ -437,13 +437,35 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                     ++nrec;
                 }
             }
+            float wk = 0.0f;
             if (seg) {
                 float alpha;
+                const float Tk = T;
                 composite_step(S.sig[j], g.dt, S.cr[j], S.cg[j], S.cb[j], T, Cr, Cg, Cb, alpha);
+                wk = __fmul_rn(Tk, alpha);
                 if (kCount) ++xc;
                 if (T < kTStop) {
                     done = true;
                     if (kCount) xs = (long long)(base + j - rg.x) + 1;
+                }
+            }
+            if (st_contrib && __any_sync(0xffffffffu, seg)) {
+                // NEXT-1 by-products: sum T_k alpha_k (pruning / L_sparse) and
+                // sum T_k alpha_k max(n.d, 0)^2 (L_normal), warp-reduced per cell
+                float wn = 0.0f;
+                if (kDipole && seg) {
+                    const float4 Nn = S.nrm[j];
+                    const float nd = fmaxf(fmaf(P.R.dx, Nn.x, fmaf(P.R.dy, Nn.y, __fmul_rn(P.R.dz, Nn.z))), 0.0f);
+                    wn = wk * nd * nd;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    wk += __shfl_xor_sync(0xffffffffu, wk, o);
+                    if (kDipole) wn += __shfl_xor_sync(0xffffffffu, wn, o);
+                }
+                if (lane == 0) {
+                    atomicAdd(st_contrib + S.cell[j], wk);
+                    if (kDipole && st_normal) atomicAdd(st_normal + S.cell[j], wn);
                 }
             }
             if (__all_sync(0xffffffffu, done)) break;
@@ -490,35 +512,37 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
 
 template <bool kDipole>
 static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                             uint32_t *rec_used, cudaStream_t st)
+                             uint32_t *rec_used, float *stc, float *stn, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
     if (counters)
         k6_forward<true, false, kDipole><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
-            nullptr, 0u);
+            nullptr, 0u, nullptr, nullptr);
     else if (rec_used)
         k6_forward<false, true, kDipole><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
-            (uint32_t)v.rec_cap);
+            (uint32_t)v.rec_cap, stc, stn);
     else
         k6_forward<false, false, kDipole><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
-            (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u);
+            (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
+            stc, stn);
 }
 
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           uint32_t *rec_used, cudaStream_t st)
+                           uint32_t *rec_used, float *st_contrib, float *st_normal,
+                           cudaStream_t st)
 {
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
     if (s->ds.cellN)
-        launch_forward_t<true>(s, v, out, counters, rec_used, st);
+        launch_forward_t<true>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     else
-        launch_forward_t<false>(s, v, out, counters, rec_used, st);
+        launch_forward_t<false>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     ++s->launches;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();

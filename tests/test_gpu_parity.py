@@ -343,3 +343,30 @@ def test_dipole_validation_rejects_zero_normal():
     with pytest.raises(pf.PFError) as e:
         renderer(bad)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("name", ["small", "small360+dipoles"])
+def test_forward_by_products_match_oracle(name):
+    """NEXT-1 by-products of the forward: per-cell sum T alpha (and the L_normal term
+    with dipoles) against the oracle, plus the telescoping identity on the GPU."""
+    sc, cams = case(name)
+    r = renderer(sc)
+    N = sc.num_cells
+    st = {"contrib": torch.zeros(N, device="cuda"),
+          "normal": torch.zeros(N, device="cuda") if sc.normals is not None else None}
+    out = r.forward(cams[:2], stats=st)
+    c = st["contrib"].double().cpu().numpy()
+    ref_c = np.zeros(N)
+    ref_n = np.zeros(N)
+    for cam in cams[:2]:
+        o = oracle.cell_stats(sc, cam, mode=oracle.O3)
+        ref_c += o["contrib"]
+        if o["normal"] is not None:
+            ref_n += o["normal"]
+    assert np.linalg.norm(c - ref_c) <= 1e-4 * np.linalg.norm(ref_c)
+    tel = (1.0 - out[..., 3].double()).sum().item()
+    assert abs(c.sum() - tel) <= 1e-4 * tel
+    if st["normal"] is not None:
+        nn = st["normal"].double().cpu().numpy()
+        assert np.linalg.norm(nn - ref_n) <= 1e-4 * np.linalg.norm(ref_n)
+    r.close()
