@@ -60,6 +60,8 @@ def lib():
                                       P, P, P, P, P, P, C.c_int]
         L.oracle_cell_stats.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P,
                                          P, C.c_int]
+        L.oracle_cech_rows.argtypes = [i64, P, P, i64, P, P, P, P, C.c_int]
+        L.oracle_connect_loss.argtypes = [i64, P, P, P, P, P, P, P]
         L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, P, i64, P, P,
                                            C.c_double, P, P]
         L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P,
@@ -255,3 +257,38 @@ def composite(sigma, dt, rgb, bg=(0.0, 0.0, 0.0)):
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: Čech graph and L_connect
+# ---------------------------------------------------------------------------
+
+def cech_rows(sites, radii, rows=None, nthreads=0):
+    """Brute-force Čech neighbour rows (ascending j).  rows=None -> all cells.
+    Returns (offsets i64[n+1], indices i32[E])."""
+    sites = _c(sites, np.float32).reshape(-1, 3)
+    radii = _c(radii, np.float32).reshape(-1)
+    N = sites.shape[0]
+    rws = np.arange(N, dtype=np.int64) if rows is None else _c(rows, np.int64)
+    n = rws.shape[0]
+    counts = np.zeros(n, np.int64)
+    L = lib()
+    L.oracle_cech_rows(N, _p(sites), _p(radii), n, _p(rws), _p(counts), None, None, nthreads)
+    offs = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=offs[1:])
+    idx = np.zeros(max(int(offs[-1]), 1), np.int32)
+    L.oracle_cech_rows(N, _p(sites), _p(radii), n, _p(rws), _p(counts), _p(offs[:-1].copy()),
+                       _p(idx), nthreads)
+    return offs, idx[:int(offs[-1])]
+
+
+def connect_loss(sites, radii, offsets, indices):
+    """L_connect per cell and the gradient of its sum."""
+    sites = _c(sites, np.float32).reshape(-1, 3)
+    radii = _c(radii, np.float32).reshape(-1)
+    N = sites.shape[0]
+    off = _c(offsets, np.int64)
+    idx = _c(indices, np.int32) if len(indices) else np.zeros(1, np.int32)
+    loss = np.zeros(N); gs = np.zeros((N, 3)); gr = np.zeros(N)
+    lib().oracle_connect_loss(N, _p(sites), _p(radii), _p(off), _p(idx), _p(loss), _p(gs), _p(gr))
+    return dict(loss=loss, sites=gs, radii=gr)

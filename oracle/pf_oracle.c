@@ -913,3 +913,79 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* ======================================================================== */
+/* NEXT-3: the Čech graph ("the graph of all overlapping spheres")    */
+/* ======================================================================== */
+
+/* Edge (i, j), i != j, iff |p_i - p_j| < r_i + r_j (strict),
+ * evaluated in double in this fixed order (the inputs are fp32, so every
+ * difference is exact):  d2 = (dx*dx + dy*dy) + dz*dz,  s = r_i + r_j,  d2 < s*s. */
+static int cech_edge(const float *sites, const float *radii, int64_t i, int64_t j)
+{
+    double dx = (double)sites[3 * i] - (double)sites[3 * j];
+    double dy = (double)sites[3 * i + 1] - (double)sites[3 * j + 1];
+    double dz = (double)sites[3 * i + 2] - (double)sites[3 * j + 2];
+    double d2 = (dx * dx + dy * dy) + dz * dz;
+    double s = (double)radii[i] + (double)radii[j];
+    return d2 < s * s;
+}
+
+/* Brute-force rows of the Čech graph: for each requested row i (rows[k]), every
+ * j in [0, N) in ascending order.  counts[k] = degree; if indices != NULL the
+ * neighbours of row k are written at indices[offs[k] ...] (offs = exclusive scan
+ * of counts, computed by the caller).  O(nrows * N). */
+int oracle_cech_rows(int64_t N, const float *sites, const float *radii, int64_t nrows,
+                     const int64_t *rows, int64_t *counts, const int64_t *offs, int32_t *indices,
+                     int nthreads)
+{
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t k = 0; k < nrows; ++k) {
+        int64_t i = rows[k], c = 0;
+        for (int64_t j = 0; j < N; ++j) {
+            if (j == i || !cech_edge(sites, radii, i, j)) continue;
+            if (indices) indices[offs[k] + c] = (int32_t)j;
+            ++c;
+        }
+        counts[k] = c;
+    }
+    return 0;
+}
+
+/* L_connect:  L(P_i) = sum_{j in Cech(i)} max(r_i + r_j - d_ij, 0)^2 for
+ * every cell (so the total counts each overlapping pair from both ends), and its
+ * gradient: with o = max(r_i + r_j - d_ij, 0), u = (p_i - p_j)/d_ij,
+ *   dL(P_i)/dr_i = dL(P_i)/dr_j = 2o,  dL(P_i)/dp_i = -2o u,  dL(P_i)/dp_j = +2o u.
+ * g_sites / g_radii accumulate d(sum_i L(P_i)); loss[i] = L(P_i). */
+int oracle_connect_loss(int64_t N, const float *sites, const float *radii,
+                        const int64_t *nbr_off, const int32_t *nbr_idx, double *loss,
+                        double *g_sites, double *g_radii)
+{
+    for (int64_t i = 0; i < N; ++i) {
+        double Li = 0.0;
+        for (int64_t q = nbr_off[i]; q < nbr_off[i + 1]; ++q) {
+            int64_t j = nbr_idx[q];
+            double dv[3], d2 = 0.0;
+            for (int m = 0; m < 3; ++m) {
+                dv[m] = (double)sites[3 * i + m] - (double)sites[3 * j + m];
+                d2 += dv[m] * dv[m];
+            }
+            double d = sqrt(d2);
+            double o = (double)radii[i] + (double)radii[j] - d;
+            if (o <= 0.0) continue;
+            Li += o * o;
+            g_radii[i] += 2.0 * o;
+            g_radii[j] += 2.0 * o;
+            if (d > 0.0)
+                for (int m = 0; m < 3; ++m) {
+                    g_sites[3 * i + m] -= 2.0 * o * dv[m] / d;
+                    g_sites[3 * j + m] += 2.0 * o * dv[m] / d;
+                }
+        }
+        loss[i] = Li;
+    }
+    return 0;
+}
