@@ -401,6 +401,27 @@ def main():
     sort_gbs = sort_bytes / (sort_ms / max(sort_n, 1) / 1e3) / 1e9 if sort_ms > 0 else None
     hbm = float(peaks.get("hbm_gbs", 6650.0))
 
+    # ---------------- NEXT-3: GPU Čech graph build of this scene (extra) --------
+    cech = None
+    try:
+        cb = pf.CechBuilder()
+        st_, ra_ = r._tensors[0], r._tensors[2]
+        off_, idx_ = cb.build(st_, ra_)
+        ok = bool(torch.equal(off_, r._tensors[5]) and torch.equal(idx_, r._tensors[6]))
+        ts_ = []
+        for _ in range(5):
+            c0_, c1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0_.record(stream)
+            cb.build(st_, ra_)
+            c1_.record(stream)
+            torch.cuda.synchronize()
+            ts_.append(c0_.elapsed_time(c1_))
+        cech = {"build_ms": float(np.median(ts_)), "edges": int(idx_.numel()),
+                "equals_input_lists": ok, "note": "pf_cech_build (LBVH), incl. its one sync"}
+        cb.close()
+    except Exception as ex:  # noqa
+        cech = {"error": str(ex)}
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
@@ -434,7 +455,7 @@ def main():
             "sort": {"ms_per_launch": sort_ms / max(sort_n, 1), "pairs_per_launch": P * nv,
                      "passes": passes, "bytes_per_launch": sort_bytes, "achieved_gbs": sort_gbs,
                      "hbm_frac": (sort_gbs / hbm) if sort_gbs else None},
-            "peaks_source": peaks_kind, "scene_gen_s": t_gen,
+            "peaks_source": peaks_kind, "scene_gen_s": t_gen, "cech_graph": cech,
         }
         print(json.dumps(line), flush=True)
     r.close()

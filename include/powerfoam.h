@@ -215,6 +215,42 @@ PF_API int pf_stage_times(pf_scene *s, double *ms /* [PF_NUM_STAGES] */,
 /* Pairs P of each view of the last forward (host int64[num_views]). */
 PF_API int pf_last_pair_counts(const pf_scene *s, int64_t *pairs, int32_t num_views);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-3: the Čech graph on the GPU (the graph of all overlapping
+ * spheres, "significantly cheaper to construct using GPU-accelerated collision
+ * detection") and the connectivity loss L_connect.
+ * ------------------------------------------------------------------------- */
+typedef struct pf_cech pf_cech; /* opaque builder; owns grow-only workspaces */
+
+PF_API int pf_cech_create(pf_cech **out);
+PF_API int pf_cech_destroy(pf_cech *h);
+PF_API const char *pf_cech_last_error(void);
+
+/*
+ * Builds the CSR neighbour lists of the Čech complex of N spheres (device
+ * sites f32[N,3], radii f32[N]): j is a neighbour of i iff i != j and
+ * |p_i - p_j| < r_i + r_j (strict), evaluated in double as
+ * ((dx*dx + dy*dy) + dz*dz) < (r_i + r_j)^2.  Writes nbr_offsets (device i64[N+1])
+ * and *num_edges (host); if nbr_indices != NULL and capacity >= E, also the
+ * indices (device i32[E]), each row ascending (canonical).  Otherwise call again
+ * with an array of at least *num_edges entries.  One stream sync per call.
+ * The output feeds pf_scene_desc (with w = r^2 the lists are exact).
+ */
+PF_API int pf_cech_build(pf_cech *h, int64_t num_cells, const float *sites, const float *radii,
+                         int64_t *nbr_offsets, int32_t *nbr_indices, int64_t capacity,
+                         int64_t *num_edges, pf_stream_t stream);
+
+/*
+ * L_connect over given lists: loss[i] = sum_{j in N(i)} max(r_i + r_j - d_ij, 0)^2
+ * (device f32[N], or NULL); gradients of sum_i loss[i] are ACCUMULATED (+=) into
+ * grad_sites [N,3] / grad_radii [N] (device, or NULL).  Asynchronous.
+ */
+PF_API int pf_connect_loss(int64_t num_cells, const float *sites, const float *radii,
+                           const int64_t *nbr_offsets, const int32_t *nbr_indices, float *loss,
+                           float *grad_sites, float *grad_radii, pf_stream_t stream);
+
+PF_API int64_t pf_cech_launch_count(const pf_cech *h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,9 @@ _STATUS = {0: "PF_OK", 1: "PF_ERR_INVALID_ARGUMENT", 2: "PF_ERR_CUDA",
 EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_forward_ex", "pf_render_backward",
            "pf_render_backward_ex", "pf_destroy",
            "pf_last_error", "pf_debug_binning", "pf_debug_counters", "pf_launch_count",
-           "pf_set_profiling", "pf_stage_times", "pf_last_pair_counts"]
+           "pf_set_profiling", "pf_stage_times", "pf_last_pair_counts",
+           "pf_cech_create", "pf_cech_destroy", "pf_cech_last_error", "pf_cech_build",
+           "pf_connect_loss", "pf_cech_launch_count"]
 
 
 class PFError(RuntimeError):
@@ -93,10 +95,19 @@ def load_library(build_if_missing: bool = True):
     L.pf_set_profiling.argtypes = [P, C.c_int]
     L.pf_stage_times.argtypes = [P, P, P]
     L.pf_last_pair_counts.argtypes = [P, P, i32]
+    L.pf_cech_create.argtypes = [C.POINTER(C.c_void_p)]
+    L.pf_cech_destroy.argtypes = [P]
+    L.pf_cech_last_error.restype = C.c_char_p
+    L.pf_cech_build.argtypes = [P, i64, P, P, P, P, i64, C.POINTER(i64), P]
+    L.pf_connect_loss.argtypes = [i64, P, P, P, P, P, P, P, P]
+    L.pf_cech_launch_count.argtypes = [P]
+    L.pf_cech_launch_count.restype = i64
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or C.c_int
     L.pf_last_error.restype = C.c_char_p
+    L.pf_cech_last_error.restype = C.c_char_p
     L.pf_launch_count.restype = i64
+    L.pf_cech_launch_count.restype = i64
     _lib = L
     return L
 
@@ -325,3 +336,77 @@ def render(renderer: Renderer, cams):
     """Autograd-aware forward over the renderer's parameter tensors."""
     s, w, r, d, c, _, _, n = renderer._tensors
     return _RenderFn.apply(renderer, cams, s, w, r, d, c, n)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: Čech graph builder and L_connect
+# ---------------------------------------------------------------------------
+
+def _check_cech(status: int):
+    if status != 0:
+        raise PFError(status, load_library().pf_cech_last_error().decode())
+
+
+class CechBuilder:
+    """GPU Čech complex (all overlapping sphere pairs) as CSR lists."""
+
+    def __init__(self):
+        self._L = load_library()
+        h = C.c_void_p()
+        _check_cech(self._L.pf_cech_create(C.byref(h)))
+        self._h = h
+        self._cap = 0
+
+    def build(self, sites, radii, stream=None):
+        """sites f32[N,3], radii f32[N] (CUDA) -> (nbr_offsets i64[N+1], nbr_indices i32[E])."""
+        _dev_f32(sites)
+        _dev_f32(radii)
+        N = int(sites.shape[0])
+        offs = torch.empty(N + 1, device=sites.device, dtype=torch.int64)
+        cap = max(self._cap, 16 * N)
+        idx = torch.empty(max(cap, 1), device=sites.device, dtype=torch.int32)
+        E = C.c_int64()
+        _check_cech(self._L.pf_cech_build(self._h, N, C.c_void_p(sites.data_ptr()),
+                                          C.c_void_p(radii.data_ptr()),
+                                          C.c_void_p(offs.data_ptr()), C.c_void_p(idx.data_ptr()),
+                                          cap, C.byref(E), _stream(stream)))
+        if E.value > cap:   # first guess too small: size exactly and rebuild
+            cap = int(E.value)
+            idx = torch.empty(max(cap, 1), device=sites.device, dtype=torch.int32)
+            _check_cech(self._L.pf_cech_build(self._h, N, C.c_void_p(sites.data_ptr()),
+                                              C.c_void_p(radii.data_ptr()),
+                                              C.c_void_p(offs.data_ptr()),
+                                              C.c_void_p(idx.data_ptr()), cap, C.byref(E),
+                                              _stream(stream)))
+        self._cap = max(self._cap, int(E.value * 1.2))
+        return offs, idx[:E.value]
+
+    def launch_count(self) -> int:
+        return int(self._L.pf_cech_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pf_cech_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def connect_loss(sites, radii, nbr_offsets, nbr_indices, grads=True, stream=None):
+    """L_connect: per-cell loss f32[N] and, if grads, (dL/dsites, dL/dradii)
+    of its sum."""
+    L = load_library()
+    N = int(sites.shape[0])
+    loss = torch.empty(N, device=sites.device, dtype=torch.float32)
+    gs = torch.zeros_like(sites) if grads else None
+    gr = torch.zeros_like(radii) if grads else None
+    _check_cech(L.pf_connect_loss(N, C.c_void_p(sites.data_ptr()), C.c_void_p(radii.data_ptr()),
+                                  C.c_void_p(nbr_offsets.data_ptr()),
+                                  C.c_void_p(nbr_indices.data_ptr()), C.c_void_p(loss.data_ptr()),
+                                  C.c_void_p(gs.data_ptr()) if grads else None,
+                                  C.c_void_p(gr.data_ptr()) if grads else None, _stream(stream)))
+    return loss, gs, gr

@@ -370,3 +370,51 @@ def test_forward_by_products_match_oracle(name):
         nn = st["normal"].double().cpu().numpy()
         assert np.linalg.norm(nn - ref_n) <= 1e-4 * np.linalg.norm(ref_n)
     r.close()
+
+
+# --------------------------------------------------------------- NEXT-3: Čech graph
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small360"])
+def test_cech_build_bit_exact_small(name):
+    import paper_2604_24994_b200 as pf
+    sc, _ = case(name)
+    b = pf.CechBuilder()
+    s = torch.from_numpy(sc.sites).cuda()
+    r = torch.from_numpy(sc.radii).cuda()
+    off, idx = b.build(s, r)
+    o_off, o_idx = oracle.cech_rows(sc.sites, sc.radii)
+    assert np.array_equal(off.cpu().numpy(), o_off)
+    assert np.array_equal(idx.cpu().numpy(), o_idx)
+    b.close()
+
+
+def test_cech_build_1m_vs_generator_and_sampled_oracle_rows():
+    import paper_2604_24994_b200 as pf
+    sc, _ = case("train8_1m")
+    b = pf.CechBuilder()
+    s = torch.from_numpy(sc.sites).cuda()
+    r = torch.from_numpy(sc.radii).cuda()
+    off, idx = b.build(s, r)
+    off, idx = off.cpu().numpy(), idx.cpu().numpy()
+    rows = np.random.default_rng(0).choice(sc.num_cells, 200, replace=False)
+    o_off, o_idx = oracle.cech_rows(sc.sites, sc.radii, rows=rows)
+    for k, i in enumerate(rows):
+        assert np.array_equal(idx[off[i]:off[i + 1]], o_idx[o_off[k]:o_off[k + 1]])
+    # the generator's lists are the exact Čech complex too (Lemma L3): identical CSR
+    assert np.array_equal(off, sc.nbr_offsets) and np.array_equal(idx, sc.nbr_indices)
+    b.close()
+
+
+def test_connect_loss_matches_oracle():
+    import paper_2604_24994_b200 as pf
+    sc, _ = case("small360")
+    s = torch.from_numpy(sc.sites).cuda()
+    r = torch.from_numpy(sc.radii).cuda()
+    off = torch.from_numpy(sc.nbr_offsets).cuda()
+    idx = torch.from_numpy(sc.nbr_indices).cuda()
+    loss, gs, gr = pf.connect_loss(s, r, off, idx)
+    ref = oracle.connect_loss(sc.sites, sc.radii, sc.nbr_offsets, sc.nbr_indices)
+    for a, b_ in ((loss, ref["loss"]), (gs, ref["sites"]), (gr, ref["radii"])):
+        a = a.double().cpu().numpy().reshape(-1)
+        b_ = b_.reshape(-1)
+        assert np.linalg.norm(a - b_) <= 1e-4 * np.linalg.norm(b_)
