@@ -165,10 +165,11 @@ def run_reference(args):
     sc = pf_synth.make_scene(wl)
     nv = args.views or default_views(wl)
     cams = workload_cameras(wl, nv, 1, 0)
-    res = cpu_baseline(sc, cams[0], args.cpu_seconds, train=wl != "mip360_1m")
+    train = wl not in ("mip360_1m", "sweep64_3m")
+    res = cpu_baseline(sc, cams[0], args.cpu_seconds, train=train)
     steps = []
     for _ in range(args.steps):
-        r = cpu_baseline(sc, cams[0], args.cpu_seconds / max(args.steps, 1), train=wl != "mip360_1m",
+        r = cpu_baseline(sc, cams[0], args.cpu_seconds / max(args.steps, 1), train=train,
                          calib=res["calib"])
         steps.append(r["value"])
     val = float(np.median(steps)) if steps else res["value"]
@@ -261,7 +262,7 @@ def main():
     cams = workload_cameras(wl, nv, ws, rank)
     t_gen = time.perf_counter() - t_gen
     H, W = cams[0].height, cams[0].width
-    train = wl != "mip360_1m"
+    train = wl not in ("mip360_1m", "sweep64_3m")   # forward render-FPS workloads
     r = pf.Renderer.from_scene(sc, dev, flags=0 if train else pf.PF_INFERENCE)
     # render-only handle on the same tensors (no backward state saved)
     r_inf = r.sibling(pf.PF_INFERENCE)
@@ -381,7 +382,7 @@ def main():
     d_avg = d_ms / max(d_n, 1)
     d_flops = f_bwd if dom == "K7_backward" else f_fwd
     achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
-    traffic, traffic_src = load_traffic("k7" if dom == "K7_backward" else "k6")
+    traffic, traffic_src = load_traffic("k7_backward" if dom == "K7_backward" else "k6_forward")
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write)",
