@@ -22,7 +22,10 @@ namespace pf {
 
 namespace {
 
-constexpr int kEndSphere = -1, kEndNear = -2, kEndDipole = -3;
+// binding-constraint codes (tracked by K6/K7, stored in the K6 -> K7 records):
+// 0 sphere, 1 near plane, 2 + k the cell's k-th neighbour plane, kEndDipole the
+// dipole face (NEXT-1)
+constexpr int kEndSphere = 0, kEndNear = 1, kEndDipole = 0x1000;
 
 struct Ray {
     float dx, dy, dz;      // unit direction
@@ -82,7 +85,7 @@ struct Seg {
     float s, tc;           // sphere half-chord, t_c (local frame origin)
     float ex, ey, ez;      // e = c - t_c d  (offset of the centre from the ray)
     float lo, hi;          // t'_in, t'_out (local frame)
-    int lo_q, hi_q;        // binding constraint: edge index, or kEndSphere / kEndNear (K7 only)
+    int lo_q, hi_q;        // binding constraint code (kEnd*, or 2 + local plane index)
     float dt;              // interval length (0 = empty)
 };
 
@@ -177,17 +180,24 @@ __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__rest
     }
     g.hi = g.s;
     g.hi_q = kEndSphere;
-    uint32_t q = eb;
-    const uint32_t qe = eb + deg;
-    for (; q + 4 <= qe; q += 4) {
-        const float4 E0 = __ldg(edges + q), E1 = __ldg(edges + q + 1), E2 = __ldg(edges + q + 2),
-                     E3 = __ldg(edges + q + 3);
-        clip_plane<kTrack>(R, E0, (int)q, g);
-        clip_plane<kTrack>(R, E1, (int)q + 1, g);
-        clip_plane<kTrack>(R, E2, (int)q + 2, g);
-        clip_plane<kTrack>(R, E3, (int)q + 3, g);
+    const float4 *ep = edges + eb;
+    uint32_t k = 0;
+    for (; k + 4 <= deg; k += 4) {
+        const float4 E0 = __ldg(ep + k), E1 = __ldg(ep + k + 1), E2 = __ldg(ep + k + 2),
+                     E3 = __ldg(ep + k + 3);
+        clip_plane<kTrack>(R, E0, (int)k + 2, g);
+        clip_plane<kTrack>(R, E1, (int)k + 3, g);
+        clip_plane<kTrack>(R, E2, (int)k + 4, g);
+        clip_plane<kTrack>(R, E3, (int)k + 5, g);
     }
-    for (; q < qe; ++q) clip_plane<kTrack>(R, __ldg(edges + q), (int)q, g);
+    if (k < deg) {   // 1..3 left (deg is warp-uniform: these branches do not diverge)
+        const float4 E0 = __ldg(ep + k);
+        const float4 E1 = k + 1 < deg ? __ldg(ep + k + 1) : E0;
+        const float4 E2 = k + 2 < deg ? __ldg(ep + k + 2) : E0;
+        clip_plane<kTrack>(R, E0, (int)k + 2, g);
+        if (k + 1 < deg) clip_plane<kTrack>(R, E1, (int)k + 3, g);
+        if (k + 2 < deg) clip_plane<kTrack>(R, E2, (int)k + 4, g);
+    }
     if (kDipole)  // the occupied half (x - p_i).n_i <= 0: a plane through p_i with k = 0
         clip_plane<kTrack>(R, S.nrm[j], kEndDipole, g);
     const float dt = __fsub_rn(g.hi, g.lo);
@@ -360,13 +370,10 @@ struct WarpRec {
     uint32_t code[32][16];      // 32 lanes x u16, as 16 words
 };
 
-__device__ __forceinline__ uint32_t end_code(int q, uint32_t eb, bool lo)
+__device__ __forceinline__ uint32_t end_code(int q)
 {
-    if (q == kEndSphere) return 0u;
-    if (lo && q == kEndNear) return 1u;
-    if (q == kEndDipole) return 254u;
-    const uint32_t k = (uint32_t)q - eb;
-    return k < 252u ? k + 2u : 255u;
+    // tracked codes are already record codes; only the dipole and planes >= 252 remap
+    return q == kEndDipole ? 254u : min((uint32_t)q, 255u);
 }
 
 }  // namespace
@@ -426,9 +433,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             if (kRecord) {
                 const unsigned sm = __ballot_sync(0xffffffffu, seg);
                 if (sm) {
-                    const uint32_t eb = S.eb[j];
-                    const uint32_t c = seg ? (end_code(g.lo_q, eb, true) |
-                                              (end_code(g.hi_q, eb, false) << 8)) : 0u;
+                    const uint32_t c = seg ? (end_code(g.lo_q) | (end_code(g.hi_q) << 8)) : 0u;
                     reinterpret_cast<uint16_t *>(Rb.code[nrec])[lane] = (uint16_t)c;
                     if (lane == 0) {
                         Rb.mask[nrec] = sm;
@@ -595,14 +600,15 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
         o.r = fmaf(f, rad, o.r);
         return;
     }
-    const float4 E = __ldg(edges + q);
+    const uint32_t qe = S.eb[jslot] + (uint32_t)q - 2u;   // global edge of the binding plane
+    const float4 E = __ldg(edges + qe);
     const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float f = __fdividef(wgt, a);
     o.px = fmaf(f, xpx, o.px);
     o.py = fmaf(f, xpy, o.py);
     o.pz = fmaf(f, xpz, o.pz);
     o.w = fmaf(0.5f, f, o.w);
-    const int j = __ldg(nbr + q);
+    const int j = __ldg(nbr + qe);
     atomicAdd(reinterpret_cast<float4 *>(acc + 12 * (size_t)j),
               make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f));
 }
@@ -680,8 +686,8 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
         q = kEndDipole;
         E = S.nrm[j];
     } else {
-        q = (int)(eb + code - 2u);
-        E = __ldg(edges + q);
+        q = (int)code;                      // 2 + local plane index
+        E = __ldg(edges + eb + code - 2u);
     }
     const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
