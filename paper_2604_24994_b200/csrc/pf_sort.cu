@@ -7,7 +7,7 @@
 //            (3) stable scatter: warp-level multisplit ranking with
 //                __match_any_sync, per-warp digit counters in shared memory,
 //                block prefix over warps, global base from the scan.
-// Stability: warp w of block b owns keys [b*4096 + w*512, +512) in 16 rounds of
+// Stability: warp w of block b owns keys [b*4096 + w*32*I, +32*I) in I rounds of
 // 32 consecutive keys; ranks follow (round, lane) = input order.
 #include <cuda_runtime.h>
 
@@ -18,16 +18,20 @@ namespace pf {
 cudaError_t exclusive_scan_counts(pf_scene *s, const int *cnt, int64_t n, uint32_t *offs,
                                   long long *d_total, cudaStream_t st);
 
-constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems;
+#ifndef PF_SORT_THREADS
+#define PF_SORT_THREADS 512
+#endif
+constexpr int kSortThreads = PF_SORT_THREADS, kSortItems = 4096 / PF_SORT_THREADS,
+              kSortTile = kSortThreads * kSortItems, kSortWarps = kSortThreads / 32;
 constexpr int kRadixBits = 8, kRadix = 1 << kRadixBits;
 
 __global__ void __launch_bounds__(kSortThreads)
 k4_histogram(const unsigned long long *__restrict__ keys, int64_t n, int shift, int nb,
              int *__restrict__ hist)
 {
-    __shared__ int h[8][kRadix];
+    __shared__ int h[kSortWarps][kRadix];
     const int warp = threadIdx.x >> 5;
-    for (int q = threadIdx.x; q < 8 * kRadix; q += kSortThreads) (&h[0][0])[q] = 0;
+    for (int q = threadIdx.x; q < kSortWarps * kRadix; q += kSortThreads) (&h[0][0])[q] = 0;
     __syncthreads();
     int64_t base = (int64_t)blockIdx.x * kSortTile;
 #pragma unroll 4
@@ -42,7 +46,7 @@ k4_histogram(const unsigned long long *__restrict__ keys, int64_t n, int shift, 
     for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
         int t = 0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) t += h[w][d];
+        for (int w = 0; w < kSortWarps; ++w) t += h[w][d];
         hist[(int64_t)d * nb + blockIdx.x] = t;
     }
 }
@@ -52,9 +56,9 @@ k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restric
            unsigned long long *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
            int shift, int nb, const uint32_t *__restrict__ digit_offs)
 {
-    __shared__ uint32_t wh[8][kRadix];
+    __shared__ uint32_t wh[kSortWarps][kRadix];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int q = threadIdx.x; q < 8 * kRadix; q += kSortThreads) (&wh[0][0])[q] = 0;
+    for (int q = threadIdx.x; q < kSortWarps * kRadix; q += kSortThreads) (&wh[0][0])[q] = 0;
     __syncthreads();
     const unsigned lt_mask = (1u << lane) - 1u;
     int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (32 * kSortItems);
@@ -85,7 +89,7 @@ k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restric
     for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
         uint32_t run = digit_offs[(int64_t)d * nb + blockIdx.x];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kSortWarps; ++w) {
             uint32_t c = wh[w][d];
             wh[w][d] = run;
             run += c;
