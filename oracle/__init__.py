@@ -25,7 +25,7 @@ T_STOP = 1e-4
 class OCamera(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32),
                 ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
-                ("c2w", C.c_float * 12), ("near_plane", C.c_float)]
+                ("c2w", C.c_float * 12), ("near_plane", C.c_float), ("model", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -51,7 +51,7 @@ def lib():
         P = C.c_void_p
         i64 = C.c_int64
         L.oracle_bin_cells.argtypes = [i64, P, P, P, P, P, P, P]
-        L.oracle_emit_sort.argtypes = [i64, P, P, P, C.c_int32, P, P]
+        L.oracle_emit_sort.argtypes = [i64, P, P, P, C.c_int32, P, P, P, P, P]
         L.oracle_emit_sort.restype = i64
         L.oracle_tile_ranges.argtypes = [i64, P, C.c_int32, P]
         L.oracle_render.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P, P,
@@ -90,6 +90,7 @@ def make_camera(cam) -> OCamera:
     for k, v in enumerate(np.asarray(cam.c2w, np.float32).reshape(12)):
         oc.c2w[k] = float(v)
     oc.near_plane = cam.near
+    oc.model = int(getattr(cam, "model", 0))
     return oc
 
 
@@ -136,10 +137,14 @@ def binning(sc, cam):
     tiles_x = (cam.width + 15) // 16
     tiles_y = (cam.height + 15) // 16
     L = lib()
-    P = L.oracle_emit_sort(sc.num_cells, _p(rect), _p(count), _p(kb), tiles_x, None, None)
+    A = _SceneArrays(sc)
+    oc = make_camera(cam)
+    P = L.oracle_emit_sort(sc.num_cells, _p(rect), _p(count), _p(kb), tiles_x, None, None,
+                           C.byref(oc), _p(A.sites), _p(A.radii))
     keys = np.zeros(max(P, 1), np.uint64)
     vals = np.zeros(max(P, 1), np.uint32)
-    L.oracle_emit_sort(sc.num_cells, _p(rect), _p(count), _p(kb), tiles_x, _p(keys), _p(vals))
+    L.oracle_emit_sort(sc.num_cells, _p(rect), _p(count), _p(kb), tiles_x, _p(keys), _p(vals),
+                       C.byref(oc), _p(A.sites), _p(A.radii))
     ranges = np.zeros((tiles_x * tiles_y, 2), np.uint32)
     L.oracle_tile_ranges(P, _p(keys), tiles_x * tiles_y, _p(ranges))
     return dict(rect=rect, count=count, keybits=kb, keys=keys[:P], vals=vals[:P],

@@ -79,6 +79,7 @@ typedef struct {
     float fx, fy, cx, cy;
     float c2w[12]; /* row-major [R | Q]: R[m][k] = c2w[4m+k], Q[m] = c2w[4m+3] */
     float near_plane;
+    int32_t model; /* 0 pinhole, 1 equidistant fisheye (NEXT-4) */
 } oc_camera;
 
 typedef struct {
@@ -135,7 +136,103 @@ static float clampf_(float v, float lo, float hi)
     return fminf(fmaxf(v, lo), hi);
 }
 
-/* rect[4*i] = (tx0, ty0, tx1, ty1) half-open tile rectangle; count = area. */
+/* ---- equidistant fisheye (NEXT-4): pixel (u, v) -> a = (u-cx)/fx, b = (v-cy)/fy,
+ * theta = |(a, b)|, camera ray (sin(theta) a/theta, sin(theta) b/theta, cos(theta))
+ * (S:285); pixels with theta > pi are outside the image circle.  The map (a,b) ->
+ * ray is 1-Lipschitz in angle, so every pixel ray of tile t lies within the angle
+ * th = |(9/fx, 9/fy)| (8 px to the tile border + 1 px guard) of the ray through
+ * the tile centre (16 tx + 8, 16 ty + 8); a sphere (c, r) in camera coordinates
+ * can meet a ray of the tile only if  c.a_t >= cos(th) sqrt(|c|^2 - r^2) - sin(th) r
+ * (angle(c, a_t) <= th + asin(r/|c|)), or if |c| <= r.  Binning = the tiles that
+ * pass this test (evaluated in double; the candidate rectangle is any superset). */
+static void fisheye_dir(const oc_camera *cam, double u, double v, double dc[3], int *valid)
+{
+    double a = (u - (double)cam->cx) / (double)cam->fx, b = (v - (double)cam->cy) / (double)cam->fy;
+    double th = sqrt(a * a + b * b);
+    *valid = th <= 3.14159265358979323846;
+    if (th > 0.0) {
+        double st = sin(th) / th;
+        dc[0] = st * a;
+        dc[1] = st * b;
+        dc[2] = cos(th);
+    } else {
+        dc[0] = dc[1] = 0.0;
+        dc[2] = 1.0;
+    }
+}
+
+static int fisheye_tile_pass(const oc_camera *cam, const double c[3], double r, int tx, int ty)
+{
+    double cc = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+    if (cc <= r * r) return 1;
+    double at[3];
+    int valid;
+    fisheye_dir(cam, 16.0 * tx + 8.0, 16.0 * ty + 8.0, at, &valid);
+    double th = sqrt((9.0 / cam->fx) * (9.0 / cam->fx) + (9.0 / cam->fy) * (9.0 / cam->fy));
+    double lhs = c[0] * at[0] + c[1] * at[1] + c[2] * at[2];
+    double rhs = cos(th) * sqrt(cc - r * r) - sin(th) * r;
+    return lhs >= rhs;
+}
+
+/* candidate tile rectangle of a sphere for the fisheye: the bounding box, in (a,b),
+ * of the annular sector of directions within th + asin(r/|c|) of c (plus margin) */
+static void fisheye_rect(const oc_camera *cam, const double c[3], double r, int tiles_x,
+                         int tiles_y, int rc[4])
+{
+    double cc = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    double th = sqrt((9.0 / cam->fx) * (9.0 / cam->fx) + (9.0 / cam->fy) * (9.0 / cam->fy));
+    double amin, amax, bmin, bmax;
+    const double PI = 3.14159265358979323846;
+    if (cc <= r) {
+        amin = bmin = -PI;
+        amax = bmax = PI;
+    } else {
+        double beta = asin(r / cc) + th + 1e-6;
+        double thc = acos(fmax(-1.0, fmin(1.0, c[2] / cc)));
+        double phc = atan2(c[1], c[0]);
+        double rmax = fmin(thc + beta, PI);
+        if (thc - beta <= 0.0 || thc + beta >= PI) {
+            amin = bmin = -rmax;
+            amax = bmax = rmax;
+        } else {
+            double rmin = thc - beta;
+            double dph = asin(fmin(1.0, sin(beta) / sin(thc)));
+            double p0 = phc - dph, p1 = phc + dph;
+            amin = bmin = 1e30;
+            amax = bmax = -1e30;
+            double cand[4] = {p0, p1, 0, 0};
+            for (int k = 0; k < 2; ++k)
+                for (int q = 0; q < 2; ++q) {
+                    double rr = q ? rmax : rmin, ph = cand[k];
+                    amin = fmin(amin, rr * cos(ph)); amax = fmax(amax, rr * cos(ph));
+                    bmin = fmin(bmin, rr * sin(ph)); bmax = fmax(bmax, rr * sin(ph));
+                }
+            for (int k = -4; k <= 4; ++k) {   /* axis directions inside the sector */
+                double ph = k * (PI / 2);
+                if (ph >= p0 && ph <= p1) {
+                    amin = fmin(amin, rmax * cos(ph)); amax = fmax(amax, rmax * cos(ph));
+                    bmin = fmin(bmin, rmax * sin(ph)); bmax = fmax(bmax, rmax * sin(ph));
+                }
+            }
+        }
+    }
+    double u0 = cam->cx + cam->fx * amin, u1 = cam->cx + cam->fx * amax;
+    double v0 = cam->cy + cam->fy * bmin, v1 = cam->cy + cam->fy * bmax;
+    rc[0] = (int)fmax(0.0, fmin((double)tiles_x, floor((u0 - 1.0) / 16.0)));
+    rc[2] = (int)fmax(0.0, fmin((double)tiles_x, floor((u1 + 1.0) / 16.0) + 1.0));
+    rc[1] = (int)fmax(0.0, fmin((double)tiles_y, floor((v0 - 1.0) / 16.0)));
+    rc[3] = (int)fmax(0.0, fmin((double)tiles_y, floor((v1 + 1.0) / 16.0) + 1.0));
+}
+
+static void camera_coords(const oc_camera *cam, const float *p, double c[3])
+{
+    const float *M = cam->c2w;
+    double v[3] = {(double)p[0] - M[3], (double)p[1] - M[7], (double)p[2] - M[11]};
+    for (int k = 0; k < 3; ++k) c[k] = M[k] * v[0] + M[4 + k] * v[1] + M[8 + k] * v[2];
+}
+
+/* rect[4*i] = (tx0, ty0, tx1, ty1) half-open tile rectangle; count = area (pinhole)
+ * or the number of tiles of the rectangle passing the fisheye test. */
 int oracle_bin_cells(int64_t N, const float *sites, const float *weights, const float *radii,
                      const oc_camera *cam, int32_t *rect, int32_t *count, uint32_t *keybits)
 {
@@ -156,6 +253,22 @@ int oracle_bin_cells(int64_t N, const float *sites, const float *weights, const 
         keybits[i] = key_bits(K);
         rect[4 * i + 0] = rect[4 * i + 1] = rect[4 * i + 2] = rect[4 * i + 3] = 0;
         count[i] = 0;
+        if (cam->model == 1) {   /* fisheye: cull only inside the near ball */
+            double c[3];
+            camera_coords(cam, sites + 3 * i, c);
+            double dist = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+            if (!(r > 0.0f) || dist + r <= (double)cam->near_plane) continue;
+            int rc[4];
+            fisheye_rect(cam, c, r, tiles_x, tiles_y, rc);
+            int n = 0;
+            for (int ty = rc[1]; ty < rc[3]; ++ty)
+                for (int tx = rc[0]; tx < rc[2]; ++tx) n += fisheye_tile_pass(cam, c, r, tx, ty);
+            if (n > 0) {
+                for (int k = 0; k < 4; ++k) rect[4 * i + k] = rc[k];
+                count[i] = n;
+            }
+            continue;
+        }
         if (!(czz + r > cam->near_plane) || !(r > 0.0f))
             continue; /* entirely behind the near plane (or degenerate) */
         int in_front = (czz - r > cam->near_plane);
@@ -196,7 +309,8 @@ static int cmp_pair(const void *a, const void *b)
 /* Emits (tile<<32 | keybits, cell) in cell-major order and sorts stably.
  * Returns P (number of pairs); keys/vals may be NULL to query P. */
 int64_t oracle_emit_sort(int64_t N, const int32_t *rect, const int32_t *count,
-                         const uint32_t *keybits, int32_t tiles_x, uint64_t *keys, uint32_t *vals)
+                         const uint32_t *keybits, int32_t tiles_x, uint64_t *keys, uint32_t *vals,
+                         const oc_camera *cam, const float *sites, const float *radii)
 {
     int64_t P = 0;
     for (int64_t i = 0; i < N; ++i) P += count[i];
@@ -205,8 +319,12 @@ int64_t oracle_emit_sort(int64_t N, const int32_t *rect, const int32_t *count,
     int64_t k = 0;
     for (int64_t i = 0; i < N; ++i) {
         if (count[i] == 0) continue;
+        double c[3] = {0, 0, 0};
+        const int fish = cam && cam->model == 1;
+        if (fish) camera_coords(cam, sites + 3 * i, c);
         for (int ty = rect[4 * i + 1]; ty < rect[4 * i + 3]; ++ty)
             for (int tx = rect[4 * i + 0]; tx < rect[4 * i + 2]; ++tx) {
+                if (fish && !fisheye_tile_pass(cam, c, radii[i], tx, ty)) continue;
                 uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + (uint64_t)tx;
                 pairs[k].key = (tile << 32) | (uint64_t)keybits[i];
                 pairs[k].val = (uint32_t)i;
@@ -241,12 +359,14 @@ int oracle_tile_ranges(int64_t P, const uint64_t *keys, int32_t num_tiles, uint3
 /* ray through the centre of pixel (px, py) = (x+0.5, y+0.5) (C11):
  * d_cam = ((px-cx)/fx, (py-cy)/fy, 1), d = normalize(R d_cam),
  * t_near = near * |d_cam| (C10: camera-space z >= near). */
-static void pixel_ray(const oc_camera *cam, double px, double py, double Q[3], double d[3],
-                      double *t_near)
+static int pixel_ray(const oc_camera *cam, double px, double py, double Q[3], double d[3],
+                     double *t_near)
 {
     const float *M = cam->c2w;
     double dc[3] = {(px - (double)cam->cx) / (double)cam->fx,
                     (py - (double)cam->cy) / (double)cam->fy, 1.0};
+    int valid = 1;
+    if (cam->model == 1) fisheye_dir(cam, px, py, dc, &valid);
     double ndc = sqrt(dc[0] * dc[0] + dc[1] * dc[1] + dc[2] * dc[2]);
     double n2 = 0.0;
     for (int m = 0; m < 3; ++m) {
@@ -257,7 +377,9 @@ static void pixel_ray(const oc_camera *cam, double px, double py, double Q[3], d
     }
     double nd = sqrt(n2);
     for (int m = 0; m < 3; ++m) d[m] /= nd;
-    *t_near = (double)cam->near_plane * ndc;
+    /* pinhole: camera-space z >= near (C10); fisheye: distance >= near (reading R5) */
+    *t_near = (double)cam->near_plane * (cam->model == 1 ? 1.0 : ndc);
+    return valid;
 }
 
 /* which constraint bounds an interval end */
@@ -416,10 +538,11 @@ static int build_bins(const oc_scene *S, const oc_camera *cam, oc_bins *B)
     int32_t *count = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
     uint32_t *kb = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)N);
     oracle_bin_cells(N, S->sites, S->weights, S->radii, cam, rect, count, kb);
-    int64_t P = oracle_emit_sort(N, rect, count, kb, B->tiles_x, NULL, NULL);
+    int64_t P = oracle_emit_sort(N, rect, count, kb, B->tiles_x, NULL, NULL, cam, S->sites,
+                                 S->radii);
     uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(P > 0 ? P : 1));
     B->vals = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(P > 0 ? P : 1));
-    oracle_emit_sort(N, rect, count, kb, B->tiles_x, keys, B->vals);
+    oracle_emit_sort(N, rect, count, kb, B->tiles_x, keys, B->vals, cam, S->sites, S->radii);
     B->ranges = (uint32_t *)malloc(sizeof(uint32_t) * 2 * (size_t)T);
     oracle_tile_ranges(P, keys, T, B->ranges);
     free(rect);
@@ -580,14 +703,18 @@ int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
             int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
             int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
             double Q[3], d[3], tn;
-            pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+            const int pv = pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
             int64_t v = 0;
-            int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, &v);
+            int64_t n = pv ? collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, &v) : 0;
             total_viol += v;
             int64_t K = composite(&S, scr.segs, n, out + 4 * q);
-            if (counters)
-                pixel_counters(&S, &B, x, y, Q, d, tn, scr.segs, K, out[4 * q + 3] < T_STOP,
-                               counters + 4 * q);
+            if (counters) {
+                if (pv)
+                    pixel_counters(&S, &B, x, y, Q, d, tn, scr.segs, K, out[4 * q + 3] < T_STOP,
+                                   counters + 4 * q);
+                else
+                    counters[4 * q] = counters[4 * q + 1] = counters[4 * q + 2] = counters[4 * q + 3] = 0;
+            }
             if (nseg_out) nseg_out[q] = K;
             if (sig) {
                 uint64_t h = 1469598103934665603ull;
@@ -640,8 +767,8 @@ int oracle_cell_stats(int mode, int64_t N, const float *sites, const float *weig
             int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
             int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
             double Q[3], d[3], tn, out[4];
-            pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
-            int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL);
+            const int pv = pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+            int64_t n = pv ? collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL) : 0;
             int64_t K = composite(&S, scr.segs, n, out);
             double T = 1.0;
             for (int64_t k = 0; k < K; ++k) {
@@ -759,8 +886,8 @@ int oracle_backward(int mode, int64_t N, const float *sites, const float *weight
             int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
             int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
             double Q[3], d[3], tn;
-            pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
-            int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL);
+            const int pv = pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+            int64_t n = pv ? collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL) : 0;
             double out[4];
             int64_t K = composite(&S, scr.segs, n, out);
             if (K + 1 > capk) {
@@ -862,8 +989,8 @@ int64_t oracle_pixel_segments(int mode, int64_t N, const float *sites, const flo
     if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
     oc_scratch scr = {NULL, 0};
     double Q[3], d[3], tn, out[4];
-    pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
-    int64_t n = collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL);
+    const int pv = pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn);
+    int64_t n = pv ? collect_segments(&S, mode, &B, x, y, Q, d, tn, &scr, NULL, NULL) : 0;
     int64_t K = composite(&S, scr.segs, n, out);
     int64_t m = K < cap ? K : cap;
     for (int64_t k = 0; k < m; ++k) {

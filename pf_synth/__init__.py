@@ -42,6 +42,7 @@ class Camera:
     cy: float
     c2w: np.ndarray          # f32[12] row-major [R | Q], world-from-camera
     near: float
+    model: int = 0           # 0 pinhole, 1 equidistant fisheye (NEXT-4)
 
     def as_tuple(self):
         return (self.width, self.height, self.fx, self.fy, self.cx, self.cy,
@@ -382,6 +383,18 @@ def make_cameras(preset: str, variant: str | None = None, width: int | None = No
         return _cams_mip360(n or 64, width or 1920, height or 1080, jitter=0.3, seed=3,
                             az_step=math.radians(5.625))
     raise ValueError(f"unknown preset {preset}")
+
+
+def fisheye(cam: Camera, fov_deg: float = 200.0) -> Camera:
+    """Equidistant fisheye (NEXT-4) with the same pose and image size: the
+    image circle of diameter min(W, H) spans fov_deg."""
+    import copy
+    c = copy.deepcopy(cam)
+    f = 0.5 * min(cam.width, cam.height) / math.radians(0.5 * fov_deg)
+    c.fx = c.fy = float(f)
+    c.cx, c.cy = cam.width / 2.0, cam.height / 2.0
+    c.model = 1
+    return c
 
 
 def make_grad_out(num_views: int, H: int, W: int, seed: int = 11) -> np.ndarray:
