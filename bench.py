@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--views", type=int, default=None, help="views per GPU (default: preset)")
     ap.add_argument("--dipoles", action="store_true",
                     help="oriented-point dipole cells (NEXT-1) on the workload's foam")
+    ap.add_argument("--fisheye", action="store_true",
+                    help="equidistant fisheye cameras (NEXT-4), 200 deg image circle")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -260,6 +262,8 @@ def main():
     t_gen = time.perf_counter()
     sc = pf_synth.make_scene(wl, dipoles=args.dipoles)
     cams = workload_cameras(wl, nv, ws, rank)
+    if args.fisheye:
+        cams = [pf_synth.fisheye(c, 200.0) for c in cams]
     t_gen = time.perf_counter() - t_gen
     H, W = cams[0].height, cams[0].width
     train = wl not in ("mip360_1m", "sweep64_3m")   # forward render-FPS workloads
@@ -439,7 +443,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (pf_synth seeded generator, random-init foam)",
-            "config": {"workload": wl + ("+dipoles" if args.dipoles else ""), "cells": N,
+            "config": {"workload": wl + ("+dipoles" if args.dipoles else "") +
+                                   ("+fisheye" if args.fisheye else ""), "cells": N,
                        "edges": sc.num_edges, "views_per_gpu": nv,
                        "global_batch_views": nv * ws, "width": W, "height": H,
                        "pass": "fwd+bwd" if train else "fwd",

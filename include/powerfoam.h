@@ -94,15 +94,21 @@ typedef struct {
                                    zero density.  Non-zero, finite (not required to be unit). */
 } pf_scene_desc;
 
-/* Pinhole camera, OpenCV axes (x right, y down, z forward).
- * Pixel ray: d_cam = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1), d = normalize(R d_cam),
- * origin Q; the ray is clipped to camera-space z >= near_plane, i.e.
- * t >= near_plane * |d_cam|. */
+/* Camera, OpenCV axes (x right, y down, z forward).
+ * model PF_PINHOLE: d_cam = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1), d = normalize(R d_cam),
+ *   origin Q; the ray is clipped to camera-space z >= near_plane, i.e.
+ *   t >= near_plane * |d_cam|.
+ * model PF_FISHEYE (equidistant, NEXT-4): (a, b) = ((x+0.5-cx)/fx,
+ *   (y+0.5-cy)/fy), theta = |(a,b)|, d_cam = (sin(theta) a/theta, sin(theta) b/theta,
+ *   cos(theta)); pixels with theta > pi lie outside the image circle (output
+ *   (background, T = 1)); rays are clipped to t >= near_plane (distance). */
+enum { PF_PINHOLE = 0, PF_FISHEYE = 1 };
 typedef struct {
     int32_t width, height; /* pixels, 1..32768 */
     float fx, fy, cx, cy;  /* pixel units, fx, fy > 0 */
     float c2w[12];         /* row-major 3x4 [R | Q], world-from-camera */
     float near_plane;      /* > 0 */
+    int32_t model;         /* PF_PINHOLE or PF_FISHEYE */
 } pf_camera;
 
 /* Creates a handle for the scene described by *desc (pointers are stored, not

@@ -18,6 +18,7 @@ from . import _build
 __all__ = ["PFError", "Renderer", "render", "load_library", "PF_VALIDATE", "PF_STATIC_SCENE",
            "PF_INFERENCE", "STAGES"]
 
+PF_PINHOLE, PF_FISHEYE = 0, 1
 PF_VALIDATE = 1
 PF_STATIC_SCENE = 2
 PF_INFERENCE = 4
@@ -43,7 +44,7 @@ class PFError(RuntimeError):
 class _Camera(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32),
                 ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
-                ("c2w", C.c_float * 12), ("near_plane", C.c_float)]
+                ("c2w", C.c_float * 12), ("near_plane", C.c_float), ("model", C.c_int32)]
 
 
 class _SceneDesc(C.Structure):
@@ -129,6 +130,7 @@ def _cams(cams) -> tuple:
         for q in range(12):
             arr[k].c2w[q] = m[q]
         arr[k].near_plane = float(c.near if hasattr(c, "near") else c.near_plane)
+        arr[k].model = int(getattr(c, "model", 0))
     return arr, len(cams)
 
 

@@ -61,6 +61,8 @@ int check_camera(const pf_camera &c)
         if (!finitef(c.c2w[k])) return fail(PF_ERR_INVALID_ARGUMENT, "camera c2w not finite");
     if (!(c.near_plane > 0.0f) || !finitef(c.near_plane))
         return fail(PF_ERR_INVALID_ARGUMENT, "camera near_plane must be finite and > 0");
+    if (c.model != PF_PINHOLE && c.model != PF_FISHEYE)
+        return fail(PF_ERR_INVALID_ARGUMENT, "camera model must be PF_PINHOLE or PF_FISHEYE");
     return PF_OK;
 }
 
@@ -77,6 +79,7 @@ pf::CamParams cam_params(const pf_camera &c)
     p.cy = c.cy;
     for (int k = 0; k < 12; ++k) p.M[k] = c.c2w[k];
     p.near_plane = c.near_plane;
+    p.model = c.model;
     return p;
 }
 

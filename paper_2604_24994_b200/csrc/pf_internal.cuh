@@ -22,6 +22,7 @@ struct CamParams {
     float fx, fy, cx, cy;
     float M[12];     // c2w row-major
     float near_plane;
+    int model;       // PF_PINHOLE / PF_FISHEYE
 };
 
 // Device-side records built by K0 from the caller's arrays.

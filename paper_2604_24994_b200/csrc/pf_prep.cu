@@ -162,6 +162,104 @@ __device__ __forceinline__ int tile_hi(float px, int ntiles)
     return (int)fminf(fmaxf(t, 0.0f), (float)ntiles);
 }
 
+// ---- equidistant fisheye binning (NEXT-4) --------------------------------
+// The map (a, b) -> camera ray is 1-Lipschitz in angle, so every pixel ray of a
+// tile is within th = |(9/fx, 9/fy)| of the ray through the tile centre (8 px to
+// the border + 1 px guard); the sphere (c, r) can meet a ray of the tile only if
+// c.a_t >= cos(th) sqrt(|c|^2 - r^2) - sin(th) r, or |c| <= r.  Evaluated in fp64;
+// the candidate rectangle (bounding box of the angular cap's annular sector) is
+// any superset, the count is the number of passing tiles.
+__device__ __forceinline__ void fisheye_dir(const CamParams &cam, double u, double v, double dc[3])
+{
+    const double a = (u - (double)cam.cx) / (double)cam.fx, b = (v - (double)cam.cy) / (double)cam.fy;
+    const double th = sqrt(a * a + b * b);
+    if (th > 0.0) {
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        dc[0] = sn / th * a;
+        dc[1] = sn / th * b;
+        dc[2] = cs;
+    } else {
+        dc[0] = dc[1] = 0.0;
+        dc[2] = 1.0;
+    }
+}
+
+__device__ __forceinline__ double fisheye_half_angle(const CamParams &cam)
+{
+    const double ax = 9.0 / (double)cam.fx, ay = 9.0 / (double)cam.fy;
+    return sqrt(ax * ax + ay * ay);
+}
+
+__device__ __forceinline__ bool fisheye_tile_pass(const CamParams &cam, const double c[3], double r,
+                                                  double cth, double sth, int tx, int ty)
+{
+    const double cc = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+    if (cc <= r * r) return true;
+    double at[3];
+    fisheye_dir(cam, 16.0 * tx + 8.0, 16.0 * ty + 8.0, at);
+    const double lhs = c[0] * at[0] + c[1] * at[1] + c[2] * at[2];
+    return lhs >= cth * sqrt(cc - r * r) - sth * r;
+}
+
+__device__ void fisheye_rect(const CamParams &cam, const double c[3], double r, double th, int4 &rc)
+{
+    const double PI = 3.14159265358979323846;
+    const double cc = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    double amin, amax, bmin, bmax;
+    if (cc <= r) {
+        amin = bmin = -PI;
+        amax = bmax = PI;
+    } else {
+        const double beta = asin(r / cc) + th + 1e-6;
+        const double thc = acos(fmax(-1.0, fmin(1.0, c[2] / cc)));
+        const double phc = atan2(c[1], c[0]);
+        const double rmax = fmin(thc + beta, PI);
+        if (thc - beta <= 0.0 || thc + beta >= PI) {
+            amin = bmin = -rmax;
+            amax = bmax = rmax;
+        } else {
+            const double rmin = thc - beta;
+            const double dph = asin(fmin(1.0, sin(beta) / sin(thc)));
+            const double p0 = phc - dph, p1 = phc + dph;
+            amin = bmin = 1e30;
+            amax = bmax = -1e30;
+            for (int k = 0; k < 2; ++k)
+                for (int q = 0; q < 2; ++q) {
+                    const double rr = q ? rmax : rmin, ph = k ? p1 : p0;
+                    double sn, cs;
+                    sincos(ph, &sn, &cs);
+                    amin = fmin(amin, rr * cs); amax = fmax(amax, rr * cs);
+                    bmin = fmin(bmin, rr * sn); bmax = fmax(bmax, rr * sn);
+                }
+            for (int k = -4; k <= 4; ++k) {   // axis directions inside the sector
+                const double ph = k * (PI / 2);
+                if (ph >= p0 && ph <= p1) {
+                    double sn, cs;
+                    sincos(ph, &sn, &cs);
+                    amin = fmin(amin, rmax * cs); amax = fmax(amax, rmax * cs);
+                    bmin = fmin(bmin, rmax * sn); bmax = fmax(bmax, rmax * sn);
+                }
+            }
+        }
+    }
+    const double u0 = cam.cx + cam.fx * amin, u1 = cam.cx + cam.fx * amax;
+    const double v0 = cam.cy + cam.fy * bmin, v1 = cam.cy + cam.fy * bmax;
+    rc.x = (int)fmax(0.0, fmin((double)cam.tiles_x, floor((u0 - 1.0) / 16.0)));
+    rc.z = (int)fmax(0.0, fmin((double)cam.tiles_x, floor((u1 + 1.0) / 16.0) + 1.0));
+    rc.y = (int)fmax(0.0, fmin((double)cam.tiles_y, floor((v0 - 1.0) / 16.0)));
+    rc.w = (int)fmax(0.0, fmin((double)cam.tiles_y, floor((v1 + 1.0) / 16.0) + 1.0));
+}
+
+__device__ __forceinline__ void camera_coords(const CamParams &cam, const float *p, double c[3])
+{
+    const float *M = cam.M;
+    const double v0 = (double)p[0] - (double)M[3], v1 = (double)p[1] - (double)M[7],
+                 v2 = (double)p[2] - (double)M[11];
+    for (int k = 0; k < 3; ++k)
+        c[k] = (double)M[k] * v0 + (double)M[4 + k] * v1 + (double)M[8 + k] * v2;
+}
+
 __global__ void __launch_bounds__(256)
 k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights,
               const float *__restrict__ radii, int64_t N, CamParams cam, int4 *__restrict__ rect,
@@ -185,6 +283,23 @@ k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights
     keybits[i] = order_bits(K);
     int4 rc = make_int4(0, 0, 0, 0);
     int cnt = 0;
+    if (cam.model == PF_FISHEYE) {
+        double c[3];
+        camera_coords(cam, sites + 3 * i, c);
+        const double dist = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+        if ((r > 0.0f) && !(dist + r <= (double)cam.near_plane)) {
+            const double th = fisheye_half_angle(cam), cth = cos(th), sth = sin(th);
+            int4 cand;
+            fisheye_rect(cam, c, r, th, cand);
+            for (int ty = cand.y; ty < cand.w; ++ty)
+                for (int tx = cand.x; tx < cand.z; ++tx)
+                    cnt += fisheye_tile_pass(cam, c, r, cth, sth, tx, ty) ? 1 : 0;
+            if (cnt) rc = cand;
+        }
+        rect[i] = rc;
+        count[i] = cnt;
+        return;
+    }
     if ((__fadd_rn(cz, r) > cam.near_plane) && (r > 0.0f)) {
         bool in_front = __fsub_rn(cz, r) > cam.near_plane;
         float xlo, xhi, ylo, yhi;
@@ -402,9 +517,48 @@ k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__rest
     }
 }
 
+// fisheye emission: one thread per cell re-tests the tiles of its candidate
+// rectangle (the count from K1 is the number that pass)
+__global__ void __launch_bounds__(256)
+k3_emit_fisheye(int64_t N, CamParams cam, const float *__restrict__ sites,
+                const float *__restrict__ radii, const int4 *__restrict__ rect,
+                const int *__restrict__ count, const uint32_t *__restrict__ keybits,
+                const uint32_t *__restrict__ offs, unsigned long long *__restrict__ keys,
+                uint32_t *__restrict__ vals, unsigned long long view_key)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N || count[i] == 0) return;
+    const int4 rc = rect[i];
+    double c[3];
+    camera_coords(cam, sites + 3 * i, c);
+    const double th = fisheye_half_angle(cam), cth = cos(th), sth = sin(th);
+    const double r = radii[i];
+    const uint32_t k = keybits[i];
+    uint32_t o = offs[i];
+    for (int ty = rc.y; ty < rc.w; ++ty)
+        for (int tx = rc.x; tx < rc.z; ++tx)
+            if (fisheye_tile_pass(cam, c, r, cth, sth, tx, ty)) {
+                const unsigned long long tile = (unsigned long long)(ty * cam.tiles_x + tx);
+                keys[o] = view_key | (tile << 32) | k;
+                vals[o] = (uint32_t)i;
+                ++o;
+            }
+}
+
 cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
                         uint64_t view_key, cudaStream_t st)
 {
+    if (v.cam.model == PF_FISHEYE) {
+        cudaEvent_t ev;
+        stage_begin(s, 3, st, &ev);
+        k3_emit_fisheye<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
+            s->ds.N, v.cam, s->ds.sites, s->ds.radii, v.rect.as<int4>(), v.count.as<int>(),
+            v.keybits.as<uint32_t>(), v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals,
+            (unsigned long long)view_key);
+        ++s->launches;
+        stage_end(s, 3, st, ev);
+        return cudaGetLastError();
+    }
     cudaEvent_t ev;
     stage_begin(s, 3, st, &ev);
     k3_emit<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(

@@ -33,23 +33,44 @@ struct Ray {
     float tnear;           // near * |d_cam|
 };
 
-// pixel ray through the continuous pixel coordinate (u, v) (pixel centre = x + 0.5)
+// pixel ray through the continuous pixel coordinate (u, v) (pixel centre = x + 0.5).
+// Pinhole: d = normalize(R (a, b, 1)), t_near = near |(a, b, 1)|.  Equidistant
+// fisheye (NEXT-4): d = R (sin(th) a/th, sin(th) b/th, cos(th)), th = |(a, b)|,
+// t_near = near; *valid = false outside the image circle (th > pi).
 __device__ __forceinline__ void ray_dir(const CamParams &cam, double u, double v, double d[3],
-                                        double *tnear)
+                                        double *tnear, bool *valid = nullptr)
 {
     // explicit IEEE double intrinsics: K6 and K7 must produce bit-identical rays
     double a = __ddiv_rn(__dsub_rn(u, (double)cam.cx), (double)cam.fx);
     double b = __ddiv_rn(__dsub_rn(v, (double)cam.cy), (double)cam.fy);
-    double w0 = __dadd_rn(__fma_rn((double)cam.M[0], a, __dmul_rn((double)cam.M[1], b)), (double)cam.M[2]);
-    double w1 = __dadd_rn(__fma_rn((double)cam.M[4], a, __dmul_rn((double)cam.M[5], b)), (double)cam.M[6]);
-    double w2 = __dadd_rn(__fma_rn((double)cam.M[8], a, __dmul_rn((double)cam.M[9], b)), (double)cam.M[10]);
+    double c = 1.0;
+    if (cam.model == PF_FISHEYE) {
+        const double th = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
+        if (valid) *valid = th <= 3.14159265358979323846;
+        if (th > 0.0) {
+            double sn, cs;
+            sincos(th, &sn, &cs);
+            const double f = __ddiv_rn(sn, th);
+            a = __dmul_rn(f, a);
+            b = __dmul_rn(f, b);
+            c = cs;
+        } else {
+            a = b = 0.0;
+        }
+    } else if (valid) {
+        *valid = true;
+    }
+    double w0 = __fma_rn((double)cam.M[2], c, __fma_rn((double)cam.M[0], a, __dmul_rn((double)cam.M[1], b)));
+    double w1 = __fma_rn((double)cam.M[6], c, __fma_rn((double)cam.M[4], a, __dmul_rn((double)cam.M[5], b)));
+    double w2 = __fma_rn((double)cam.M[10], c, __fma_rn((double)cam.M[8], a, __dmul_rn((double)cam.M[9], b)));
     double nrm = __dsqrt_rn(__fma_rn(w0, w0, __fma_rn(w1, w1, __dmul_rn(w2, w2))));
     d[0] = __ddiv_rn(w0, nrm);
     d[1] = __ddiv_rn(w1, nrm);
     d[2] = __ddiv_rn(w2, nrm);
     if (tnear)
-        *tnear = __dmul_rn((double)cam.near_plane,
-                           __dsqrt_rn(__fma_rn(a, a, __fma_rn(b, b, 1.0))));
+        *tnear = cam.model == PF_FISHEYE
+                     ? (double)cam.near_plane
+                     : __dmul_rn((double)cam.near_plane, __dsqrt_rn(__fma_rn(a, a, __fma_rn(b, b, 1.0))));
 }
 
 // ---------------------------------------------------------------------------
@@ -221,7 +242,8 @@ __device__ __forceinline__ void composite_step(float sig, float dt, float cr, fl
 
 struct PixelSetup {
     int x, y;
-    bool valid;
+    bool in_image;   // inside the W x H image (gets an output)
+    bool valid;      // and has a ray (fisheye: inside the image circle)
     Ray R;
 };
 
@@ -234,15 +256,24 @@ __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, Pixe
     const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 4;
     P.x = x0 + (lane & 7);
     P.y = y0 + (lane >> 3);
-    P.valid = P.x < cam.W && P.y < cam.H;
+    P.in_image = P.x < cam.W && P.y < cam.H;
+    P.valid = P.in_image;
     double dw[3];
     ray_dir(cam, x0 + 4.0, y0 + 2.0, dw, nullptr);
-    // cone half-angle: the largest angle to the four corner pixel rays (the
-    // angle to d_w is quasi-convex over the image plane, so corners bound it)
-    double dcn[3];
+    // cone half-angle.  Pinhole: the largest angle to the four corner pixel rays
+    // (the angle to d_w is quasi-convex over the image plane, so corners bound it).
+    // Fisheye: the (a, b) -> ray map is 1-Lipschitz in angle, so the largest
+    // (a, b) distance to a corner pixel centre bounds it.
     const int cxo = (lane & 1) ? 7 : 0, cyo = (lane & 2) ? 3 : 0;
-    ray_dir(cam, x0 + cxo + 0.5, y0 + cyo + 0.5, dcn, nullptr);
-    double cs = __fma_rn(dw[0], dcn[0], __fma_rn(dw[1], dcn[1], __dmul_rn(dw[2], dcn[2])));
+    double cs;
+    if (cam.model == PF_FISHEYE) {
+        const double da = (cxo + 0.5 - 4.0) / (double)cam.fx, db = (cyo + 0.5 - 2.0) / (double)cam.fy;
+        cs = cos(fmin(sqrt(da * da + db * db) * 1.000001 + 1e-9, 3.14159265358979323846));
+    } else {
+        double dcn[3];
+        ray_dir(cam, x0 + cxo + 0.5, y0 + cyo + 0.5, dcn, nullptr);
+        cs = __fma_rn(dw[0], dcn[0], __fma_rn(dw[1], dcn[1], __dmul_rn(dw[2], dcn[2])));
+    }
     cs = fmin(cs, __shfl_xor_sync(0xffffffffu, cs, 1));
     cs = fmin(cs, __shfl_xor_sync(0xffffffffu, cs, 2));
     cs = fmin(cs, 1.0);
@@ -254,7 +285,9 @@ __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, Pixe
         W.sin_t = sqrt(fmax(0.0, 1.0 - cs * cs));
     }
     double d[3], tn;
-    ray_dir(cam, P.x + 0.5, P.y + 0.5, d, &tn);
+    bool in_circle;
+    ray_dir(cam, P.x + 0.5, P.y + 0.5, d, &tn, &in_circle);
+    P.valid = P.valid && in_circle;
     P.R.dx = __double2float_rn(d[0]);
     P.R.dy = __double2float_rn(d[1]);
     P.R.dz = __double2float_rn(d[2]);
@@ -499,7 +532,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
         __syncwarp();
     }
     if (kRecord && lane == 0) wdone[(size_t)tile * kWarps + warp] = chunks;
-    if (P.valid) {
+    if (P.in_image) {   // pixels without a ray keep T = 1: the background
         const float4 o = make_float4(fmaf(T, ds.bg[0], Cr), fmaf(T, ds.bg[1], Cg),
                                      fmaf(T, ds.bg[2], Cb), T);
         const size_t pix = (size_t)P.y * cam.W + P.x;
