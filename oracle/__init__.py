@@ -28,6 +28,11 @@ class OCamera(C.Structure):
                 ("c2w", C.c_float * 12), ("near_plane", C.c_float), ("model", C.c_int32)]
 
 
+class ODetail(C.Structure):
+    _fields_ = [("K", C.c_int32), ("uv", C.c_void_p), ("disp", C.c_void_p), ("sv", C.c_void_p),
+                ("axes", C.c_float * 24), ("gamma", C.c_float), ("tau", C.c_float)]
+
+
 def build(force: bool = False) -> str:
     """Compile the oracle (plain C, OpenMP, no FMA contraction)."""
     if force or not os.path.exists(_LIB_PATH) or \
@@ -54,18 +59,21 @@ def lib():
         L.oracle_emit_sort.argtypes = [i64, P, P, P, C.c_int32, P, P, P, P, P]
         L.oracle_emit_sort.restype = i64
         L.oracle_tile_ranges.argtypes = [i64, P, C.c_int32, P]
-        L.oracle_render.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P, P,
-                                    P, P, P, C.c_int]
-        L.oracle_backward.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P,
-                                      P, P, P, P, P, P, C.c_int]
-        L.oracle_cell_stats.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, i64, P, P,
-                                         P, C.c_int]
+        L.oracle_render.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, P, i64, P, P,
+                                    P, P, P, P, C.c_int]
+        L.oracle_backward.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, P, i64, P, P,
+                                      P, P, P, P, P, P, P, P, P, C.c_int]
+        L.oracle_cell_stats.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, P, i64, P,
+                                         P, P, C.c_int]
         L.oracle_cech_rows.argtypes = [i64, P, P, i64, P, P, P, P, C.c_int]
         L.oracle_connect_loss.argtypes = [i64, P, P, P, P, P, P, P]
-        L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, P, i64, P, P,
+        L.oracle_cell_interval.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, i64, P, P,
                                            C.c_double, P, P]
-        L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P,
+        L.oracle_pixel_segments.argtypes = [C.c_int, i64, P, P, P, P, P, P, P, P, P, P, P,
                                              C.c_int32, C.c_int32, P, i64]
+        L.oracle_tangent_frame.argtypes = [P, P]
+        L.oracle_soft_voronoi.argtypes = [P, P, C.c_int32, C.c_double, P]
+        L.oracle_detail_probe.argtypes = [i64, P, P, P, P, i64, P, P, C.c_double, P]
         L.oracle_pixel_segments.restype = i64
         L.oracle_pixel_ray.argtypes = [P, C.c_int32, C.c_int32, P, P, P]
         L.oracle_composite.argtypes = [i64, P, P, P, P, P]
@@ -109,10 +117,27 @@ class _SceneArrays:
         self.bg = np.asarray(sc.background, np.float32)
         nrm = getattr(sc, "normals", None)
         self.normals = None if nrm is None else _c(nrm, np.float32)
+        det = getattr(sc, "detail", None)
+        self.det = None
+        if det is not None and self.normals is not None:
+            self.uv = _c(det.uv, np.float32)
+            self.disp = _c(det.disp, np.float32)
+            self.sv = _c(det.sv, np.float32)
+            d = ODetail()
+            d.K = int(self.uv.shape[1])
+            d.uv, d.disp, d.sv = _p(self.uv), _p(self.disp), _p(self.sv)
+            for k, v in enumerate(np.asarray(det.axes, np.float32).reshape(24)):
+                d.axes[k] = float(v)
+            d.gamma, d.tau = float(det.gamma), float(det.tau)
+            self.det = d
+
+    def detp(self):
+        return None if self.det is None else C.cast(C.pointer(self.det), C.c_void_p)
 
     def args(self):
         return [self.N, _p(self.sites), _p(self.weights), _p(self.radii), _p(self.density),
-                _p(self.rgb), _p(self.off), _p(self.idx), _p(self.bg), _p(self.normals)]
+                _p(self.rgb), _p(self.off), _p(self.idx), _p(self.bg), _p(self.normals),
+                self.detp()]
 
 
 # ---------------------------------------------------------------------------
@@ -194,11 +219,17 @@ def backward(sc, cam, grad_out, mode=O3, pixels=None, nthreads=0):
     gs = np.zeros((N, 3)); gw = np.zeros(N); gr = np.zeros(N); gsig = np.zeros(N)
     grgb = np.zeros((N, 3))
     gn = np.zeros((N, 3)) if A.normals is not None else None
+    guv = gdisp = gsv = None
+    if A.det is not None:
+        guv = np.zeros(A.uv.shape); gdisp = np.zeros(A.disp.shape); gsv = np.zeros(A.sv.shape)
     lib().oracle_backward(mode, *A.args(), C.byref(oc), n, _p(pix), _p(g), _p(gs), _p(gw),
-                          _p(gr), _p(gsig), _p(grgb), _p(gn), nthreads)
+                          _p(gr), _p(gsig), _p(grgb), _p(gn), _p(guv), _p(gdisp), _p(gsv),
+                          nthreads)
     out = dict(sites=gs, weights=gw, radii=gr, density=gsig, rgb=grgb)
     if gn is not None:
         out["normals"] = gn
+    if guv is not None:
+        out.update(detail_uv=guv, detail_disp=gdisp, detail_sv=gsv)
     return out
 
 
@@ -228,7 +259,8 @@ def cell_interval(sc, i, Q, d, t_near=0.0, mode=O2):
     res = np.zeros(2)
     kinds = np.zeros(4, np.int32)
     hit = lib().oracle_cell_interval(mode, A.N, _p(A.sites), _p(A.weights), _p(A.radii),
-                                     _p(A.off), _p(A.idx), _p(A.normals), int(i), _p(Qa), _p(da),
+                                     _p(A.off), _p(A.idx), _p(A.normals), A.detp(), int(i),
+                                     _p(Qa), _p(da),
                                      float(t_near), _p(res), _p(kinds))
     return bool(hit), float(res[0]), float(res[1]), kinds
 
@@ -242,6 +274,34 @@ def pixel_segments(sc, cam, x, y, mode=O3, cap=4096):
     n = lib().oracle_pixel_segments(mode, *A.args(), C.byref(oc), int(x), int(y), _p(buf), cap)
     keys = ("cell", "t_in", "t_out", "kin", "kout", "jin", "jout", "list_pos")
     return [dict(zip(keys, row)) for row in buf[:n]]
+
+
+def tangent_frame(n):
+    """(u, v, m) of a face normal and the chosen axis."""
+    nn = _c(n, np.float32)
+    out = np.zeros(9)
+    k = lib().oracle_tangent_frame(_p(nn), _p(out))
+    return out[:3], out[3:6], out[6:], int(k)
+
+
+def soft_voronoi(q, uv, tau):
+    """Soft-Voronoi weights of the chart point q against sites uv [K,2]."""
+    qa = _c(q, np.float64); u = _c(uv, np.float32).reshape(-1, 2)
+    w = np.zeros(u.shape[0])
+    assert lib().oracle_soft_voronoi(_p(qa), _p(u), u.shape[0], float(tau), _p(w)) == 0
+    return w
+
+
+def detail_probe(sc, i, Q, d, t_entry=0.0):
+    """Detail evaluation of cell i on the ray Q + t d: dict(parallel, tb, dr, delta, ts,
+    col[3], qb[2], qs[2]) (P:284-293)."""
+    A = _SceneArrays(sc)
+    Qa = _c(Q, np.float64); da = _c(d, np.float64)
+    out = np.zeros(12)
+    assert lib().oracle_detail_probe(A.N, _p(A.sites), _p(A.radii), _p(A.normals), A.detp(),
+                                     int(i), _p(Qa), _p(da), float(t_entry), _p(out)) == 0
+    return dict(parallel=bool(out[0]), tb=out[1], dr=out[2], delta=out[3], ts=out[4],
+                col=out[5:8].copy(), qb=out[8:10].copy(), qs=out[10:12].copy())
 
 
 def pixel_ray(cam, x, y):

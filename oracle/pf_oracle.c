@@ -45,6 +45,19 @@
  *      the side the normal points away from); the other half has zero density,
  *      so I_i is further intersected with that half-space.
  *
+ *      Detail sites (NEXT-2, P:278-297 Eqs. svdisp/svrad): each
+ *      dipole face carries K detail sites s_k in the face's 2D chart (the
+ *      tangent frame of SPEC S:186-189), displacements d_k and per-site
+ *      Spherical-Voronoi radiance (8 shared axes a_a, sharpness gamma).
+ *      Step by step as P:284-293 describes it (with the readings R6 of
+ *      DESIGN.md): x_bar = the ray's hit on the base face (x-p).n = 0;
+ *      delta = sum_k softmax_k(-tau |q(x_bar) - s_k|) d_k (Eq. svdisp),
+ *      clamped to [-r, r]; the occupied half becomes
+ *      (x - p).n <= delta; x = the ray's hit on that displaced face; the
+ *      segment colour is c(x) = sum_k softmax_k(-tau |q(x) - s_k|) c_k(d)
+ *      (Eq. svrad) with c_k(d) = sum_a softmax_a(gamma d.a_a) v_{k,a}.
+ *      q(y) = ((y-p).u, (y-p).v) are the chart coordinates.
+ *
  *  (2) The backward pass: the exact derivative of (1) for a fixed active set
  *      and termination index, L = sum_pixels <grad_out, out> (
  *      endpoint derivatives of the sphere and the radical plane).
@@ -89,7 +102,21 @@ typedef struct {
     const int32_t *nbr_idx;
     double bg[3];
     const float *normals; /* dipole normals n_i [N,3] or NULL (NEXT-1) */
+    const struct oc_detail_s *det; /* detail sites (NEXT-2) or NULL */
 } oc_scene;
+
+/* Detail sites of the dipole faces (NEXT-2). */
+#define OC_MAX_DETAIL 8
+#define OC_SV_AXES 8
+typedef struct oc_detail_s {
+    int32_t K;           /* detail sites per cell, 1..8 (0 = none) */
+    const float *uv;     /* s_{i,k} [N,K,2] chart coordinates (world units) */
+    const float *disp;   /* d_{i,k} [N,K] displacement along the unit normal */
+    const float *sv;     /* v_{i,k,a} [N,K,8,3] SV radiance per axis */
+    float axes[OC_SV_AXES][3]; /* the shared SV axes a_a (unit) */
+    float gamma;         /* SV sharpness */
+    float tau;           /* soft-Voronoi temperature (1 / world units) */
+} oc_detail;
 
 #define O1_ALL_PAIRS 1
 #define O2_LIST_PLANES 2
@@ -394,12 +421,154 @@ typedef struct {
     int32_t kin, kout;   /* END_* */
     int32_t jin, jout;   /* neighbour cell for END_PLANE */
     int32_t list_pos;    /* position in the tile list (O3), else -1 */
+    double col[3];       /* segment radiance: rgb_i, or c(x) of the detail sites */
 } oc_seg;
 
 static double powd(const double x[3], const float *p, float w)
 {
     double a = x[0] - p[0], b = x[1] - p[1], c = x[2] - p[2];
     return a * a + b * b + c * c - (double)w;
+}
+
+/* ---- detail sites (NEXT-2) --------------------------------------------- */
+
+static double dot3(const double a[3], const double b[3])
+{
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+static void cross3(const double a[3], const double b[3], double o[3])
+{
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* Tangent frame of the face: m = n/|n|; k = the axis of the
+ * smallest |n_k| (strictly smaller than the others for x, ties -> the higher
+ * index); u = (e_k x m)/|e_k x m|, v = m x u, so (u, v, m) is right-handed and
+ * n = (0,0,1) gives u = (1,0,0), v = (0,1,0). */
+typedef struct {
+    double m[3], u[3], v[3];
+    double nn, wl; /* |n|, |e_k x m| */
+    int kax;
+} oc_frame;
+
+static void tangent_frame(const float *n, oc_frame *F)
+{
+    F->nn = sqrt((double)n[0] * n[0] + (double)n[1] * n[1] + (double)n[2] * n[2]);
+    for (int c = 0; c < 3; ++c) F->m[c] = (double)n[c] / F->nn;
+    const float ax = fabsf(n[0]), ay = fabsf(n[1]), az = fabsf(n[2]);
+    F->kax = (ax < ay && ax < az) ? 0 : (ay <= az ? 1 : 2);
+    double e[3] = {0, 0, 0}, w[3];
+    e[F->kax] = 1.0;
+    cross3(e, F->m, w);
+    F->wl = sqrt(dot3(w, w));
+    for (int c = 0; c < 3; ++c) F->u[c] = w[c] / F->wl;
+    cross3(F->m, F->u, F->v);
+}
+
+/* soft-Voronoi weights (Eqs. svdisp/svrad): w_k = exp(-tau rho_k) /
+ * sum_j exp(-tau rho_j), rho_k = |q - s_k|, with max-subtraction */
+static void soft_voronoi(const double q[2], const float *uv, int K, double tau, double rho[],
+                         double w[])
+{
+    double zmax = -HUGE_VAL, z[OC_MAX_DETAIL], sum = 0.0;
+    for (int k = 0; k < K; ++k) {
+        double a = q[0] - uv[2 * k], b = q[1] - uv[2 * k + 1];
+        rho[k] = sqrt(a * a + b * b);
+        z[k] = -tau * rho[k];
+        if (z[k] > zmax) zmax = z[k];
+    }
+    for (int k = 0; k < K; ++k) {
+        w[k] = exp(z[k] - zmax);
+        sum += w[k];
+    }
+    for (int k = 0; k < K; ++k) w[k] /= sum;
+}
+
+/* Everything the detail evaluation of one (ray, cell) computes, in the order of
+ * P:284-293.  Vectors from p_i: c = p - Q, y = x_bar - p, ys = x - p. */
+typedef struct {
+    oc_frame F;
+    double c[3], A, B;         /* A = d.m, B = c.m */
+    int parallel;              /* A == 0: no base-face hit (reading R6e) */
+    double tb, y[3], qb[2], rho[OC_MAX_DETAIL], w[OC_MAX_DETAIL];
+    double dr, delta;          /* sum_k w_k d_k and its clamp to [-r, r] */
+    int clamp;                 /* 0, +1 (delta = r), -1 (delta = -r) */
+    double ts, ys[3], qs[2], rhos[OC_MAX_DETAIL], ws[OC_MAX_DETAIL];
+    double om[OC_SV_AXES];     /* softmax_a(gamma d.a_a) */
+    double ck[OC_MAX_DETAIL][3], col[3];
+} oc_dstate;
+
+/* steps 1-3 of P:284-289: base-face hit, displacement, displaced-face hit t* */
+static void detail_geometry(const oc_scene *S, int64_t i, const double Q[3], const double d[3],
+                            oc_dstate *D)
+{
+    const oc_detail *X = S->det;
+    const float *p = S->sites + 3 * i;
+    const int K = X->K;
+    tangent_frame(S->normals + 3 * i, &D->F);
+    for (int c = 0; c < 3; ++c) D->c[c] = (double)p[c] - Q[c];
+    D->A = dot3(d, D->F.m);
+    D->B = dot3(D->c, D->F.m);
+    D->parallel = (D->A == 0.0);
+    D->delta = 0.0;
+    D->clamp = 0;
+    if (D->parallel) return;
+    /* x_bar: (Q + t d - p).m = 0 */
+    D->tb = D->B / D->A;
+    for (int c = 0; c < 3; ++c) D->y[c] = D->tb * d[c] - D->c[c];
+    D->qb[0] = dot3(D->y, D->F.u);
+    D->qb[1] = dot3(D->y, D->F.v);
+    soft_voronoi(D->qb, X->uv + (size_t)2 * K * i, K, (double)X->tau, D->rho, D->w);
+    D->dr = 0.0;
+    for (int k = 0; k < K; ++k) D->dr += D->w[k] * (double)X->disp[(size_t)K * i + k];
+    const double r = (double)S->radii[i];
+    D->delta = D->dr;
+    if (D->dr > r) {
+        D->delta = r;
+        D->clamp = 1;
+    } else if (D->dr < -r) {
+        D->delta = -r;
+        D->clamp = -1;
+    }
+    /* x on the displaced face (Q + t d - p).m = delta */
+    D->ts = (D->B + D->delta) / D->A;
+}
+
+/* step 4 (Eq. svrad): the radiance at x = p + ys (the parallel case uses the
+ * interval's entry point, reading R6e) */
+static void detail_radiance(const oc_scene *S, int64_t i, const double d[3], double t_entry,
+                            oc_dstate *D)
+{
+    const oc_detail *X = S->det;
+    const int K = X->K;
+    const double t = D->parallel ? t_entry : D->ts;
+    for (int c = 0; c < 3; ++c) D->ys[c] = t * d[c] - D->c[c];
+    D->qs[0] = dot3(D->ys, D->F.u);
+    D->qs[1] = dot3(D->ys, D->F.v);
+    soft_voronoi(D->qs, X->uv + (size_t)2 * K * i, K, (double)X->tau, D->rhos, D->ws);
+    double z[OC_SV_AXES], zmax = -HUGE_VAL, sum = 0.0;
+    for (int a = 0; a < OC_SV_AXES; ++a) {
+        z[a] = (double)X->gamma * (d[0] * X->axes[a][0] + d[1] * X->axes[a][1] +
+                                   d[2] * X->axes[a][2]);
+        if (z[a] > zmax) zmax = z[a];
+    }
+    for (int a = 0; a < OC_SV_AXES; ++a) {
+        D->om[a] = exp(z[a] - zmax);
+        sum += D->om[a];
+    }
+    for (int a = 0; a < OC_SV_AXES; ++a) D->om[a] /= sum;
+    D->col[0] = D->col[1] = D->col[2] = 0.0;
+    for (int k = 0; k < K; ++k) {
+        const float *vk = X->sv + ((size_t)K * i + k) * OC_SV_AXES * 3;
+        for (int c = 0; c < 3; ++c) {
+            D->ck[k][c] = 0.0;
+            for (int a = 0; a < OC_SV_AXES; ++a) D->ck[k][c] += D->om[a] * (double)vk[3 * a + c];
+            D->col[c] += D->ws[k] * D->ck[k][c];
+        }
+    }
 }
 
 /* Interval of cell i along the ray.  Returns 1 (and fills *s) if the ray meets
@@ -422,6 +591,7 @@ static int cell_interval(const oc_scene *S, int mode, int64_t i, const double Q[
     if (!(tc + sq > t_near)) return 0;
     s->cell = (int32_t)i;
     s->list_pos = -1;
+    for (int c = 0; c < 3; ++c) s->col[c] = S->rgb ? (double)S->rgb[3 * i + c] : 0.0;
     s->t_in = tc - sq;
     s->kin = END_SPHERE;
     s->jin = -1;
@@ -469,7 +639,27 @@ static int cell_interval(const oc_scene *S, int mode, int64_t i, const double Q[
             empty = 1; /* ray parallel to the plane, on j's side (C14) */
         }
     }
-    if (S->normals) {
+    if (S->det && S->det->K > 0) {
+        /* detail sites (NEXT-2): the occupied half is (x - p).m <= delta, delta
+         * from the soft-Voronoi displacement at the base-face hit */
+        oc_dstate D;
+        detail_geometry(S, i, Q, d, &D);
+        if (D.parallel) {
+            if (D.B < 0.0) empty = 1; /* (x - p).m = -B > 0 = delta everywhere */
+        } else if (D.A > 0.0) {
+            if (D.ts < s->t_out) {
+                s->t_out = D.ts;
+                s->kout = END_DIPOLE;
+                s->jout = -1;
+            }
+        } else if (D.ts > s->t_in) {
+            s->t_in = D.ts;
+            s->kin = END_DIPOLE;
+            s->jin = -1;
+        }
+        detail_radiance(S, i, d, s->t_in, &D);
+        for (int c = 0; c < 3; ++c) s->col[c] = D.col[c];
+    } else if (S->normals) {
         /* oriented-point dipole: only the half-space the normal points
          * away from is occupied, (x - p_i).n_i <= 0 (SPEC S:242 convention);
          * (x(t) - p_i).n_i = (Q - p_i).n_i + t d.n_i  ->  A t <= B */
@@ -613,7 +803,7 @@ static int64_t composite(const oc_scene *S, const oc_seg *segs, int64_t n, doubl
         double sig = (double)S->density[s->cell];
         double tau = sig * (s->t_out - s->t_in);
         double alpha = 1.0 - exp(-tau);
-        for (int c = 0; c < 3; ++c) C[c] += T * alpha * (double)S->rgb[3 * s->cell + c];
+        for (int c = 0; c < 3; ++c) C[c] += T * alpha * s->col[c];
         T *= exp(-tau);
         ++k;
         if (T < T_STOP) break;
@@ -657,9 +847,10 @@ static void pixel_counters(const oc_scene *S, const oc_bins *B, int x, int y, co
 static void make_scene(oc_scene *S, int64_t N, const float *sites, const float *weights,
                        const float *radii, const float *density, const float *rgb,
                        const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                       const float *normals)
+                       const float *normals, const oc_detail *det)
 {
     S->normals = normals;
+    S->det = (det && det->K > 0 && normals) ? det : NULL;
     S->N = N;
     S->sites = sites;
     S->weights = weights;
@@ -681,12 +872,12 @@ static void make_scene(oc_scene *S, int64_t N, const float *sites, const float *
 int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
                   const float *radii, const float *density, const float *rgb,
                   const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                  const float *normals, const oc_camera *cam, int64_t npix, const int32_t *pix_xy, double *out,
+                  const float *normals, const oc_detail *det, const oc_camera *cam, int64_t npix, const int32_t *pix_xy, double *out,
                   int64_t *counters, uint64_t *sig, int64_t *nseg_out, int64_t *viol,
                   int nthreads)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals, det);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS || counters) build_bins(&S, cam, &B);
@@ -747,11 +938,11 @@ int oracle_render(int mode, int64_t N, const float *sites, const float *weights,
 int oracle_cell_stats(int mode, int64_t N, const float *sites, const float *weights,
                       const float *radii, const float *density, const float *rgb,
                       const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                      const float *normals, const oc_camera *cam, int64_t npix,
+                      const float *normals, const oc_detail *det, const oc_camera *cam, int64_t npix,
                       const int32_t *pix_xy, double *contrib, double *normal_term, int nthreads)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals, det);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
@@ -851,6 +1042,123 @@ static void end_grad(const oc_scene *S, int kind, int64_t i, int64_t j, double t
     g_w[j] -= sgn_gdt * 0.5 / a;
 }
 
+/* Reverse-mode derivative of one detail segment (NEXT-2), step by step back
+ * through detail_radiance and detail_geometry.  g_ts = dL/dt* from the
+ * interval ends the displaced face binds; gC = dL/dc(x) = T_k alpha_k G. */
+static void detail_backward(const oc_scene *S, int64_t i, const double Q[3], const double d[3],
+                            const oc_seg *s, double g_ts, const double gC[3], double *g_sites,
+                            double *g_r, double *g_normals, double *g_uv, double *g_disp,
+                            double *g_sv)
+{
+    const oc_detail *X = S->det;
+    const int K = X->K;
+    const float *uv = X->uv + (size_t)2 * K * i;
+    const double tau = (double)X->tau;
+    oc_dstate D;
+    detail_geometry(S, i, Q, d, &D);
+    detail_radiance(S, i, d, s->t_in, &D);
+    const oc_frame *F = &D.F;
+    double gm[3] = {0, 0, 0}, gc[3] = {0, 0, 0}, gu[3] = {0, 0, 0}, gv[3] = {0, 0, 0};
+    /* Eq. svrad: col = sum_k ws_k c_k,  c_k = sum_a om_a v_{k,a} */
+    double gws[OC_MAX_DETAIL], sw = 0.0;
+    for (int k = 0; k < K; ++k) {
+        double *gvk = g_sv + ((size_t)K * i + k) * OC_SV_AXES * 3;
+        for (int a = 0; a < OC_SV_AXES; ++a)
+            for (int c = 0; c < 3; ++c) {
+#pragma omp atomic
+                gvk[3 * a + c] += D.ws[k] * D.om[a] * gC[c];
+            }
+        gws[k] = dot3(D.ck[k], gC);
+        sw += D.ws[k] * gws[k];
+    }
+    /* softmax of z_k = -tau rho_k, rho_k = |qs - s_k| */
+    double gqs[2] = {0, 0};
+    for (int k = 0; k < K; ++k) {
+        const double grho = -tau * D.ws[k] * (gws[k] - sw);
+        if (D.rhos[k] > 0.0) {
+            const double ex = (D.qs[0] - uv[2 * k]) / D.rhos[k], ey = (D.qs[1] - uv[2 * k + 1]) / D.rhos[k];
+            gqs[0] += grho * ex;
+            gqs[1] += grho * ey;
+#pragma omp atomic
+            g_uv[(size_t)2 * K * i + 2 * k] -= grho * ex;
+#pragma omp atomic
+            g_uv[(size_t)2 * K * i + 2 * k + 1] -= grho * ey;
+        }
+    }
+    if (!D.parallel) {
+        /* qs = (ys.u, ys.v) */
+        double gys[3];
+        for (int c = 0; c < 3; ++c) {
+            gys[c] = gqs[0] * F->u[c] + gqs[1] * F->v[c];
+            gu[c] += gqs[0] * D.ys[c];
+            gv[c] += gqs[1] * D.ys[c];
+        }
+        /* ys = ts d - c */
+        g_ts += dot3(gys, d);
+        for (int c = 0; c < 3; ++c) gc[c] -= gys[c];
+        /* ts = (c.m + delta) / (d.m) */
+        const double f = g_ts / D.A;
+        for (int c = 0; c < 3; ++c) {
+            gc[c] += f * F->m[c];
+            gm[c] -= f * D.ys[c];
+        }
+        double gdr = 0.0;
+        if (D.clamp) {
+#pragma omp atomic
+            g_r[i] += f * (double)D.clamp;
+        } else {
+            gdr = f;
+        }
+        /* Eq. svdisp: dr = sum_k w_k d_k, w = softmax(-tau rho), rho_k = |qb - s_k| */
+        double gqb[2] = {0, 0};
+        for (int k = 0; k < K; ++k) {
+            const double dk = (double)X->disp[(size_t)K * i + k];
+#pragma omp atomic
+            g_disp[(size_t)K * i + k] += D.w[k] * gdr;
+            const double grho = -tau * D.w[k] * gdr * (dk - D.dr);
+            if (D.rho[k] > 0.0) {
+                const double ex = (D.qb[0] - uv[2 * k]) / D.rho[k], ey = (D.qb[1] - uv[2 * k + 1]) / D.rho[k];
+                gqb[0] += grho * ex;
+                gqb[1] += grho * ey;
+#pragma omp atomic
+                g_uv[(size_t)2 * K * i + 2 * k] -= grho * ex;
+#pragma omp atomic
+                g_uv[(size_t)2 * K * i + 2 * k + 1] -= grho * ey;
+            }
+        }
+        /* qb = (y.u, y.v), y = tb d - c, tb = c.m / (d.m) */
+        double gy[3];
+        for (int c = 0; c < 3; ++c) {
+            gy[c] = gqb[0] * F->u[c] + gqb[1] * F->v[c];
+            gu[c] += gqb[0] * D.y[c];
+            gv[c] += gqb[1] * D.y[c];
+        }
+        const double f2 = dot3(gy, d) / D.A;
+        for (int c = 0; c < 3; ++c) {
+            gc[c] += f2 * F->m[c] - gy[c];
+            gm[c] -= f2 * D.y[c];
+        }
+    }
+    /* frame: v = m x u, u = w/|w|, w = e_k x m, m = n/|n| */
+    double t3[3], e[3] = {0, 0, 0}, gw[3];
+    cross3(F->u, gv, t3);
+    for (int c = 0; c < 3; ++c) gm[c] += t3[c];
+    cross3(gv, F->m, t3);
+    for (int c = 0; c < 3; ++c) gu[c] += t3[c];
+    const double ug = dot3(F->u, gu);
+    for (int c = 0; c < 3; ++c) gw[c] = (gu[c] - F->u[c] * ug) / F->wl;
+    e[F->kax] = 1.0;
+    cross3(gw, e, t3);
+    for (int c = 0; c < 3; ++c) gm[c] += t3[c];
+    const double mg = dot3(F->m, gm);
+    for (int c = 0; c < 3; ++c) {
+#pragma omp atomic
+        g_sites[3 * i + c] += gc[c];
+#pragma omp atomic
+        g_normals[3 * i + c] += (gm[c] - F->m[c] * mg) / F->nn;
+    }
+}
+
 /*
  * Gradients of L = sum_pixels <grad_out[pixel], out[pixel]> for npix pixels
  * (same pixel convention as oracle_render; grad_out float[npix*4]).
@@ -863,12 +1171,13 @@ static void end_grad(const oc_scene *S, int kind, int64_t i, int64_t j, double t
 int oracle_backward(int mode, int64_t N, const float *sites, const float *weights,
                     const float *radii, const float *density, const float *rgb,
                     const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                    const float *normals, const oc_camera *cam, int64_t npix,
+                    const float *normals, const oc_detail *det, const oc_camera *cam, int64_t npix,
                     const int32_t *pix_xy, const float *grad_out, double *g_sites, double *g_w,
-                    double *g_r, double *g_sigma, double *g_rgb, double *g_normals, int nthreads)
+                    double *g_r, double *g_sigma, double *g_rgb, double *g_normals,
+                    double *g_uv, double *g_disp, double *g_sv, int nthreads)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals, det);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
@@ -920,17 +1229,33 @@ int oracle_backward(int mode, int64_t N, const float *sites, const float *weight
                 for (int c = 0; c < 3; ++c) Sk[c] = Tend * S.bg[c];
                 for (int64_t m = k + 1; m < K; ++m)
                     for (int c = 0; c < 3; ++c)
-                        Sk[c] += Tk[m] * Ak[m] * (double)S.rgb[3 * scr.segs[m].cell + c];
+                        Sk[c] += Tk[m] * Ak[m] * scr.segs[m].col[c];
                 double dtau = -GT * Tend;
                 for (int c = 0; c < 3; ++c) {
-                    dtau += G[c] * (Tnext * (double)S.rgb[3 * i + c] - Sk[c]);
+                    dtau += G[c] * (Tnext * s->col[c] - Sk[c]);
+                    if (!S.det) {
 #pragma omp atomic
-                    g_rgb[3 * i + c] += Tk[k] * Ak[k] * G[c];
+                        g_rgb[3 * i + c] += Tk[k] * Ak[k] * G[c];
+                    }
                 }
 #pragma omp atomic
                 g_sigma[i] += dtau * dt;
                 double gdt = dtau * sig;
-                if (gdt != 0.0) {
+                if (S.det) {
+                    /* the displaced face's end goes through the detail chain */
+                    double g_ts = 0.0, gC[3];
+                    if (s->kout == END_DIPOLE) g_ts += gdt;
+                    if (s->kin == END_DIPOLE) g_ts -= gdt;
+                    if (s->kout != END_DIPOLE)
+                        end_grad(&S, s->kout, i, s->jout, s->t_out, Q, d, gdt, g_sites, g_w, g_r,
+                                 g_normals);
+                    if (s->kin != END_DIPOLE)
+                        end_grad(&S, s->kin, i, s->jin, s->t_in, Q, d, -gdt, g_sites, g_w, g_r,
+                                 g_normals);
+                    for (int c = 0; c < 3; ++c) gC[c] = Tk[k] * Ak[k] * G[c];
+                    detail_backward(&S, i, Q, d, s, g_ts, gC, g_sites, g_r, g_normals, g_uv,
+                                    g_disp, g_sv);
+                } else if (gdt != 0.0) {
                     end_grad(&S, s->kout, i, s->jout, s->t_out, Q, d, gdt, g_sites, g_w, g_r,
                              g_normals);
                     end_grad(&S, s->kin, i, s->jin, s->t_in, Q, d, -gdt, g_sites, g_w, g_r,
@@ -955,11 +1280,12 @@ int oracle_backward(int mode, int64_t N, const float *sites, const float *weight
  * Returns 1 on a sphere hit, 0 otherwise. */
 int oracle_cell_interval(int mode, int64_t N, const float *sites, const float *weights,
                          const float *radii, const int64_t *nbr_off, const int32_t *nbr_idx,
-                         const float *normals, int64_t i, const double *Q, const double *d,
+                         const float *normals, const oc_detail *det, int64_t i,
+                         const double *Q, const double *d,
                          double t_near, double *res, int32_t *kinds)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, NULL, NULL, nbr_off, nbr_idx, NULL, normals);
+    make_scene(&S, N, sites, weights, radii, NULL, NULL, nbr_off, nbr_idx, NULL, normals, det);
     oc_seg s;
     int64_t np = 0;
     int hit = cell_interval(&S, mode, i, Q, d, t_near, &s, &np);
@@ -979,11 +1305,11 @@ int oracle_cell_interval(int mode, int64_t N, const float *sites, const float *w
 int64_t oracle_pixel_segments(int mode, int64_t N, const float *sites, const float *weights,
                               const float *radii, const float *density, const float *rgb,
                               const int64_t *nbr_off, const int32_t *nbr_idx, const float *bg,
-                              const float *normals, const oc_camera *cam, int32_t x, int32_t y,
+                              const float *normals, const oc_detail *det, const oc_camera *cam, int32_t x, int32_t y,
                               double *seg, int64_t cap)
 {
     oc_scene S;
-    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals);
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals, det);
     oc_bins B;
     memset(&B, 0, sizeof(B));
     if (mode == O3_TILE_LISTS) build_bins(&S, cam, &B);
@@ -1114,5 +1440,57 @@ int oracle_connect_loss(int64_t N, const float *sites, const float *radii,
         }
         loss[i] = Li;
     }
+    return 0;
+}
+
+/* ======================================================================== */
+/* detail-site probes (NEXT-2 pins)                                         */
+/* ======================================================================== */
+
+/* tangent frame of one normal: out[9] = (u, v, m) */
+int oracle_tangent_frame(const float *n, double *out)
+{
+    oc_frame F;
+    tangent_frame(n, &F);
+    for (int c = 0; c < 3; ++c) {
+        out[c] = F.u[c];
+        out[3 + c] = F.v[c];
+        out[6 + c] = F.m[c];
+    }
+    return F.kax;
+}
+
+/* soft-Voronoi weights of q against K sites (Eqs. svdisp/svrad) */
+int oracle_soft_voronoi(const double *q, const float *uv, int32_t K, double tau, double *w)
+{
+    double rho[OC_MAX_DETAIL];
+    if (K < 1 || K > OC_MAX_DETAIL) return -1;
+    soft_voronoi(q, uv, K, tau, rho, w);
+    return 0;
+}
+
+/* Detail evaluation of cell i along (Q, d) with the interval entry t_entry
+ * (used by the parallel case): out = (parallel, tb, dr, delta, ts, col[3],
+ * qb[2], qs[2]) -- 12 doubles. */
+int oracle_detail_probe(int64_t N, const float *sites, const float *radii, const float *normals,
+                        const oc_detail *det, int64_t i, const double *Q, const double *d,
+                        double t_entry, double *out)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, NULL, radii, NULL, NULL, NULL, NULL, NULL, normals, det);
+    if (!S.det) return -1;
+    oc_dstate D;
+    detail_geometry(&S, i, Q, d, &D);
+    detail_radiance(&S, i, d, t_entry, &D);
+    out[0] = D.parallel;
+    out[1] = D.parallel ? 0.0 : D.tb;
+    out[2] = D.parallel ? 0.0 : D.dr;
+    out[3] = D.delta;
+    out[4] = D.parallel ? 0.0 : D.ts;
+    for (int c = 0; c < 3; ++c) out[5 + c] = D.col[c];
+    out[8] = D.parallel ? 0.0 : D.qb[0];
+    out[9] = D.parallel ? 0.0 : D.qb[1];
+    out[10] = D.qs[0];
+    out[11] = D.qs[1];
     return 0;
 }

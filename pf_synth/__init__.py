@@ -63,6 +63,7 @@ class Scene:
     name: str = ""
     meta: dict = field(default_factory=dict)
     normals: np.ndarray | None = None   # f32[N,3] dipole normals (NEXT-1), or None
+    detail: "Detail | None" = None      # detail sites of the dipole faces (NEXT-2), or None
 
     @property
     def num_cells(self) -> int:
@@ -77,7 +78,27 @@ class Scene:
                      self.density.copy(), self.rgb.copy(),
                      self.nbr_offsets.copy(), self.nbr_indices.copy(),
                      tuple(self.background), self.name, dict(self.meta),
-                     None if self.normals is None else self.normals.copy())
+                     None if self.normals is None else self.normals.copy(),
+                     None if self.detail is None else self.detail.copy())
+
+
+@dataclass
+class Detail:
+    """Detail sites of the dipole faces (NEXT-2)."""
+    uv: np.ndarray       # f32[N,K,2] site positions in the face chart (world units)
+    disp: np.ndarray     # f32[N,K] displacements along the unit normal
+    sv: np.ndarray       # f32[N,K,8,3] Spherical-Voronoi radiance per axis
+    axes: np.ndarray     # f32[8,3] shared unit SV axes
+    gamma: float = 4.0   # SV sharpness (SPEC S:245 default)
+    tau: float = 1.0     # soft-Voronoi temperature (1 / world units)
+
+    @property
+    def K(self) -> int:
+        return int(self.uv.shape[1])
+
+    def copy(self) -> "Detail":
+        return Detail(self.uv.copy(), self.disp.copy(), self.sv.copy(), self.axes.copy(),
+                      float(self.gamma), float(self.tau))
 
 
 # --------------------------------------------------------------------------
@@ -339,12 +360,53 @@ def add_dipoles(sc: Scene, seed: int = 77, toward=(0.0, 0.0, 0.0)) -> Scene:
     return sc
 
 
+def fibonacci_axes(n: int = 8) -> np.ndarray:
+    """n unit directions on the Fibonacci sphere (the SV axes)."""
+    k = np.arange(n, dtype=np.float64) + 0.5
+    z = 1.0 - 2.0 * k / n
+    phi = np.pi * (3.0 - np.sqrt(5.0)) * k
+    rr = np.sqrt(1.0 - z * z)
+    return np.stack([rr * np.cos(phi), rr * np.sin(phi), z], 1).astype(np.float32)
+
+
+def add_detail(sc: Scene, K: int = 8, seed: int = 91, gamma: float = 4.0,
+               tau_scale: float = 8.0, clamp_frac: float = 0.02) -> Scene:
+    """Detail sites (NEXT-2) on a dipole scene.  Recipe: uv on a
+    centred ring of radius r/2 at equal angles plus N(0, (0.15 r)^2)
+    jitter; displacements U(-0.3 r, 0.3 r), except a `clamp_frac` share of cells
+    at +-1.5 r (exercising the |delta| <= r clamp); SV values: the cell's rgb
+    times U(0.6, 1.4) per (site, axis, channel), clipped to [0, 1];
+    tau = tau_scale / median radius, gamma = 4."""
+    if sc.normals is None:
+        add_dipoles(sc)
+    rng = np.random.default_rng(seed)
+    N = sc.num_cells
+    r = sc.radii.astype(np.float64)
+    ang = 2.0 * np.pi * np.arange(K) / K
+    ring = np.stack([np.cos(ang), np.sin(ang)], 1)[None] * (0.5 * r)[:, None, None]
+    uv = ring + rng.normal(scale=0.15, size=(N, K, 2)) * r[:, None, None]
+    disp = rng.uniform(-0.3, 0.3, size=(N, K)) * r[:, None]
+    big = rng.random(N) < clamp_frac
+    disp[big] = np.where(rng.random((int(big.sum()), K)) < 0.5, -1.5, 1.5) * r[big, None]
+    sv = sc.rgb.astype(np.float64)[:, None, None, :] * rng.uniform(0.6, 1.4, size=(N, K, 8, 3))
+    sc.detail = Detail(uv.astype(np.float32), disp.astype(np.float32),
+                       np.clip(sv, 0.0, 1.0).astype(np.float32), fibonacci_axes(8),
+                       float(gamma), float(np.float32(tau_scale / np.median(r))))
+    sc.meta["detail"] = (K, seed)
+    return sc
+
+
 def make_scene(preset: str, seed: int | None = None, variant: str | None = None,
-               num_cells: int | None = None, dipoles: bool = False) -> Scene:
+               num_cells: int | None = None, dipoles: bool = False,
+               detail: int = 0) -> Scene:
     """Deterministic scene for a preset; dipoles=True adds
-    seeded dipole normals (NEXT-1)."""
+    seeded dipole normals (NEXT-1); detail=K adds K detail sites per face (NEXT-2)."""
     sc = _make_scene(preset, seed, variant, num_cells)
-    return add_dipoles(sc) if dipoles else sc
+    if dipoles or detail:
+        add_dipoles(sc)
+    if detail:
+        add_detail(sc, K=int(detail))
+    return sc
 
 
 def _make_scene(preset, seed, variant, num_cells):
