@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--views", type=int, default=None, help="views per GPU (default: preset)")
     ap.add_argument("--dipoles", action="store_true",
                     help="oriented-point dipole cells (NEXT-1) on the workload's foam")
+    ap.add_argument("--detail", type=int, default=0, metavar="K",
+                    help="K detail sites per dipole face (NEXT-2; implies --dipoles)")
     ap.add_argument("--fisheye", action="store_true",
                     help="equidistant fisheye cameras (NEXT-4), 200 deg image circle")
     ap.add_argument("--no-e2e", action="store_true")
@@ -164,7 +166,7 @@ def run_reference(args):
     import oracle
     import pf_synth
     wl = args.workload
-    sc = pf_synth.make_scene(wl)
+    sc = pf_synth.make_scene(wl, dipoles=args.dipoles, detail=args.detail)
     nv = args.views or default_views(wl)
     cams = workload_cameras(wl, nv, 1, 0)
     train = wl not in ("mip360_1m", "sweep64_3m")
@@ -260,7 +262,7 @@ def main():
     wl = args.workload
     nv = args.views or default_views(wl)
     t_gen = time.perf_counter()
-    sc = pf_synth.make_scene(wl, dipoles=args.dipoles)
+    sc = pf_synth.make_scene(wl, dipoles=args.dipoles, detail=args.detail)
     cams = workload_cameras(wl, nv, ws, rank)
     if args.fisheye:
         cams = [pf_synth.fisheye(c, 200.0) for c in cams]
@@ -443,7 +445,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (pf_synth seeded generator, random-init foam)",
-            "config": {"workload": wl + ("+dipoles" if args.dipoles else "") +
+            "config": {"workload": wl + ("+dipoles" if args.dipoles and not args.detail else "") +
+                                   (f"+detail{args.detail}" if args.detail else "") +
                                    ("+fisheye" if args.fisheye else ""), "cells": N,
                        "edges": sc.num_edges, "views_per_gpu": nv,
                        "global_batch_views": nv * ws, "width": W, "height": H,

@@ -92,6 +92,21 @@ typedef struct {
                                    NEXT-1): cell i is occupied only on the side its normal points
                                    away from, (x - p_i).n_i <= 0; the other half has
                                    zero density.  Non-zero, finite (not required to be unit). */
+    /* Detail sites of the dipole faces (NEXT-2, P:278-297 Eqs. svdisp/svrad);
+     * num_detail = 0 disables them.  Requires normals.  Face chart: m = n/|n|, axis k of
+     * the smallest |n_k| (ties to the higher index), u = (e_k x m)/|e_k x m|, v = m x u
+     * (SPEC S:186-189); chart coordinates q(y) = ((y-p).u, (y-p).v).  Per ray and cell:
+     * x_bar = hit of the base face (x-p).m = 0; delta = clamp(sum_k softmax_k(-tau
+     * |q(x_bar) - s_k|) d_k, -r, r); occupied half (x-p).m <= delta; x = hit of that
+     * face; radiance c(x) = sum_k softmax_k(-tau |q(x) - s_k|) sum_a softmax_a(gamma
+     * d.a_a) v_{k,a} replaces rgb_i (readings R6). */
+    int32_t num_detail;         /* K: 0, or 1..8 detail sites per cell */
+    float sv_gamma;             /* SV sharpness gamma (finite) */
+    float sv_tau;               /* soft-Voronoi temperature tau > 0 (1/world units) */
+    float sv_axes[8][3];        /* the 8 shared SV axes a_a (unit) */
+    const float *detail_uv;     /* device f32[N,K,2] s_{i,k} (world units, face chart), 8-byte aligned */
+    const float *detail_disp;   /* device f32[N,K]   d_{i,k} along m */
+    const float *detail_sv;     /* device f32[N,K,8,3] v_{i,k,a} (linear radiance), 16-byte aligned */
 } pf_scene_desc;
 
 /* Camera, OpenCV axes (x right, y down, z forward).
@@ -167,6 +182,9 @@ typedef struct {
     float *density;  /* [N]   */
     float *rgb;      /* [N,3] */
     float *normals;  /* [N,3] dL/dn_i of the dipole normals, or NULL (ignored without dipoles) */
+    float *detail_uv;   /* [N,K,2] or NULL (detail scenes; rgb receives no gradient there) */
+    float *detail_disp; /* [N,K]   or NULL */
+    float *detail_sv;   /* [N,K,8,3] or NULL; 8-byte aligned */
 } pf_grads;
 
 /* pf_render_backward with the gradient arrays in a struct (adds dL/d normals). */

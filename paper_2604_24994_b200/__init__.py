@@ -52,12 +52,17 @@ class _SceneDesc(C.Structure):
                 ("sites", C.c_void_p), ("weights", C.c_void_p), ("radii", C.c_void_p),
                 ("density", C.c_void_p), ("rgb", C.c_void_p), ("nbr_offsets", C.c_void_p),
                 ("nbr_indices", C.c_void_p), ("background", C.c_float * 3),
-                ("flags", C.c_uint32), ("normals", C.c_void_p)]
+                ("flags", C.c_uint32), ("normals", C.c_void_p),
+                ("num_detail", C.c_int32), ("sv_gamma", C.c_float), ("sv_tau", C.c_float),
+                ("sv_axes", C.c_float * 24), ("detail_uv", C.c_void_p),
+                ("detail_disp", C.c_void_p), ("detail_sv", C.c_void_p)]
 
 
 class _Grads(C.Structure):
     _fields_ = [("sites", C.c_void_p), ("weights", C.c_void_p), ("radii", C.c_void_p),
-                ("density", C.c_void_p), ("rgb", C.c_void_p), ("normals", C.c_void_p)]
+                ("density", C.c_void_p), ("rgb", C.c_void_p), ("normals", C.c_void_p),
+                ("detail_uv", C.c_void_p), ("detail_disp", C.c_void_p),
+                ("detail_sv", C.c_void_p)]
 
 
 _lib = None
@@ -153,18 +158,27 @@ class Renderer:
 
     sites f32[N,3], weights f32[N], radii f32[N], density f32[N], rgb f32[N,3],
     nbr_offsets i64[N+1], nbr_indices i32[E]: CUDA tensors on one device.
+    normals f32[N,3]: dipoles (NEXT-1).  detail: dict(uv f32[N,K,2], disp f32[N,K],
+    sv f32[N,K,8,3], axes (8x3 floats), gamma, tau) -- detail sites (NEXT-2).
     """
 
     def __init__(self, sites, weights, radii, density, rgb, nbr_offsets, nbr_indices,
                  background=(0.0, 0.0, 0.0), flags: int = 0, num_edges: int | None = None,
-                 stream=None, normals=None):
+                 stream=None, normals=None, detail=None):
         L = load_library()
         self.N = int(sites.shape[0])
         self.device = sites.device
         self.has_normals = normals is not None
+        self.detail = detail
+        self.K = 0 if detail is None else int(detail["uv"].shape[1])
         self._tensors = (sites, weights, radii, density, rgb, nbr_offsets, nbr_indices, normals)
         for t in (sites, weights, radii, density, rgb) + ((normals,) if self.has_normals else ()):
             _dev_f32(t)
+        if detail is not None:
+            K = self.K
+            _dev_f32(detail["uv"], (self.N, K, 2))
+            _dev_f32(detail["disp"], (self.N, K))
+            _dev_f32(detail["sv"], (self.N, K, 8, 3))
         if nbr_offsets.dtype != torch.int64 or nbr_indices.dtype != torch.int32:
             raise TypeError("nbr_offsets must be int64 and nbr_indices int32")
         if not (nbr_offsets.is_cuda and nbr_indices.is_cuda):
@@ -181,6 +195,15 @@ class Renderer:
             d.background[c] = float(background[c])
         d.flags = int(flags)
         d.normals = normals.data_ptr() if self.has_normals else None
+        if detail is not None:
+            d.num_detail = self.K
+            d.sv_gamma, d.sv_tau = float(detail["gamma"]), float(detail["tau"])
+            ax = [float(v) for v in torch.as_tensor(detail["axes"]).reshape(24).tolist()]
+            for q in range(24):
+                d.sv_axes[q] = ax[q]
+            d.detail_uv = detail["uv"].data_ptr()
+            d.detail_disp = detail["disp"].data_ptr()
+            d.detail_sv = detail["sv"].data_ptr()
         self.background = tuple(float(b) for b in background)
         self.flags = int(flags)
         h = C.c_void_p()
@@ -195,21 +218,48 @@ class Renderer:
         dev = torch.device(device)
         t = lambda a, dt: torch.as_tensor(a).to(device=dev, dtype=dt).contiguous()
         nrm = getattr(sc, "normals", None)
+        det = getattr(sc, "detail", None)
+        detail = None
+        if det is not None and nrm is not None:
+            detail = dict(uv=t(det.uv, torch.float32), disp=t(det.disp, torch.float32),
+                          sv=t(det.sv, torch.float32),
+                          axes=[float(v) for v in det.axes.reshape(-1)],
+                          gamma=float(det.gamma), tau=float(det.tau))
         return cls(t(sc.sites, torch.float32), t(sc.weights, torch.float32),
                    t(sc.radii, torch.float32), t(sc.density, torch.float32),
                    t(sc.rgb, torch.float32), t(sc.nbr_offsets, torch.int64),
                    t(sc.nbr_indices, torch.int32), background=sc.background, flags=flags,
-                   normals=None if nrm is None else t(nrm, torch.float32))
+                   normals=None if nrm is None else t(nrm, torch.float32), detail=detail)
 
     def sibling(self, flags: int):
         """Another handle on the same tensors (e.g. a PF_INFERENCE renderer)."""
         s, w, r, d, c, o, i, n = self._tensors
-        return Renderer(s, w, r, d, c, o, i, background=self.background, flags=flags, normals=n)
+        return Renderer(s, w, r, d, c, o, i, background=self.background, flags=flags, normals=n,
+                        detail=self.detail)
 
     @property
     def grad_size(self) -> int:
-        """Length of the flat gradient buffer: 9N, or 12N with dipole normals."""
-        return (12 if self.has_normals else 9) * self.N
+        """Length of the flat gradient buffer: 9N, 12N with dipole normals, plus 27KN
+        with K detail sites (uv 2K, disp K, sv 24K per cell)."""
+        return (12 if self.has_normals else 9) * self.N + 27 * self.K * self.N
+
+    @property
+    def param_names(self):
+        names = ["sites", "weights", "radii", "density", "rgb"]
+        if self.has_normals:
+            names.append("normals")
+        if self.K:
+            names += ["detail_uv", "detail_disp", "detail_sv"]
+        return names
+
+    def params(self):
+        s, w, r, d, c, _, _, n = self._tensors
+        p = [s, w, r, d, c]
+        if self.has_normals:
+            p.append(n)
+        if self.K:
+            p += [self.detail["uv"], self.detail["disp"], self.detail["sv"]]
+        return p
 
     # -------------------------------------------------------------- hot path
     def forward(self, cams, out=None, stream=None, stats=None):
@@ -243,6 +293,8 @@ class Renderer:
         for k in ("sites", "weights", "radii", "density", "rgb"):
             setattr(g, k, _dev_f32(views[k]).value)
         g.normals = _dev_f32(views["normals"]).value if "normals" in views else None
+        for k in ("detail_uv", "detail_disp", "detail_sv"):
+            setattr(g, k, _dev_f32(views[k]).value if k in views else None)
         _check(self._L.pf_render_backward_ex(self._h, arr, V, C.c_void_p(grad_out.data_ptr()),
                                              C.byref(g), _stream(stream)))
         return views
@@ -255,6 +307,14 @@ class Renderer:
                "rgb": flat[6 * N:9 * N].view(N, 3)}
         if self.has_normals and flat.numel() >= 12 * N:
             out["normals"] = flat[9 * N:12 * N].view(N, 3)
+        K = self.K
+        if K and flat.numel() >= self.grad_size:
+            o = 12 * N
+            out["detail_uv"] = flat[o:o + 2 * K * N].view(N, K, 2)
+            o += 2 * K * N
+            out["detail_disp"] = flat[o:o + K * N].view(N, K)
+            o += K * N
+            out["detail_sv"] = flat[o:o + 24 * K * N].view(N, K, 8, 3)
         return out
 
     # ----------------------------------------------------------- debug / stats
@@ -317,11 +377,12 @@ class Renderer:
 
 
 class _RenderFn(torch.autograd.Function):
-    """Differentiable render: inputs are the five parameter tensors; the
-    neighbour lists and cameras are non-differentiable context."""
+    """Differentiable render: inputs are the renderer's parameter tensors
+    (Renderer.params(), in param_names order); the neighbour lists and cameras
+    are non-differentiable context."""
 
     @staticmethod
-    def forward(ctx, renderer, cams, sites, weights, radii, density, rgb, normals):
+    def forward(ctx, renderer, cams, *params):
         ctx.renderer, ctx.cams = renderer, cams
         return renderer.forward(cams)
 
@@ -330,14 +391,12 @@ class _RenderFn(torch.autograd.Function):
         r = ctx.renderer
         g = torch.zeros(r.grad_size, device=r.device, dtype=torch.float32)
         v = r.backward(ctx.cams, grad_out.contiguous(), g)
-        return (None, None, v["sites"], v["weights"], v["radii"], v["density"], v["rgb"],
-                v.get("normals"))
+        return (None, None) + tuple(v[k] for k in r.param_names)
 
 
 def render(renderer: Renderer, cams):
     """Autograd-aware forward over the renderer's parameter tensors."""
-    s, w, r, d, c, _, _, n = renderer._tensors
-    return _RenderFn.apply(renderer, cams, s, w, r, d, c, n)
+    return _RenderFn.apply(renderer, cams, *renderer.params())
 
 
 # ---------------------------------------------------------------------------

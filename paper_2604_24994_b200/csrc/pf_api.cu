@@ -269,6 +269,22 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
     for (int c = 0; c < 3; ++c)
         if (!isfinite(d->background[c]))
             return fail(PF_ERR_INVALID_ARGUMENT, "background not finite");
+    if (d->num_detail != 0) {
+        if (d->num_detail < 0 || d->num_detail > pf::kMaxDetail)
+            return fail(PF_ERR_INVALID_ARGUMENT, "num_detail must be 0 or 1..8");
+        if (!d->normals)
+            return fail(PF_ERR_INVALID_ARGUMENT, "detail sites need dipole normals");
+        if (!d->detail_uv || !d->detail_disp || !d->detail_sv)
+            return fail(PF_ERR_INVALID_ARGUMENT, "a detail array pointer is NULL");
+        if (((uintptr_t)d->detail_uv & 7) || ((uintptr_t)d->detail_sv & 15))
+            return fail(PF_ERR_INVALID_ARGUMENT,
+                        "detail_uv must be 8-byte and detail_sv 16-byte aligned");
+        if (!(d->sv_tau > 0.0f) || !isfinite(d->sv_tau) || !isfinite(d->sv_gamma))
+            return fail(PF_ERR_INVALID_ARGUMENT, "sv_tau must be finite and > 0, sv_gamma finite");
+        for (int a = 0; a < 24; ++a)
+            if (!isfinite(d->sv_axes[a / 3][a % 3]))
+                return fail(PF_ERR_INVALID_ARGUMENT, "sv_axes not finite");
+    }
     cudaStream_t st = (cudaStream_t)stream;
     pf_scene *s = new (std::nothrow) pf_scene();
     if (!s) return fail(PF_ERR_OUT_OF_MEMORY, "host allocation failed");
@@ -294,6 +310,15 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
     ds.nbr_idx = d->nbr_indices;
     ds.normals = d->normals;
     for (int c = 0; c < 3; ++c) ds.bg[c] = d->background[c];
+    if (d->num_detail > 0) {
+        ds.K = d->num_detail;
+        ds.sv_gamma = d->sv_gamma;
+        ds.sv_tau = d->sv_tau;
+        for (int a = 0; a < 24; ++a) ds.sv_axes[a] = d->sv_axes[a / 3][a % 3];
+        ds.duv = d->detail_uv;
+        ds.ddisp = d->detail_disp;
+        ds.dsv = d->detail_sv;
+    }
     int rc = PF_OK;
     do {
         size_t N = (size_t)ds.N, E = (size_t)(ds.E > 0 ? ds.E : 1);
@@ -305,6 +330,10 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
         if (ds.normals) {
             if ((e = s->cellN.reserve(16 * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellN"); break; }
             ds.cellN = s->cellN.as<float4>();
+        }
+        if (ds.K) {
+            if ((e = s->cellF.reserve(sizeof(double) * pf::kCellF * N)) != cudaSuccess) { rc = cuda_fail(e, "alloc cellF"); break; }
+            ds.cellF = s->cellF.as<double>();
         }
         ds.cellA = s->cellA.as<float4>();
         ds.cellB = s->cellB.as<float4>();
@@ -330,6 +359,7 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
                 if (host & 32) why += " bad neighbour offsets;";
                 if (host & 64) why += " neighbour index out of range or self loop;";
                 if (host & 128) why += " dipole normal zero or non-finite;";
+                if (host & 256) why += " non-finite detail-site value;";
                 rc = fail(PF_ERR_INVALID_ARGUMENT, why);
                 break;
             }
@@ -357,6 +387,7 @@ int pf_destroy(pf_scene *s)
     s->cellE.release();
     s->edges.release();
     s->cellN.release();
+    s->cellF.release();
     s->keys0.release();
     s->keys1.release();
     s->vals1.release();
@@ -479,7 +510,8 @@ int pf_render_backward(pf_scene *s, const pf_camera *cams, int32_t V, const floa
                        float *grad_sites, float *grad_weights, float *grad_radii,
                        float *grad_density, float *grad_rgb, pf_stream_t stream)
 {
-    pf_grads g = {grad_sites, grad_weights, grad_radii, grad_density, grad_rgb, nullptr};
+    pf_grads g = {grad_sites, grad_weights, grad_radii, grad_density, grad_rgb, nullptr,
+                  nullptr, nullptr, nullptr};
     return pf_render_backward_ex(s, cams, V, grad_out, &g, stream);
 }
 
@@ -500,11 +532,20 @@ int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const f
     PF_CUDA(s->acc.reserve(N * 48));   // 12 floats per cell (pf_raster.cu)
     PF_CUDA(cudaMemsetAsync(s->acc.ptr, 0, N * 48, st));
     const size_t npix = (size_t)cams[0].width * cams[0].height;
-    for (int v = 0; v < V; ++v) {
+    if (s->ds.K && g->detail_sv && ((uintptr_t)g->detail_sv & 7))
+        return fail(PF_ERR_INVALID_ARGUMENT, "grads.detail_sv must be 8-byte aligned");
+    s->ds.g_uv = g->detail_uv;        // detail-site gradients go straight to the caller (+=)
+    s->ds.g_disp = g->detail_disp;
+    s->ds.g_sv = g->detail_sv;
+    int brc = PF_OK;
+    for (int v = 0; v < V && brc == PF_OK; ++v) {
         pf::ViewState &vs = s->views[v];
         if (vs.P == 0) continue;
-        PF_CUDA(pf::launch_backward(s, vs, grad_out + 4 * npix * (size_t)v, st));
+        cudaError_t e = pf::launch_backward(s, vs, grad_out + 4 * npix * (size_t)v, st);
+        if (e != cudaSuccess) brc = cuda_fail(e, "K7");
     }
+    s->ds.g_uv = s->ds.g_disp = s->ds.g_sv = nullptr;
+    if (brc != PF_OK) return brc;
     PF_CUDA(pf::launch_unpack(s, g->sites, g->weights, g->radii, g->density, g->rgb,
                               s->ds.cellN ? g->normals : nullptr, st));
     return PF_OK;

@@ -43,7 +43,16 @@ struct DeviceScene {
     uint2 *cellE = nullptr;
     const float *normals = nullptr;   // caller's dipole normals [N,3] or null
     float4 *cellN = nullptr;          // (n_i, 0) when dipoles are present
+    // detail sites (NEXT-2)
+    int K = 0;                        // detail sites per cell (0 = none)
+    float sv_gamma = 0.0f, sv_tau = 0.0f;
+    float sv_axes[24] = {};
+    const float *duv = nullptr, *ddisp = nullptr, *dsv = nullptr;
+    double *cellF = nullptr;          // per cell: m(3) u(3) v(3) |n| |e_k x m| k  (fp64)
+    float *g_uv = nullptr, *g_disp = nullptr, *g_sv = nullptr;   // backward outputs (+=)
 };
+constexpr int kMaxDetail = 8;
+constexpr int kCellF = 12;
 
 // grow-only device buffer
 struct DevBuf {
@@ -81,7 +90,7 @@ struct pf_scene {
     int device = 0;
     uint32_t flags = 0;
     pf::DeviceScene ds;
-    pf::DevBuf cellA, cellB, cellE, edges, cellN;
+    pf::DevBuf cellA, cellB, cellE, edges, cellN, cellF;
     bool edges_built = false;
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;

@@ -15,6 +15,31 @@ namespace pf {
 // ------------------------------------------------------------------------
 // K0: cell and edge records
 // ------------------------------------------------------------------------
+// Face chart of a detail cell (NEXT-2; the frame of SPEC S:186-189), fp64:
+// m = n/|n|, k = the axis of the smallest |n_k| (ties to the higher index),
+// u = (e_k x m)/|e_k x m|, v = m x u.  cellF[i] = (m, u, v, |n|, |e_k x m|, k).
+__device__ __forceinline__ void face_frame(const DeviceScene &ds, int64_t i)
+{
+    const float fx = ds.normals[3 * i], fy = ds.normals[3 * i + 1], fz = ds.normals[3 * i + 2];
+    const double nn = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
+    const double m0 = fx / nn, m1 = fy / nn, m2 = fz / nn;
+    const float ax = fabsf(fx), ay = fabsf(fy), az = fabsf(fz);
+    const int k = (ax < ay && ax < az) ? 0 : (ay <= az ? 1 : 2);
+    // w = e_k x m
+    const double w0 = k == 0 ? 0.0 : (k == 1 ? m2 : -m1);
+    const double w1 = k == 0 ? -m2 : (k == 1 ? 0.0 : m0);
+    const double w2 = k == 0 ? m1 : (k == 1 ? -m0 : 0.0);
+    const double wl = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+    const double u0 = w0 / wl, u1 = w1 / wl, u2 = w2 / wl;
+    double *F = ds.cellF + (size_t)kCellF * i;
+    F[0] = m0; F[1] = m1; F[2] = m2;
+    F[3] = u0; F[4] = u1; F[5] = u2;
+    F[6] = m1 * u2 - m2 * u1;
+    F[7] = m2 * u0 - m0 * u2;
+    F[8] = m0 * u1 - m1 * u0;
+    F[9] = nn; F[10] = wl; F[11] = (double)k;
+}
+
 __global__ void __launch_bounds__(256) k0_edge_records(DeviceScene ds)
 {
     // cell records: one thread per cell.  Edge records: the warp's 32 cells own
@@ -40,6 +65,7 @@ __global__ void __launch_bounds__(256) k0_edge_records(DeviceScene ds)
         if (ds.normals)
             ds.cellN[i] = make_float4(ds.normals[3 * i], ds.normals[3 * i + 1],
                                       ds.normals[3 * i + 2], 0.0f);
+        if (ds.K) face_frame(ds, i);
     }
     const int64_t base = __shfl_sync(0xffffffffu, ob, 0);
     const int last = (int)min((int64_t)31, ds.N - 1 - i0);
@@ -99,6 +125,12 @@ __global__ void k_validate(DeviceScene ds, int *flag)
         const float nx = ds.normals[3 * i], ny = ds.normals[3 * i + 1], nz = ds.normals[3 * i + 2];
         if (!isfinite(nx) || !isfinite(ny) || !isfinite(nz) || (nx == 0.f && ny == 0.f && nz == 0.f))
             bad |= 128;
+    }
+    for (int k = 0; k < ds.K; ++k) {
+        const size_t q = (size_t)ds.K * i + k;
+        bad |= (!isfinite(ds.duv[2 * q]) || !isfinite(ds.duv[2 * q + 1]) ||
+                !isfinite(ds.ddisp[q])) ? 256 : 0;
+        for (int a = 0; a < 24; ++a) bad |= !isfinite(ds.dsv[24 * q + a]) ? 256 : 0;
     }
     int64_t b = ds.nbr_off[i], e = ds.nbr_off[i + 1];
     if (b < 0 || e < b || e > ds.E) bad |= 32;

@@ -190,7 +190,7 @@ __device__ __forceinline__ void clip_plane(const Ray &R, const float4 E, int q, 
 template <bool kTrack, bool kDipole>
 __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__restrict__ edges,
                                               uint32_t eb, uint32_t deg, Seg &g, bool active,
-                                              const WarpStage &S, int j)
+                                              const float4 &dplane)
 {
     g.lo = -g.s;
     g.lo_q = kEndSphere;
@@ -219,8 +219,8 @@ __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__rest
         if (k + 1 < deg) clip_plane<kTrack>(R, E1, (int)k + 3, g);
         if (k + 2 < deg) clip_plane<kTrack>(R, E2, (int)k + 4, g);
     }
-    if (kDipole)  // the occupied half (x - p_i).n_i <= 0: a plane through p_i with k = 0
-        clip_plane<kTrack>(R, S.nrm[j], kEndDipole, g);
+    if (kDipole)  // the occupied half (x - p_i).n_i <= k: the dipole face (k = 0) or the
+        clip_plane<kTrack>(R, dplane, kEndDipole, g);   // displaced detail face (k = delta)
     const float dt = __fsub_rn(g.hi, g.lo);
     g.dt = (active && dt > 0.0f) ? dt : 0.0f;
 }
@@ -382,6 +382,186 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
 }
 
 // ---------------------------------------------------------------------------
+// Detail sites (NEXT-2, P:278-297 Eqs. svdisp/svrad).  Per (pixel,
+// cell): the base-face hit x_bar, its chart point, the soft-Voronoi
+// displacement delta (clamped to [-r, r]), the displaced face (m, delta) that
+// clips the interval like the plain dipole face, and the radiance at the
+// displaced-face hit x.  The chart geometry runs in fp64 from the exact ray
+// (PixelRays) and c = p - Q: at grazing incidence the chart point moves by
+// |c| eps / |d.m| per rounding, which fp32 would turn into visible colour
+// error (condition number tau r / |d.m|).  Weights, blending and the reverse
+// pass are fp32 on fp64-derived values.
+// ---------------------------------------------------------------------------
+struct DetailGeo {
+    double A, ts;     // d.m and the absolute t of the displaced-face hit
+    float delta;      // clamped displacement
+    float dr;         // unclamped soft-Voronoi displacement
+    bool parallel;    // d.m == 0: no base-face hit (reading R6e)
+};
+
+// softmax_a(gamma d.a_a) of the pixel's ray
+__device__ __forceinline__ void sv_axis_weights(const DeviceScene &ds, const Ray &R, float om[8])
+{
+    float zmax = -3.0e38f;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        om[a] = ds.sv_gamma * fmaf(R.dx, ds.sv_axes[3 * a],
+                                   fmaf(R.dy, ds.sv_axes[3 * a + 1], R.dz * ds.sv_axes[3 * a + 2]));
+        zmax = fmaxf(zmax, om[a]);
+    }
+    float sum = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        om[a] = __expf(om[a] - zmax);
+        sum += om[a];
+    }
+    const float inv = __frcp_rn(sum);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) om[a] *= inv;
+}
+
+// soft-Voronoi weights w_k = softmax_k(-tau |q - s_k|) at the fp64 chart point q;
+// rho_k - rho_min = (rho_k^2 - rho_min^2) / (rho_k + rho_min) keeps the exponent
+// differences accurate when q is far from every site.  kUnit: also the unit
+// vectors (q - s_k)/rho_k.
+template <bool kUnit>
+__device__ __forceinline__ void soft_voronoi(const float2 *__restrict__ uv, int K, double q0,
+                                             double q1, float tau, float w[kMaxDetail],
+                                             float ux[kMaxDetail], float uy[kMaxDetail])
+{
+    double r2[kMaxDetail];
+    double r2min = 1.0e300;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        r2[k] = 1.0e300;
+        if (k < K) {
+            const float2 sk = __ldg(uv + k);
+            const double dx = __dsub_rn(q0, (double)sk.x), dy = __dsub_rn(q1, (double)sk.y);
+            r2[k] = __fma_rn(dx, dx, __dmul_rn(dy, dy));
+            r2min = fmin(r2min, r2[k]);
+            if (kUnit) {
+                ux[k] = __double2float_rn(dx);
+                uy[k] = __double2float_rn(dy);
+            }
+        }
+    }
+    const float rmin = __fsqrt_rn(__double2float_rn(r2min));
+    float sum = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        w[k] = 0.0f;
+        if (k < K) {
+            const float rk = __fsqrt_rn(__double2float_rn(r2[k]));
+            const float diff = (r2[k] == r2min)
+                                   ? 0.0f
+                                   : __fdiv_rn(__double2float_rn(__dsub_rn(r2[k], r2min)),
+                                               __fadd_rn(rk, rmin));
+            w[k] = __expf(-__fmul_rn(tau, diff));
+            sum = __fadd_rn(sum, w[k]);
+            if (kUnit) {
+                const float inv = rk > 0.0f ? __frcp_rn(rk) : 0.0f;
+                ux[k] *= inv;
+                uy[k] *= inv;
+            }
+        }
+    }
+    const float inv = __frcp_rn(sum);
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) w[k] = __fmul_rn(w[k], inv);
+}
+
+// c = p - Q in fp64 (the exact site minus the exact camera centre)
+__device__ __forceinline__ void cell_c(const DeviceScene &ds, const CamParams &cam, uint32_t cell,
+                                       double c[3])
+{
+    const float4 A = __ldg(ds.cellA + cell);
+    c[0] = __dsub_rn((double)A.x, (double)cam.M[3]);
+    c[1] = __dsub_rn((double)A.y, (double)cam.M[7]);
+    c[2] = __dsub_rn((double)A.z, (double)cam.M[11]);
+}
+
+__device__ __forceinline__ double dot3d(const double a[3], double b0, double b1, double b2)
+{
+    return __fma_rn(a[0], b0, __fma_rn(a[1], b1, __dmul_rn(a[2], b2)));
+}
+
+// Eq. svdisp: base-face hit, displacement, displaced face.  Returns the face as
+// a clip plane (m, delta):  (x - p).m <= delta  <=>  a t' <= m.e + delta.
+__device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t cell,
+                                               const double d[3], const double c[3], float r,
+                                               DetailGeo &G)
+{
+    const double *F = ds.cellF + (size_t)kCellF * cell;
+    const double m0 = __ldg(F), m1 = __ldg(F + 1), m2 = __ldg(F + 2);
+    G.A = dot3d(d, m0, m1, m2);
+    const double B = dot3d(c, m0, m1, m2);
+    G.parallel = (G.A == 0.0);
+    G.delta = 0.0f;
+    G.dr = 0.0f;
+    G.ts = 0.0;
+    if (!G.parallel) {
+        const double tb = __ddiv_rn(B, G.A);
+        const double y0 = __fma_rn(tb, d[0], -c[0]), y1 = __fma_rn(tb, d[1], -c[1]),
+                     y2 = __fma_rn(tb, d[2], -c[2]);
+        const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
+        const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
+        float w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
+        const int K = ds.K;
+        soft_voronoi<false>(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
+                            ds.sv_tau, w, ux, uy);
+        const float *dk = ds.ddisp + (size_t)K * cell;
+        float dr = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k)
+            if (k < K) dr = fmaf(w[k], __ldg(dk + k), dr);
+        G.dr = dr;
+        G.delta = fminf(fmaxf(dr, -r), r);
+        G.ts = __ddiv_rn(__dadd_rn(B, (double)G.delta), G.A);
+    }
+    return make_float4(__double2float_rn(m0), __double2float_rn(m1), __double2float_rn(m2), G.delta);
+}
+
+// Eq. svrad at the point Q + t d (t = the displaced-face hit, or the interval
+// entry for a parallel ray): sum_k w_k sum_a om_a v_{k,a}
+__device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cell, const double d[3],
+                                             const double c[3], double t, const float om[8],
+                                             float &cr, float &cg, float &cb)
+{
+    const double *F = ds.cellF + (size_t)kCellF * cell;
+    const double y0 = __fma_rn(t, d[0], -c[0]), y1 = __fma_rn(t, d[1], -c[1]),
+                 y2 = __fma_rn(t, d[2], -c[2]);
+    const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
+    const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
+    float w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
+    const int K = ds.K;
+    soft_voronoi<false>(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
+                        ds.sv_tau, w, ux, uy);
+    const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
+    cr = cg = cb = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        if (k < K) {
+            float v[24];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const float4 x = __ldg(sv + 6 * k + q);
+                v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+            }
+            float kr = 0.0f, kg = 0.0f, kb = 0.0f;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                kr = fmaf(om[a], v[3 * a], kr);
+                kg = fmaf(om[a], v[3 * a + 1], kg);
+                kb = fmaf(om[a], v[3 * a + 2], kb);
+            }
+            cr = fmaf(w[k], kr, cr);
+            cg = fmaf(w[k], kg, cg);
+            cb = fmaf(w[k], kb, cb);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K6 -> K7 segment records.  For every 32-entry chunk of its tile list a warp
 // walked, K6 writes a descriptor (first record, count); for every chunk entry
 // that produced a non-empty segment in at least one lane it writes a 72-byte
@@ -420,8 +600,8 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K7_MINB
 #define PF_K7_MINB 4
 #endif
-template <bool kCount, bool kRecord, bool kDipole>
-__global__ void __launch_bounds__(256, PF_K6_MINB)
+template <bool kCount, bool kRecord, bool kDipole, bool kDetail>
+__global__ void __launch_bounds__(256, kDetail ? 2 : PF_K6_MINB)
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
            float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
@@ -444,6 +624,8 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     const uint2 rg = ranges[tile];
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     bool done = !P.valid;
+    float om[8];
+    if (kDetail) sv_axis_weights(ds, P.R, om);
     long long xs = 0, xh = 0, xp = 0, xc = 0;
     uint32_t chunks = 0;
     for (uint32_t base = rg.x; base < rg.y; base += 32, ++chunks) {
@@ -457,7 +639,19 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
-            clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, S, j);
+            float4 dpl = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            DetailGeo G;
+            double dd[3], dc[3];
+            if (kDetail) {
+                if (hit) {
+                    dd[0] = PR.dx[threadIdx.x]; dd[1] = PR.dy[threadIdx.x]; dd[2] = PR.dz[threadIdx.x];
+                    cell_c(ds, cam, S.cell[j], dc);
+                    dpl = detail_plane(ds, S.cell[j], dd, dc, S.r[j], G);
+                }
+            } else if (kDipole) {
+                dpl = S.nrm[j];
+            }
+            clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
             if (kCount && hit) {
                 ++xh;
                 xp += S.deg[j];
@@ -479,7 +673,11 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             if (seg) {
                 float alpha;
                 const float Tk = T;
-                composite_step(S.sig[j], g.dt, S.cr[j], S.cg[j], S.cb[j], T, Cr, Cg, Cb, alpha);
+                float cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
+                if (kDetail)
+                    detail_color(ds, S.cell[j], dd, dc,
+                                 G.parallel ? (double)__fadd_rn(g.tc, g.lo) : G.ts, om, cr, cg, cb);
+                composite_step(S.sig[j], g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
                 wk = __fmul_rn(Tk, alpha);
                 if (kCount) ++xc;
                 if (T < kTStop) {
@@ -548,24 +746,24 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     }
 }
 
-template <bool kDipole>
+template <bool kDipole, bool kDetail>
 static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *counters,
                              uint32_t *rec_used, float *stc, float *stn, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
     if (counters)
-        k6_forward<true, false, kDipole><<<T, 256, 0, st>>>(
+        k6_forward<true, false, kDipole, kDetail><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
             nullptr, 0u, nullptr, nullptr);
     else if (rec_used)
-        k6_forward<false, true, kDipole><<<T, 256, 0, st>>>(
+        k6_forward<false, true, kDipole, kDetail><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
             (uint32_t)v.rec_cap, stc, stn);
     else
-        k6_forward<false, false, kDipole><<<T, 256, 0, st>>>(
+        k6_forward<false, false, kDipole, kDetail><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
             stc, stn);
@@ -577,10 +775,12 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
 {
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
-    if (s->ds.cellN)
-        launch_forward_t<true>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+    if (s->ds.K)
+        launch_forward_t<true, true>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+    else if (s->ds.cellN)
+        launch_forward_t<true, false>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     else
-        launch_forward_t<false>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<false, false>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     ++s->launches;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();
@@ -602,19 +802,22 @@ struct OwnGrad {
 
 // Accumulator layout: 12 floats per cell, acc[12 i + k]:
 //   k = 0..3 (p.x, p.y, p.z, w)  4..7 (r, sigma, R, G)  8 (B)  9..11 dipole normal.
-template <bool kDipole>
+template <bool kDipole, bool kDetail>
 __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, float tprime,
                                          float wgt, float rad, const float4 *__restrict__ edges,
                                          const int32_t *__restrict__ nbr, float *acc, OwnGrad &o,
-                                         const WarpStage &S, int jslot)
+                                         const float4 &dnrm, uint32_t eb, float &g_ts)
 {
     if (q == kEndNear) return;
+    if (kDetail && q == kEndDipole) {   // the displaced face: through the detail chain
+        g_ts += wgt;
+        return;
+    }
     const float xpx = fmaf(tprime, R.dx, -g.ex), xpy = fmaf(tprime, R.dy, -g.ey),
                 xpz = fmaf(tprime, R.dz, -g.ez);   // x* - p_i
     if (kDipole && q == kEndDipole) {
         // dipole face t* = (p - Q).n / (d.n): dt/dp_i = n/a, dt/dn_i = (p_i - x*)/a
-        const float4 Nn = S.nrm[jslot];
-        const float nx = Nn.x, ny = Nn.y, nz = Nn.z;
+        const float nx = dnrm.x, ny = dnrm.y, nz = dnrm.z;
         const float a = fmaf(R.dx, nx, fmaf(R.dy, ny, __fmul_rn(R.dz, nz)));
         const float f = __fdividef(wgt, a);
         o.px = fmaf(f, nx, o.px);
@@ -633,7 +836,7 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
         o.r = fmaf(f, rad, o.r);
         return;
     }
-    const uint32_t qe = S.eb[jslot] + (uint32_t)q - 2u;   // global edge of the binding plane
+    const uint32_t qe = eb + (uint32_t)q - 2u;   // global edge of the binding plane
     const float4 E = __ldg(edges + qe);
     const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float f = __fdividef(wgt, a);
@@ -704,7 +907,7 @@ __device__ __forceinline__ void warp_reduce16_atomic(float v[16], float *acc_cel
 template <bool kDipole>
 __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restrict__ edges,
                                            uint32_t eb, uint32_t code, bool lo, const Seg &g,
-                                           int &q, const WarpStage &S, int j)
+                                           int &q, const float4 &dplane)
 {
     if (code == 0u) {
         q = kEndSphere;
@@ -717,7 +920,7 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
     float4 E;
     if (kDipole && code == 254u) {
         q = kEndDipole;
-        E = S.nrm[j];
+        E = dplane;
     } else {
         q = (int)code;                      // 2 + local plane index
         E = __ldg(edges + eb + code - 2u);
@@ -727,6 +930,252 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
     return __fmul_rn(b, rcp_approx(a));
 }
 
+// Reverse pass of one detail segment (NEXT-2): the chain of P:284-293 run
+// backwards in the order of the oracle's detail_backward.  Every lane of the
+// warp calls it (seg lanes carry values, the others zeros).  dL/dv_{k,a,c} =
+// sum over the warp's pixels of w'_k (om_a gC_c), an outer product: both factors
+// go to a [32][33] smem tile and each lane forms 6 of the K*24 sums (float2
+// atomics); dL/ds_k and dL/dd_k are column sums of the same tile refilled.
+// Own-cell geometric terms (site, normal, radius through the clamp) go into o.
+//
+// The geometric part runs in fp64: at grazing incidence the chart point is far
+// from the sites and moves radially with t*, the softmax gradient's radial
+// components cancel (sum_k dL/drho_k = 0) and what is left is multiplied by
+// |x - p| / |d.m| ~ 1/|d.m|^2; fp32 residuals of that cancellation would
+// dominate the normal's gradient.  So the weights are renormalised in fp64
+// (the zero sum then holds to 1e-16) and the unit vectors, adjoints and the
+// frame terms are fp64 too.
+struct DetailCtx {
+    double d[3], c[3];   // the exact ray direction and p - Q
+    double tcol;         // t of the radiance point
+    DetailGeo G;
+};
+
+__device__ __forceinline__ void soft_voronoi_rev(const float2 *__restrict__ uv, int K, double q0,
+                                                 double q1, float tau, double w[kMaxDetail],
+                                                 double ux[kMaxDetail], double uy[kMaxDetail])
+{
+    double r2[kMaxDetail];
+    double r2min = 1.0e300;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        r2[k] = 1.0e300;
+        ux[k] = uy[k] = 0.0;
+        if (k < K) {
+            const float2 sk = __ldg(uv + k);
+            ux[k] = q0 - (double)sk.x;
+            uy[k] = q1 - (double)sk.y;
+            r2[k] = ux[k] * ux[k] + uy[k] * uy[k];
+            r2min = fmin(r2min, r2[k]);
+        }
+    }
+    const float rmin = sqrtf((float)r2min);
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        w[k] = 0.0;
+        if (k < K) {
+            const float rk = sqrtf((float)r2[k]);
+            const float diff = (r2[k] == r2min) ? 0.0f : (float)(r2[k] - r2min) / (rk + rmin);
+            w[k] = (double)__expf(-tau * diff);
+            sum += w[k];
+            if (r2[k] > 0.0) {
+                double ri = (double)rsqrtf((float)r2[k]);
+                ri = ri * (1.5 - 0.5 * r2[k] * ri * ri);   // one Newton step: ~1e-14
+                ux[k] *= ri;
+                uy[k] *= ri;
+            }
+        }
+    }
+    const double inv = 1.0 / sum;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) w[k] *= inv;
+}
+
+__device__ __noinline__ void detail_backward(const DeviceScene &ds, uint32_t cell, bool seg,
+                                             const DetailCtx &X, float r, const float *om,
+                                             float g_ts, float gCr, float gCg, float gCb,
+                                             OwnGrad &o, float (*buf)[33], int lane)
+{
+    const int K = ds.K;
+    const float tau = ds.sv_tau;
+    const double taud = (double)tau;
+    float guv[2 * kMaxDetail], gdisp[kMaxDetail];
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) guv[2 * k] = guv[2 * k + 1] = gdisp[k] = 0.0f;
+    if (seg) {
+        const double *F = ds.cellF + (size_t)kCellF * cell;
+        const double m0 = __ldg(F), m1 = __ldg(F + 1), m2 = __ldg(F + 2);
+        const double u0 = __ldg(F + 3), u1 = __ldg(F + 4), u2 = __ldg(F + 5);
+        const double v0 = __ldg(F + 6), v1 = __ldg(F + 7), v2 = __ldg(F + 8);
+        const double d0 = X.d[0], d1 = X.d[1], d2 = X.d[2];
+        const float2 *uv = reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell;
+        // Eq. svrad at the radiance point
+        const double ys0 = X.tcol * d0 - X.c[0], ys1 = X.tcol * d1 - X.c[1],
+                     ys2 = X.tcol * d2 - X.c[2];
+        const double qs0 = ys0 * u0 + ys1 * u1 + ys2 * u2;
+        const double qs1 = ys0 * v0 + ys1 * v1 + ys2 * v2;
+        double w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
+        soft_voronoi_rev(uv, K, qs0, qs1, tau, w, ux, uy);
+        const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
+        float og[24];   // om_a gC_c
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            og[3 * a] = om[a] * gCr;
+            og[3 * a + 1] = om[a] * gCg;
+            og[3 * a + 2] = om[a] * gCb;
+        }
+        double gws[kMaxDetail], sw = 0.0;
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k) {
+            gws[k] = 0.0;
+            if (k < K) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    const float4 x = __ldg(sv + 6 * k + q);
+                    acc = fmaf(og[4 * q], x.x, acc);
+                    acc = fmaf(og[4 * q + 1], x.y, acc);
+                    acc = fmaf(og[4 * q + 2], x.z, acc);
+                    acc = fmaf(og[4 * q + 3], x.w, acc);
+                }
+                gws[k] = acc;            // c_k . gC
+                sw += w[k] * gws[k];
+            }
+            buf[lane][k] = (float)w[k];  // zero for k >= K
+        }
+#pragma unroll
+        for (int q = 0; q < 24; ++q) buf[lane][8 + q] = og[q];
+        double gq0 = 0.0, gq1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k) {
+            if (k < K) {
+                const double grho = -taud * w[k] * (gws[k] - sw);
+                gq0 += grho * ux[k];
+                gq1 += grho * uy[k];
+                guv[2 * k] -= (float)(grho * ux[k]);
+                guv[2 * k + 1] -= (float)(grho * uy[k]);
+            }
+        }
+        double gm0 = 0.0, gm1 = 0.0, gm2 = 0.0, gc0 = 0.0, gc1 = 0.0, gc2 = 0.0;
+        double gu0 = 0.0, gu1 = 0.0, gu2 = 0.0, gv0 = 0.0, gv1 = 0.0, gv2 = 0.0;
+        if (!X.G.parallel) {
+            // qs = (ys.u, ys.v)
+            const double gy0 = gq0 * u0 + gq1 * v0, gy1 = gq0 * u1 + gq1 * v1,
+                         gy2 = gq0 * u2 + gq1 * v2;
+            gu0 = gq0 * ys0; gu1 = gq0 * ys1; gu2 = gq0 * ys2;
+            gv0 = gq1 * ys0; gv1 = gq1 * ys1; gv2 = gq1 * ys2;
+            // ys = ts d - c
+            const double gts = (double)g_ts + gy0 * d0 + gy1 * d1 + gy2 * d2;
+            gc0 = -gy0; gc1 = -gy1; gc2 = -gy2;
+            // ts = (c.m + delta) / (d.m)
+            const double f = gts / X.G.A;
+            gc0 += f * m0; gc1 += f * m1; gc2 += f * m2;
+            gm0 = -f * ys0; gm1 = -f * ys1; gm2 = -f * ys2;
+            double gdr = 0.0;
+            if (X.G.dr > r) o.r += (float)f;            // delta = r
+            else if (X.G.dr < -r) o.r -= (float)f;      // delta = -r
+            else gdr = f;
+            // Eq. svdisp at the base-face hit
+            const double B = X.c[0] * m0 + X.c[1] * m1 + X.c[2] * m2;
+            const double tb = B / X.G.A;
+            const double y0 = tb * d0 - X.c[0], y1 = tb * d1 - X.c[1], y2 = tb * d2 - X.c[2];
+            const double qb0 = y0 * u0 + y1 * u1 + y2 * u2;
+            const double qb1 = y0 * v0 + y1 * v1 + y2 * v2;
+            soft_voronoi_rev(uv, K, qb0, qb1, tau, w, ux, uy);
+            const float *dk = ds.ddisp + (size_t)K * cell;
+            double dr = 0.0, dv[kMaxDetail];
+#pragma unroll
+            for (int k = 0; k < kMaxDetail; ++k) {
+                dv[k] = k < K ? (double)__ldg(dk + k) : 0.0;
+                dr += w[k] * dv[k];
+            }
+            double gb0 = 0.0, gb1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < kMaxDetail; ++k) {
+                if (k < K) {
+                    gdisp[k] = (float)(w[k] * gdr);
+                    const double grho = -taud * w[k] * gdr * (dv[k] - dr);
+                    gb0 += grho * ux[k];
+                    gb1 += grho * uy[k];
+                    guv[2 * k] -= (float)(grho * ux[k]);
+                    guv[2 * k + 1] -= (float)(grho * uy[k]);
+                }
+            }
+            const double hy0 = gb0 * u0 + gb1 * v0, hy1 = gb0 * u1 + gb1 * v1,
+                         hy2 = gb0 * u2 + gb1 * v2;
+            gu0 += gb0 * y0; gu1 += gb0 * y1; gu2 += gb0 * y2;
+            gv0 += gb1 * y0; gv1 += gb1 * y1; gv2 += gb1 * y2;
+            const double f2 = (hy0 * d0 + hy1 * d1 + hy2 * d2) / X.G.A;
+            gc0 += f2 * m0 - hy0; gc1 += f2 * m1 - hy1; gc2 += f2 * m2 - hy2;
+            gm0 -= f2 * y0; gm1 -= f2 * y1; gm2 -= f2 * y2;
+        }
+        // frame: v = m x u, u = w/|w|, w = e_k x m, m = n/|n|
+        gm0 += u1 * gv2 - u2 * gv1;           // u x gv
+        gm1 += u2 * gv0 - u0 * gv2;
+        gm2 += u0 * gv1 - u1 * gv0;
+        gu0 += gv1 * m2 - gv2 * m1;           // gv x m
+        gu1 += gv2 * m0 - gv0 * m2;
+        gu2 += gv0 * m1 - gv1 * m0;
+        const double iwl = 1.0 / __ldg(F + 10), inn = 1.0 / __ldg(F + 9);
+        const int kax = (int)__ldg(F + 11);
+        const double ug = u0 * gu0 + u1 * gu1 + u2 * gu2;
+        const double gw0 = (gu0 - u0 * ug) * iwl, gw1 = (gu1 - u1 * ug) * iwl,
+                     gw2 = (gu2 - u2 * ug) * iwl;
+        // + gw x e_k
+        if (kax == 0) { gm1 += gw2; gm2 -= gw1; }
+        else if (kax == 1) { gm0 -= gw2; gm2 += gw0; }
+        else { gm0 += gw1; gm1 -= gw0; }
+        const double mg = m0 * gm0 + m1 * gm1 + m2 * gm2;
+        o.nx += (float)((gm0 - m0 * mg) * inn);
+        o.ny += (float)((gm1 - m1 * mg) * inn);
+        o.nz += (float)((gm2 - m2 * mg) * inn);
+        o.px += (float)gc0;
+        o.py += (float)gc1;
+        o.pz += (float)gc2;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) buf[lane][q] = 0.0f;
+    }
+    __syncwarp();
+    // dL/dv: lane -> site k = lane / 4 and 6 consecutive (a, c) entries
+    {
+        const int k = lane >> 2, ac0 = (lane & 3) * 6;
+        float acc[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+            const float wk = buf[l][k];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) acc[q] = fmaf(wk, buf[l][8 + ac0 + q], acc[q]);
+        }
+        if (k < K && ds.g_sv) {
+            float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cell + k) * 24 + ac0);
+            atomicAdd(dst, make_float2(acc[0], acc[1]));
+            atomicAdd(dst + 1, make_float2(acc[2], acc[3]));
+            atomicAdd(dst + 2, make_float2(acc[4], acc[5]));
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        buf[lane][2 * k] = guv[2 * k];
+        buf[lane][2 * k + 1] = guv[2 * k + 1];
+        buf[lane][16 + k] = gdisp[k];
+    }
+    __syncwarp();
+    if (lane < 24) {
+        float t = 0.0f;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) t += buf[l][lane];
+        if (lane < 16) {
+            if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cell + lane, t);
+        } else if (lane - 16 < K && ds.g_disp) {
+            atomicAdd(ds.g_disp + (size_t)K * cell + (lane - 16), t);
+        }
+    }
+    __syncwarp();
+}
+
 // Backward of one segment (lanes with seg) + scatter of the cell's gradients.
 struct BwdPixel {
     float T, Cr, Cg, Cb;
@@ -734,16 +1183,19 @@ struct BwdPixel {
     float GT_Tfin;
 };
 
-template <bool kDipole>
+template <bool kDipole, bool kDetail>
 __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, bool seg,
                                                  const WarpStage &S, int j, BwdPixel &px,
-                                                 const DeviceScene &ds, float *acc, int lane)
+                                                 const DeviceScene &ds, float *acc, int lane,
+                                                 float cr, float cg, float cb, const float4 &dnrm,
+                                                 const DetailCtx *X, const float *om,
+                                                 float (*buf)[33])
 {
     constexpr bool dipole = kDipole;
     OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
-    float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f;
+    float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f, g_ts = 0.0f;
     if (seg) {
-        const float sig = S.sig[j], cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
+        const float sig = S.sig[j];
         const float Tk = px.T;
         float alpha;
         composite_step(sig, g.dt, cr, cg, cb, px.T, px.Cr, px.Cg, px.Cb, alpha);
@@ -762,9 +1214,17 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
         const float gdt = dtau * sig;
         if (gdt != 0.0f) {
             const float rad = S.r[j];
-            end_grad<kDipole>(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o, S, j);
-            end_grad<kDipole>(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o, S, j);
+            const uint32_t eb = S.eb[j];
+            end_grad<kDipole, kDetail>(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o,
+                                       dnrm, eb, g_ts);
+            end_grad<kDipole, kDetail>(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o,
+                                       dnrm, eb, g_ts);
         }
+    }
+    if (kDetail) {
+        // radiance gradients go to the detail sites; rgb_i is unused (gets none)
+        detail_backward(ds, S.cell[j], seg, *X, S.r[j], om, g_ts, gR, gG, gB, o, buf, lane);
+        gR = gG = gB = 0.0f;
     }
     // own-cell terms: one lane alone issues its atomics, else a transposing warp
     // reduction then one 9-lane atomic instruction
@@ -790,8 +1250,8 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
 
 }  // namespace
 
-template <bool kDipole>
-__global__ void __launch_bounds__(256, PF_K7_MINB)
+template <bool kDipole, bool kDetail>
+__global__ void __launch_bounds__(256, kDetail ? 2 : PF_K7_MINB)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
             const float4 *__restrict__ saved, const float4 *__restrict__ grad_out,
@@ -803,10 +1263,12 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
     __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
+    extern __shared__ float dyn_smem[];   // detail variant: [kWarps][32][33] reduction tiles
     const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(dyn_smem + (kDetail ? warp * 32 * 33 : 0));
     PixelSetup P;
     setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
@@ -822,6 +1284,36 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
         px.G = grad_out[pix];
     }
     px.GT_Tfin = __fmul_rn(px.G.w, px.fin.w);
+    float om[8];
+    if (kDetail) sv_axis_weights(ds, P.R, om);
+    DetailCtx X;
+    if (kDetail) {
+        X.d[0] = PR.dx[threadIdx.x];
+        X.d[1] = PR.dy[threadIdx.x];
+        X.d[2] = PR.dz[threadIdx.x];
+    }
+    // per entry: the dipole face (plain: the staged normal; detail: the lane's
+    // displaced face) and the segment colour
+    auto prepare = [&](int j, bool active, float4 &dpl, float &cr, float &cg, float &cb) {
+        cr = S.cr[j];
+        cg = S.cg[j];
+        cb = S.cb[j];
+        dpl = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (kDetail) {
+            if (active) {
+                cell_c(ds, cam, S.cell[j], X.c);
+                dpl = detail_plane(ds, S.cell[j], X.d, X.c, S.r[j], X.G);
+            }
+        } else if (kDipole) {
+            dpl = S.nrm[j];
+        }
+    };
+    auto shade = [&](int j, const Seg &g, bool seg, float &cr, float &cg, float &cb) {
+        if (kDetail && seg) {
+            X.tcol = X.G.parallel ? (double)__fadd_rn(g.tc, g.lo) : X.G.ts;
+            detail_color(ds, S.cell[j], X.d, X.c, X.tcol, om, cr, cg, cb);
+        }
+    };
     const uint32_t nchunks = wdone[(size_t)tile * kWarps + warp];
     const uint32_t c0 = chunk_off[tile];
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -838,10 +1330,15 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 bool hit = false;
                 if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
                 if (!__any_sync(0xffffffffu, hit)) continue;
-                clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, S, j);
+                float4 dpl;
+                float cr, cg, cb;
+                prepare(j, hit, dpl, cr, cg, cb);
+                clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
                 const bool seg = g.dt > 0.0f;
                 if (!__any_sync(0xffffffffu, seg)) continue;
-                segment_backward<kDipole>(P.R, g, seg, S, j, px, ds, acc, lane);
+                shade(j, g, seg, cr, cg, cb);
+                segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb,
+                                                   dpl, &X, om, buf);
                 if (seg && px.T < kTStop) done = true;
             }
             __syncwarp();
@@ -869,45 +1366,59 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const int j = (int)k;
             Seg g;
             g.dt = 0.0f;
+            float4 dpl;
+            float cr, cg, cb;
+            if (seg) sphere_hit(P.R, S, j, g, ds, cam, PR);   // identical to K6 (recorded hit)
+            prepare(j, seg, dpl, cr, cg, cb);
             if (seg) {
-                sphere_hit(P.R, S, j, g, ds, cam, PR);   // identical to K6 (recorded hit)
                 const uint32_t eb = S.eb[j];
-                g.lo = coded_end<kDipole>(P.R, ds.edges, eb, code & 0xffu, true, g, g.lo_q, S, j);
-                g.hi = coded_end<kDipole>(P.R, ds.edges, eb, code >> 8, false, g, g.hi_q, S, j);
+                g.lo = coded_end<kDipole>(P.R, ds.edges, eb, code & 0xffu, true, g, g.lo_q, dpl);
+                g.hi = coded_end<kDipole>(P.R, ds.edges, eb, code >> 8, false, g, g.hi_q, dpl);
             }
             const bool full = seg && (((code & 0xffu) == 255u) || ((code >> 8) == 255u));
             if (__any_sync(0xffffffffu, full)) {
                 Seg h = g;
                 if (full) {
-                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], h, true, S, j);
+                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], h, true, dpl);
                     g = h;
                 } else {
-                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], h, false, S, j);
+                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], h, false, dpl);
                 }
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
-            segment_backward<kDipole>(P.R, g, seg, S, j, px, ds, acc, lane);
+            shade(j, g, seg, cr, cg, cb);
+            segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb, dpl,
+                                               &X, om, buf);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();
     }
 }
 
+template <bool kDipole, bool kDetail>
+static void launch_backward_t(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
+{
+    const int T = v.cam.tiles_x * v.cam.tiles_y;
+    constexpr int smem = kDetail ? kWarps * 32 * 33 * (int)sizeof(float) : 0;
+    if (kDetail)
+        cudaFuncSetAttribute(k7_backward<kDipole, kDetail>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k7_backward<kDipole, kDetail><<<T, 256, smem, st>>>(
+        s->ds, v.cam, v.ranges_p, v.order, v.vals_p, v.saved.as<float4>(),
+        (const float4 *)grad_out, s->acc.as<float>(), v.chunk_off, v.desc.as<uint2>(),
+        v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
+}
+
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
 {
-    int T = v.cam.tiles_x * v.cam.tiles_y;
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    if (s->ds.cellN)
-        k7_backward<true><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
-                                             v.saved.as<float4>(), (const float4 *)grad_out,
-                                             s->acc.as<float>(), v.chunk_off, v.desc.as<uint2>(),
-                                             v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
+    if (s->ds.K)
+        launch_backward_t<true, true>(s, v, grad_out, st);
+    else if (s->ds.cellN)
+        launch_backward_t<true, false>(s, v, grad_out, st);
     else
-        k7_backward<false><<<T, 256, 0, st>>>(s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
-                                              v.saved.as<float4>(), (const float4 *)grad_out,
-                                              s->acc.as<float>(), v.chunk_off, v.desc.as<uint2>(),
-                                              v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
+        launch_backward_t<false, false>(s, v, grad_out, st);
     ++s->launches;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();

@@ -41,6 +41,10 @@ def case(name, variant=None):
         elif name == "train8_1m":
             sc = pf_synth.make_scene("train8_1m")
             cams = pf_synth.make_cameras("train8_1m")
+        elif name.endswith("+detail"):
+            base, bcams = case(name[:-len("+detail")], variant)
+            sc = pf_synth.add_detail(base.copy())
+            cams = bcams
         elif name.endswith("+dipoles"):
             base, bcams = case(name[:-len("+dipoles")], variant)
             sc = pf_synth.add_dipoles(base.copy())
@@ -60,6 +64,7 @@ def grad_check(gpu, ref, tol=GRAD_TOL):
     msgs = []
     keys = ("sites", "weights", "radii", "density", "rgb") + (("normals",) if "normals" in ref
                                                                else ())
+    keys += tuple(k for k in ("detail_uv", "detail_disp", "detail_sv") if k in ref)
     for k in keys:
         a = gpu[k].detach().cpu().numpy().astype(np.float64).reshape(-1)
         b = ref[k].reshape(-1)
@@ -447,7 +452,8 @@ def test_fisheye_binning_matches_oracle(name, variant):
 
 
 @pytest.mark.parametrize("name,variant", [("tiny", "outside"), ("tiny", "inside"),
-                                          ("small360", None), ("small+dipoles", None)])
+                                          ("small360", None), ("small+dipoles", None),
+                                          ("small+detail", None)])
 def test_fisheye_forward_backward(name, variant):
     sc, cams = _fisheye_case(name, variant)
     r = renderer(sc)
@@ -465,3 +471,112 @@ def test_fisheye_forward_backward(name, variant):
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
     grad_check(got, ref)
     r.close()
+
+
+# --------------------------------------------------------------- NEXT-2: detail sites
+
+def _full_parity(sc, cams, mode, seed):
+    r = renderer(sc)
+    H, W = cams[0].height, cams[0].width
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    for v, cam in enumerate(cams):
+        ref = oracle.render(sc, cam, mode=mode)["out"]
+        assert np.abs(out[v] - ref).max() <= IMG_TOL
+    g = pf_synth.make_grad_out(len(cams), H, W, seed=seed)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    ref = None
+    for v, cam in enumerate(cams):
+        o = oracle.backward(sc, cam, g[v], mode=mode)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    msgs = grad_check(got, ref)
+    r.close()
+    return msgs
+
+
+@pytest.mark.parametrize("name,variant", [("tiny+detail", "outside"), ("tiny+detail", "inside"),
+                                          ("small+detail", None), ("small360+detail", None)])
+def test_detail_forward_and_backward_full_image(name, variant):
+    sc, cams = case(name, variant)
+    mode = oracle.O1 if name.startswith("tiny") else oracle.O3
+    _full_parity(sc, cams[:2], mode, seed=19)
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_detail_fewer_sites(K):
+    sc, cams = case("small")
+    sc = pf_synth.add_detail(sc.copy(), K=K, seed=5)
+    _full_parity(sc, cams[:1], oracle.O3, seed=21)
+
+
+def test_detail_large_sampled_pixels():
+    sc, cams = case("nerfsynth200k+detail")
+    r = renderer(sc, flags=0)
+    H, W = cams[0].height, cams[0].width
+    rng = np.random.default_rng(4)
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    g = np.zeros((len(cams), H, W, 4), np.float32)
+    pix = {}
+    for v in (0, len(cams) - 1):
+        p = np.unique(np.stack([rng.integers(0, W, 1200), rng.integers(0, H, 1200)], 1), axis=0)
+        pix[v] = p
+        ref = oracle.render(sc, cams[v], mode=oracle.O3, pixels=p)["out"]
+        assert np.abs(out[v][p[:, 1], p[:, 0]] - ref).max() <= IMG_TOL
+        g[v, p[:, 1], p[:, 0]] = rng.standard_normal((p.shape[0], 4)).astype(np.float32)
+    r.forward(cams)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    ref = None
+    for v, p in pix.items():
+        o = oracle.backward(sc, cams[v], g[v, p[:, 1], p[:, 0]], mode=oracle.O3, pixels=p)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+
+
+def test_detail_record_overflow_fallback(monkeypatch):
+    monkeypatch.setenv("PF_REC_RATIO", "0.02")
+    sc, cams = case("small360+detail")
+    _full_parity(sc, cams[:1], oracle.O3, seed=23)
+
+
+def test_detail_autograd_and_by_products():
+    """torch.autograd through the detail parameters equals the explicit backward;
+    by-products (sum T alpha) match the oracle's."""
+    import paper_2604_24994_b200 as pf
+    sc, cams = case("small+detail")
+    r = renderer(sc)
+    params = [p.detach().clone().requires_grad_(True) for p in r.params()]
+    r2 = pf.Renderer(params[0], params[1], params[2], params[3], params[4],
+                     *r._tensors[5:7], background=sc.background, normals=params[5],
+                     detail=dict(r.detail, uv=params[6], disp=params[7], sv=params[8]))
+    out = pf.render(r2, cams[:1])
+    g = torch.from_numpy(pf_synth.make_grad_out(1, cams[0].height, cams[0].width, seed=3)).cuda()
+    (out * g).sum().backward()
+    ref = oracle.backward(sc, cams[0], g[0].cpu().numpy(), mode=oracle.O3)
+    grad_check(dict(zip(r2.param_names, [p.grad for p in params])), ref)
+    N = sc.num_cells
+    st = {"contrib": torch.zeros(N, device="cuda"), "normal": torch.zeros(N, device="cuda")}
+    r.forward(cams[:1], stats=st)
+    o = oracle.cell_stats(sc, cams[0], mode=oracle.O3)
+    c = st["contrib"].double().cpu().numpy()
+    assert np.linalg.norm(c - o["contrib"]) <= 1e-4 * np.linalg.norm(o["contrib"])
+    r.close(); r2.close()
+
+
+def test_detail_abi_errors():
+    import paper_2604_24994_b200 as pf
+    sc, _ = case("tiny+detail", "outside")
+    base = pf.Renderer.from_scene(sc, "cuda")
+    s, w, rr, d, c, o, i, n = base._tensors
+    det = base.detail
+    with pytest.raises(pf.PFError):       # detail without normals
+        pf.Renderer(s, w, rr, d, c, o, i, detail=det)
+    with pytest.raises(pf.PFError):       # tau <= 0
+        pf.Renderer(s, w, rr, d, c, o, i, normals=n, detail=dict(det, tau=0.0))
+    bad = sc.copy()
+    bad.detail.sv[3, 2, 1, 0] = np.nan
+    with pytest.raises(pf.PFError):       # PF_VALIDATE catches non-finite detail values
+        renderer(bad)
+    sv_off = torch.zeros(det["sv"].numel() + 1, device="cuda")[1:].view(det["sv"].shape)
+    with pytest.raises(pf.PFError):       # misaligned (float4 loads need 16-byte alignment)
+        pf.Renderer(s, w, rr, d, c, o, i, normals=n, detail=dict(det, sv=sv_off))
+    base.close()

@@ -262,11 +262,12 @@ def test_modes_agree_and_theorem2(variant):
     assert (r1["out"][..., 3] < 0.99).mean() > 0.05
 
 
-def test_backward_fd():
+@pytest.mark.parametrize("variant", ["inside", "outside"])
+def test_backward_fd(variant):
     """Central differences of L = <g, out> w.r.t. every parameter family, where the
     active set (signature) is unchanged by the step."""
     sc = _detail_scene()
-    cam = pf_synth.make_cameras("tiny", variant="inside")[0]
+    cam = pf_synth.make_cameras("tiny", variant=variant)[0]
     g = pf_synth.make_grad_out(1, cam.height, cam.width, seed=8)[0] * (cam.height * cam.width)
     an = oracle.backward(sc, cam, g, mode=oracle.O2)
 
