@@ -420,54 +420,55 @@ __device__ __forceinline__ void sv_axis_weights(const DeviceScene &ds, const Ray
     for (int a = 0; a < 8; ++a) om[a] *= inv;
 }
 
-// soft-Voronoi weights w_k = softmax_k(-tau |q - s_k|) at the fp64 chart point q;
-// rho_k - rho_min = (rho_k^2 - rho_min^2) / (rho_k + rho_min) keeps the exponent
-// differences accurate when q is far from every site.  kUnit: also the unit
-// vectors (q - s_k)/rho_k.
-template <bool kUnit>
-__device__ __forceinline__ void soft_voronoi(const float2 *__restrict__ uv, int K, double q0,
-                                             double q1, float tau, float w[kMaxDetail],
-                                             float ux[kMaxDetail], float uy[kMaxDetail])
+__device__ __forceinline__ float sqrt_approx(float x)
 {
-    double r2[kMaxDetail];
-    double r2min = 1.0e300;
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// soft-Voronoi weights w_k = softmax_k(-tau |q - s_k|) at the chart point q
+// (fp64 in, fp32 arithmetic).  Exponents relative to the nearest site j:
+// rho_k - rho_j = (s_j - s_k).(2q - s_k - s_j) / (rho_k + rho_j), which keeps
+// full relative precision when q is far from every site (grazing rays), where
+// rho_k - rho_j from two rounded distances would not.
+__device__ __forceinline__ void soft_voronoi(const float2 *__restrict__ uv, int K, double q0d,
+                                             double q1d, float tau, float w[kMaxDetail])
+{
+    const float q0 = __double2float_rn(q0d), q1 = __double2float_rn(q1d);
+    float sx[kMaxDetail], sy[kMaxDetail], r2[kMaxDetail];
+    float r2m = 3.0e38f, jx = 0.0f, jy = 0.0f;
 #pragma unroll
     for (int k = 0; k < kMaxDetail; ++k) {
-        r2[k] = 1.0e300;
         if (k < K) {
             const float2 sk = __ldg(uv + k);
-            const double dx = __dsub_rn(q0, (double)sk.x), dy = __dsub_rn(q1, (double)sk.y);
-            r2[k] = __fma_rn(dx, dx, __dmul_rn(dy, dy));
-            r2min = fmin(r2min, r2[k]);
-            if (kUnit) {
-                ux[k] = __double2float_rn(dx);
-                uy[k] = __double2float_rn(dy);
+            sx[k] = sk.x;
+            sy[k] = sk.y;
+            const float dx = q0 - sk.x, dy = q1 - sk.y;
+            r2[k] = fmaf(dx, dx, dy * dy);
+            if (r2[k] < r2m) {
+                r2m = r2[k];
+                jx = sk.x;
+                jy = sk.y;
             }
         }
     }
-    const float rmin = __fsqrt_rn(__double2float_rn(r2min));
+    const float rj = sqrt_approx(r2m), tx = fmaf(2.0f, q0, -jx), ty = fmaf(2.0f, q1, -jy);
     float sum = 0.0f;
 #pragma unroll
     for (int k = 0; k < kMaxDetail; ++k) {
         w[k] = 0.0f;
         if (k < K) {
-            const float rk = __fsqrt_rn(__double2float_rn(r2[k]));
-            const float diff = (r2[k] == r2min)
-                                   ? 0.0f
-                                   : __fdiv_rn(__double2float_rn(__dsub_rn(r2[k], r2min)),
-                                               __fadd_rn(rk, rmin));
-            w[k] = __expf(-__fmul_rn(tau, diff));
-            sum = __fadd_rn(sum, w[k]);
-            if (kUnit) {
-                const float inv = rk > 0.0f ? __frcp_rn(rk) : 0.0f;
-                ux[k] *= inv;
-                uy[k] *= inv;
-            }
+            const float num = fmaf(jx - sx[k], tx - sx[k], (jy - sy[k]) * (ty - sy[k]));
+            const float den = sqrt_approx(r2[k]) + rj;
+            const float diff = den > 0.0f ? num * rcp_approx(den) : 0.0f;
+            w[k] = __expf(-tau * diff);
+            sum += w[k];
         }
     }
-    const float inv = __frcp_rn(sum);
+    const float inv = rcp_approx(sum);
 #pragma unroll
-    for (int k = 0; k < kMaxDetail; ++k) w[k] = __fmul_rn(w[k], inv);
+    for (int k = 0; k < kMaxDetail; ++k) w[k] *= inv;
 }
 
 // c = p - Q in fp64 (the exact site minus the exact camera centre)
@@ -505,10 +506,10 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
                      y2 = __fma_rn(tb, d[2], -c[2]);
         const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
         const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
-        float w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
+        float w[kMaxDetail];
         const int K = ds.K;
-        soft_voronoi<false>(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
-                            ds.sv_tau, w, ux, uy);
+        soft_voronoi(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
+                     ds.sv_tau, w);
         const float *dk = ds.ddisp + (size_t)K * cell;
         float dr = 0.0f;
 #pragma unroll
@@ -532,10 +533,10 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
                  y2 = __fma_rn(t, d[2], -c[2]);
     const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
     const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
-    float w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
+    float w[kMaxDetail];
     const int K = ds.K;
-    soft_voronoi<false>(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
-                        ds.sv_tau, w, ux, uy);
+    soft_voronoi(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
+                 ds.sv_tau, w);
     const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
     cr = cg = cb = 0.0f;
 #pragma unroll
@@ -600,6 +601,9 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K7_MINB
 #define PF_K7_MINB 4
 #endif
+#ifndef PF_K7D_MINB
+#define PF_K7D_MINB 2
+#endif
 template <bool kCount, bool kRecord, bool kDipole, bool kDetail>
 __global__ void __launch_bounds__(256, kDetail ? 2 : PF_K6_MINB)
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
@@ -643,15 +647,24 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             DetailGeo G;
             double dd[3], dc[3];
             if (kDetail) {
-                if (hit) {
-                    dd[0] = PR.dx[threadIdx.x]; dd[1] = PR.dy[threadIdx.x]; dd[2] = PR.dz[threadIdx.x];
-                    cell_c(ds, cam, S.cell[j], dc);
-                    dpl = detail_plane(ds, S.cell[j], dd, dc, S.r[j], G);
+                // neighbour planes first; the displaced face (its chart evaluation is
+                // the expensive part) only where the interval is still non-empty
+                clip_interval<kRecord, false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
+                const bool pre = g.dt > 0.0f;
+                if (__any_sync(0xffffffffu, pre)) {
+                    if (pre) {
+                        dd[0] = PR.dx[threadIdx.x]; dd[1] = PR.dy[threadIdx.x]; dd[2] = PR.dz[threadIdx.x];
+                        cell_c(ds, cam, S.cell[j], dc);
+                        dpl = detail_plane(ds, S.cell[j], dd, dc, S.r[j], G);
+                    }
+                    clip_plane<kRecord>(P.R, dpl, kEndDipole, g);
+                    const float dt = __fsub_rn(g.hi, g.lo);
+                    g.dt = (pre && dt > 0.0f) ? dt : 0.0f;
                 }
-            } else if (kDipole) {
-                dpl = S.nrm[j];
+            } else {
+                if (kDipole) dpl = S.nrm[j];
+                clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
             }
-            clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
             if (kCount && hit) {
                 ++xh;
                 xp += S.deg[j];
@@ -930,13 +943,15 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
     return __fmul_rn(b, rcp_approx(a));
 }
 
-// Reverse pass of one detail segment (NEXT-2): the chain of P:284-293 run
-// backwards in the order of the oracle's detail_backward.  Every lane of the
-// warp calls it (seg lanes carry values, the others zeros).  dL/dv_{k,a,c} =
-// sum over the warp's pixels of w'_k (om_a gC_c), an outer product: both factors
-// go to a [32][33] smem tile and each lane forms 6 of the K*24 sums (float2
-// atomics); dL/ds_k and dL/dd_k are column sums of the same tile refilled.
-// Own-cell geometric terms (site, normal, radius through the clamp) go into o.
+// Backward of one detail segment (NEXT-2), fused: radiance at the displaced-face
+// hit (Eq. svrad; colour and c_k . G in one pass over the SV values), the
+// compositing replay of the segment, the interval-end derivatives, then the
+// chain of P:284-293 run backwards in the order of the oracle's
+// detail_backward.  Every lane of the warp calls it (seg lanes carry values).
+// dL/dv_{k,a,c} = sum over the warp's pixels of w'_k (om_a gC_c), an outer
+// product: both factors go to a [32][33] smem tile and each lane forms 6 of the
+// K*24 sums over the seg lanes (float2 atomics); dL/ds_k and dL/dd_k are
+// column sums of the same tile refilled.
 //
 // The geometric part runs in fp64: at grazing incidence the chart point is far
 // from the sites and moves radially with t*, the softmax gradient's radial
@@ -947,59 +962,53 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
 // frame terms are fp64 too.
 struct DetailCtx {
     double d[3], c[3];   // the exact ray direction and p - Q
-    double tcol;         // t of the radiance point
     DetailGeo G;
 };
 
-__device__ __forceinline__ void soft_voronoi_rev(const float2 *__restrict__ uv, int K, double q0,
-                                                 double q1, float tau, double w[kMaxDetail],
-                                                 double ux[kMaxDetail], double uy[kMaxDetail])
+// unit vectors (q - s_k)/rho_k: fp64 (rsqrt + one Newton step, ~1e-14) or fp32
+template <typename T>
+__device__ __forceinline__ void sv_units(const float2 *__restrict__ uv, int K, double q0, double q1,
+                                         T ux[kMaxDetail], T uy[kMaxDetail])
 {
-    double r2[kMaxDetail];
-    double r2min = 1.0e300;
 #pragma unroll
     for (int k = 0; k < kMaxDetail; ++k) {
-        r2[k] = 1.0e300;
-        ux[k] = uy[k] = 0.0;
+        ux[k] = uy[k] = (T)0;
         if (k < K) {
             const float2 sk = __ldg(uv + k);
-            ux[k] = q0 - (double)sk.x;
-            uy[k] = q1 - (double)sk.y;
-            r2[k] = ux[k] * ux[k] + uy[k] * uy[k];
-            r2min = fmin(r2min, r2[k]);
-        }
-    }
-    const float rmin = sqrtf((float)r2min);
-    double sum = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMaxDetail; ++k) {
-        w[k] = 0.0;
-        if (k < K) {
-            const float rk = sqrtf((float)r2[k]);
-            const float diff = (r2[k] == r2min) ? 0.0f : (float)(r2[k] - r2min) / (rk + rmin);
-            w[k] = (double)__expf(-tau * diff);
-            sum += w[k];
-            if (r2[k] > 0.0) {
-                double ri = (double)rsqrtf((float)r2[k]);
-                ri = ri * (1.5 - 0.5 * r2[k] * ri * ri);   // one Newton step: ~1e-14
-                ux[k] *= ri;
-                uy[k] *= ri;
+            const T dx = (T)(q0 - (double)sk.x), dy = (T)(q1 - (double)sk.y);
+            const T r2 = dx * dx + dy * dy;
+            if (r2 > (T)0) {
+                T ri = (T)rsqrtf((float)r2);
+                if (sizeof(T) == 8) ri = ri * ((T)1.5 - (T)0.5 * r2 * ri * ri);
+                ux[k] = dx * ri;
+                uy[k] = dy * ri;
             }
         }
     }
-    const double inv = 1.0 / sum;
-#pragma unroll
-    for (int k = 0; k < kMaxDetail; ++k) w[k] *= inv;
 }
 
-__device__ __noinline__ void detail_backward(const DeviceScene &ds, uint32_t cell, bool seg,
-                                             const DetailCtx &X, float r, const float *om,
-                                             float g_ts, float gCr, float gCg, float gCb,
-                                             OwnGrad &o, float (*buf)[33], int lane)
+struct BwdPixel {
+    float T, Cr, Cg, Cb;
+    float4 fin, G;
+    float GT_Tfin;
+};
+
+#ifdef PF_DETAIL_NOINLINE   // A/B knob (inlined measured 20% faster: no call-boundary spills)
+#define PF_DETAIL_FN __noinline__
+#else
+#define PF_DETAIL_FN __forceinline__
+#endif
+template <typename T>
+__device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg,
+                                            const WarpStage &S, int j, BwdPixel &px,
+                                            const DeviceScene &ds, float *acc, int lane,
+                                            const DetailCtx &X, const float *om, float (*buf)[33])
 {
     const int K = ds.K;
+    const uint32_t cell = S.cell[j];
     const float tau = ds.sv_tau;
-    const double taud = (double)tau;
+    OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
+    float gs = 0.0f;
     float guv[2 * kMaxDetail], gdisp[kMaxDetail];
 #pragma unroll
     for (int k = 0; k < kMaxDetail; ++k) guv[2 * k] = guv[2 * k + 1] = gdisp[k] = 0.0f;
@@ -1010,149 +1019,197 @@ __device__ __noinline__ void detail_backward(const DeviceScene &ds, uint32_t cel
         const double v0 = __ldg(F + 6), v1 = __ldg(F + 7), v2 = __ldg(F + 8);
         const double d0 = X.d[0], d1 = X.d[1], d2 = X.d[2];
         const float2 *uv = reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell;
-        // Eq. svrad at the radiance point
-        const double ys0 = X.tcol * d0 - X.c[0], ys1 = X.tcol * d1 - X.c[1],
-                     ys2 = X.tcol * d2 - X.c[2];
+        // ---- forward: Eq. svrad at x (the interval entry for a parallel ray)
+        const double tcol = X.G.parallel ? (double)__fadd_rn(g.tc, g.lo) : X.G.ts;
+        const double ys0 = tcol * d0 - X.c[0], ys1 = tcol * d1 - X.c[1], ys2 = tcol * d2 - X.c[2];
         const double qs0 = ys0 * u0 + ys1 * u1 + ys2 * u2;
         const double qs1 = ys0 * v0 + ys1 * v1 + ys2 * v2;
-        double w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
-        soft_voronoi_rev(uv, K, qs0, qs1, tau, w, ux, uy);
+        float ws[kMaxDetail], dG[kMaxDetail];
+        soft_voronoi(uv, K, qs0, qs1, tau, ws);
         const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
-        float og[24];   // om_a gC_c
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            og[3 * a] = om[a] * gCr;
-            og[3 * a + 1] = om[a] * gCg;
-            og[3 * a + 2] = om[a] * gCb;
-        }
-        double gws[kMaxDetail], sw = 0.0;
+        float cr = 0.0f, cg = 0.0f, cb = 0.0f;
 #pragma unroll
         for (int k = 0; k < kMaxDetail; ++k) {
-            gws[k] = 0.0;
+            dG[k] = 0.0f;
             if (k < K) {
-                float acc = 0.0f;
+                float v[24];
 #pragma unroll
                 for (int q = 0; q < 6; ++q) {
                     const float4 x = __ldg(sv + 6 * k + q);
-                    acc = fmaf(og[4 * q], x.x, acc);
-                    acc = fmaf(og[4 * q + 1], x.y, acc);
-                    acc = fmaf(og[4 * q + 2], x.z, acc);
-                    acc = fmaf(og[4 * q + 3], x.w, acc);
+                    v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
                 }
-                gws[k] = acc;            // c_k . gC
-                sw += w[k] * gws[k];
-            }
-            buf[lane][k] = (float)w[k];  // zero for k >= K
-        }
+                float kr = 0.0f, kg = 0.0f, kb = 0.0f;
 #pragma unroll
-        for (int q = 0; q < 24; ++q) buf[lane][8 + q] = og[q];
-        double gq0 = 0.0, gq1 = 0.0;
+                for (int a = 0; a < 8; ++a) {
+                    kr = fmaf(om[a], v[3 * a], kr);
+                    kg = fmaf(om[a], v[3 * a + 1], kg);
+                    kb = fmaf(om[a], v[3 * a + 2], kb);
+                }
+                cr = fmaf(ws[k], kr, cr);
+                cg = fmaf(ws[k], kg, cg);
+                cb = fmaf(ws[k], kb, cb);
+                dG[k] = fmaf(kr, px.G.x, fmaf(kg, px.G.y, kb * px.G.z));   // c_k . G
+            }
+        }
+        // ---- compositing replay (as segment_backward)
+        const float sig = S.sig[j];
+        const float Tk = px.T;
+        float alpha;
+        composite_step(sig, g.dt, cr, cg, cb, px.T, px.Cr, px.Cg, px.Cb, alpha);
+        const float Sr = __fsub_rn(px.fin.x, px.Cr), Sg = __fsub_rn(px.fin.y, px.Cg),
+                    Sb = __fsub_rn(px.fin.z, px.Cb);
+        float dtau = -px.GT_Tfin;
+        dtau = fmaf(px.G.x, fmaf(px.T, cr, -Sr), dtau);
+        dtau = fmaf(px.G.y, fmaf(px.T, cg, -Sg), dtau);
+        dtau = fmaf(px.G.z, fmaf(px.T, cb, -Sb), dtau);
+        const float wa = __fmul_rn(Tk, alpha);
+        gs = dtau * g.dt;
+        const float gdt = dtau * sig;
+        float g_ts = 0.0f;
+        if (gdt != 0.0f) {
+            const float4 none = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            end_grad<true, true>(R, g, g.hi_q, g.hi, gdt, S.r[j], ds.edges, ds.nbr_idx, acc, o,
+                                 none, S.eb[j], g_ts);
+            end_grad<true, true>(R, g, g.lo_q, g.lo, -gdt, S.r[j], ds.edges, ds.nbr_idx, acc, o,
+                                 none, S.eb[j], g_ts);
+        }
+        // ---- reverse of Eq. svrad: dL/dc = wa G
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k) buf[lane][k] = ws[k];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const float oa = om[a] * wa;
+            buf[lane][8 + 3 * a] = oa * px.G.x;
+            buf[lane][9 + 3 * a] = oa * px.G.y;
+            buf[lane][10 + 3 * a] = oa * px.G.z;
+        }
+        const T tm0 = (T)m0, tm1 = (T)m1, tm2 = (T)m2, tu0 = (T)u0, tu1 = (T)u1, tu2 = (T)u2;
+        const T tv0 = (T)v0, tv1 = (T)v1, tv2 = (T)v2, td0 = (T)d0, td1 = (T)d1, td2 = (T)d2;
+        const T tA = (T)X.G.A, ttau = (T)tau;
+        T w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
+        T wsum = 0, sw = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k) {
+            w[k] = (T)ws[k];
+            wsum += w[k];
+            sw += w[k] * (T)dG[k];
+        }
+        sw /= wsum;   // renormalised: sum_k w_k (dG_k - sw) = 0 to working-precision rounding
+        sv_units<T>(uv, K, qs0, qs1, ux, uy);
+        T gq0 = 0, gq1 = 0;
 #pragma unroll
         for (int k = 0; k < kMaxDetail; ++k) {
             if (k < K) {
-                const double grho = -taud * w[k] * (gws[k] - sw);
+                const T grho = -ttau * (T)wa * (w[k] / wsum) * ((T)dG[k] - sw);
                 gq0 += grho * ux[k];
                 gq1 += grho * uy[k];
                 guv[2 * k] -= (float)(grho * ux[k]);
                 guv[2 * k + 1] -= (float)(grho * uy[k]);
             }
         }
-        double gm0 = 0.0, gm1 = 0.0, gm2 = 0.0, gc0 = 0.0, gc1 = 0.0, gc2 = 0.0;
-        double gu0 = 0.0, gu1 = 0.0, gu2 = 0.0, gv0 = 0.0, gv1 = 0.0, gv2 = 0.0;
+        T gm0 = 0, gm1 = 0, gm2 = 0, gc0 = 0, gc1 = 0, gc2 = 0;
+        T gu0 = 0, gu1 = 0, gu2 = 0, gv0 = 0, gv1 = 0, gv2 = 0;
         if (!X.G.parallel) {
+            const T s0 = (T)ys0, s1 = (T)ys1, s2 = (T)ys2;
             // qs = (ys.u, ys.v)
-            const double gy0 = gq0 * u0 + gq1 * v0, gy1 = gq0 * u1 + gq1 * v1,
-                         gy2 = gq0 * u2 + gq1 * v2;
-            gu0 = gq0 * ys0; gu1 = gq0 * ys1; gu2 = gq0 * ys2;
-            gv0 = gq1 * ys0; gv1 = gq1 * ys1; gv2 = gq1 * ys2;
+            const T gy0 = gq0 * tu0 + gq1 * tv0, gy1 = gq0 * tu1 + gq1 * tv1,
+                    gy2 = gq0 * tu2 + gq1 * tv2;
+            gu0 = gq0 * s0; gu1 = gq0 * s1; gu2 = gq0 * s2;
+            gv0 = gq1 * s0; gv1 = gq1 * s1; gv2 = gq1 * s2;
             // ys = ts d - c
-            const double gts = (double)g_ts + gy0 * d0 + gy1 * d1 + gy2 * d2;
+            const T gts = (T)g_ts + gy0 * td0 + gy1 * td1 + gy2 * td2;
             gc0 = -gy0; gc1 = -gy1; gc2 = -gy2;
             // ts = (c.m + delta) / (d.m)
-            const double f = gts / X.G.A;
-            gc0 += f * m0; gc1 += f * m1; gc2 += f * m2;
-            gm0 = -f * ys0; gm1 = -f * ys1; gm2 = -f * ys2;
-            double gdr = 0.0;
+            const T f = gts / tA;
+            gc0 += f * tm0; gc1 += f * tm1; gc2 += f * tm2;
+            gm0 = -f * s0; gm1 = -f * s1; gm2 = -f * s2;
+            T gdr = 0;
+            const float r = S.r[j];
             if (X.G.dr > r) o.r += (float)f;            // delta = r
             else if (X.G.dr < -r) o.r -= (float)f;      // delta = -r
             else gdr = f;
-            // Eq. svdisp at the base-face hit
+            // Eq. svdisp at the base-face hit (the chart point in fp64 as in the forward)
             const double B = X.c[0] * m0 + X.c[1] * m1 + X.c[2] * m2;
             const double tb = B / X.G.A;
             const double y0 = tb * d0 - X.c[0], y1 = tb * d1 - X.c[1], y2 = tb * d2 - X.c[2];
             const double qb0 = y0 * u0 + y1 * u1 + y2 * u2;
             const double qb1 = y0 * v0 + y1 * v1 + y2 * v2;
-            soft_voronoi_rev(uv, K, qb0, qb1, tau, w, ux, uy);
+            float wb[kMaxDetail];
+            soft_voronoi(uv, K, qb0, qb1, tau, wb);
+            sv_units<T>(uv, K, qb0, qb1, ux, uy);
             const float *dk = ds.ddisp + (size_t)K * cell;
-            double dr = 0.0, dv[kMaxDetail];
+            T dr = 0, bsum = 0, dv[kMaxDetail];
 #pragma unroll
             for (int k = 0; k < kMaxDetail; ++k) {
-                dv[k] = k < K ? (double)__ldg(dk + k) : 0.0;
+                w[k] = (T)wb[k];
+                bsum += w[k];
+                dv[k] = k < K ? (T)__ldg(dk + k) : (T)0;
                 dr += w[k] * dv[k];
             }
-            double gb0 = 0.0, gb1 = 0.0;
+            dr /= bsum;
+            T gb0 = 0, gb1 = 0;
 #pragma unroll
             for (int k = 0; k < kMaxDetail; ++k) {
                 if (k < K) {
-                    gdisp[k] = (float)(w[k] * gdr);
-                    const double grho = -taud * w[k] * gdr * (dv[k] - dr);
+                    const T wk = w[k] / bsum;
+                    gdisp[k] = (float)(wk * gdr);
+                    const T grho = -ttau * wk * gdr * (dv[k] - dr);
                     gb0 += grho * ux[k];
                     gb1 += grho * uy[k];
                     guv[2 * k] -= (float)(grho * ux[k]);
                     guv[2 * k + 1] -= (float)(grho * uy[k]);
                 }
             }
-            const double hy0 = gb0 * u0 + gb1 * v0, hy1 = gb0 * u1 + gb1 * v1,
-                         hy2 = gb0 * u2 + gb1 * v2;
-            gu0 += gb0 * y0; gu1 += gb0 * y1; gu2 += gb0 * y2;
-            gv0 += gb1 * y0; gv1 += gb1 * y1; gv2 += gb1 * y2;
-            const double f2 = (hy0 * d0 + hy1 * d1 + hy2 * d2) / X.G.A;
-            gc0 += f2 * m0 - hy0; gc1 += f2 * m1 - hy1; gc2 += f2 * m2 - hy2;
-            gm0 -= f2 * y0; gm1 -= f2 * y1; gm2 -= f2 * y2;
+            const T b0 = (T)y0, b1 = (T)y1, b2 = (T)y2;
+            const T hy0 = gb0 * tu0 + gb1 * tv0, hy1 = gb0 * tu1 + gb1 * tv1,
+                    hy2 = gb0 * tu2 + gb1 * tv2;
+            gu0 += gb0 * b0; gu1 += gb0 * b1; gu2 += gb0 * b2;
+            gv0 += gb1 * b0; gv1 += gb1 * b1; gv2 += gb1 * b2;
+            const T f2 = (hy0 * td0 + hy1 * td1 + hy2 * td2) / tA;
+            gc0 += f2 * tm0 - hy0; gc1 += f2 * tm1 - hy1; gc2 += f2 * tm2 - hy2;
+            gm0 -= f2 * b0; gm1 -= f2 * b1; gm2 -= f2 * b2;
         }
         // frame: v = m x u, u = w/|w|, w = e_k x m, m = n/|n|
-        gm0 += u1 * gv2 - u2 * gv1;           // u x gv
-        gm1 += u2 * gv0 - u0 * gv2;
-        gm2 += u0 * gv1 - u1 * gv0;
-        gu0 += gv1 * m2 - gv2 * m1;           // gv x m
-        gu1 += gv2 * m0 - gv0 * m2;
-        gu2 += gv0 * m1 - gv1 * m0;
-        const double iwl = 1.0 / __ldg(F + 10), inn = 1.0 / __ldg(F + 9);
+        gm0 += tu1 * gv2 - tu2 * gv1;           // u x gv
+        gm1 += tu2 * gv0 - tu0 * gv2;
+        gm2 += tu0 * gv1 - tu1 * gv0;
+        gu0 += gv1 * tm2 - gv2 * tm1;           // gv x m
+        gu1 += gv2 * tm0 - gv0 * tm2;
+        gu2 += gv0 * tm1 - gv1 * tm0;
+        const T iwl = (T)(1.0 / __ldg(F + 10)), inn = (T)(1.0 / __ldg(F + 9));
         const int kax = (int)__ldg(F + 11);
-        const double ug = u0 * gu0 + u1 * gu1 + u2 * gu2;
-        const double gw0 = (gu0 - u0 * ug) * iwl, gw1 = (gu1 - u1 * ug) * iwl,
-                     gw2 = (gu2 - u2 * ug) * iwl;
+        const T ug = tu0 * gu0 + tu1 * gu1 + tu2 * gu2;
+        const T gw0 = (gu0 - tu0 * ug) * iwl, gw1 = (gu1 - tu1 * ug) * iwl,
+                gw2 = (gu2 - tu2 * ug) * iwl;
         // + gw x e_k
         if (kax == 0) { gm1 += gw2; gm2 -= gw1; }
         else if (kax == 1) { gm0 -= gw2; gm2 += gw0; }
         else { gm0 += gw1; gm1 -= gw0; }
-        const double mg = m0 * gm0 + m1 * gm1 + m2 * gm2;
-        o.nx += (float)((gm0 - m0 * mg) * inn);
-        o.ny += (float)((gm1 - m1 * mg) * inn);
-        o.nz += (float)((gm2 - m2 * mg) * inn);
+        const T mg = tm0 * gm0 + tm1 * gm1 + tm2 * gm2;
+        o.nx += (float)((gm0 - tm0 * mg) * inn);
+        o.ny += (float)((gm1 - tm1 * mg) * inn);
+        o.nz += (float)((gm2 - tm2 * mg) * inn);
         o.px += (float)gc0;
         o.py += (float)gc1;
         o.pz += (float)gc2;
-    } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) buf[lane][q] = 0.0f;
     }
+    const unsigned segm = __ballot_sync(0xffffffffu, seg);   // rows of buf that were written
     __syncwarp();
     // dL/dv: lane -> site k = lane / 4 and 6 consecutive (a, c) entries
     {
         const int k = lane >> 2, ac0 = (lane & 3) * 6;
-        float acc[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) {
+        float accv[6] = {0, 0, 0, 0, 0, 0};
+        for (unsigned mm = segm; mm; mm &= mm - 1) {
+            const int l = __ffs(mm) - 1;
             const float wk = buf[l][k];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) acc[q] = fmaf(wk, buf[l][8 + ac0 + q], acc[q]);
+            for (int q = 0; q < 6; ++q) accv[q] = fmaf(wk, buf[l][8 + ac0 + q], accv[q]);
         }
         if (k < K && ds.g_sv) {
             float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cell + k) * 24 + ac0);
-            atomicAdd(dst, make_float2(acc[0], acc[1]));
-            atomicAdd(dst + 1, make_float2(acc[2], acc[3]));
-            atomicAdd(dst + 2, make_float2(acc[4], acc[5]));
+            atomicAdd(dst, make_float2(accv[0], accv[1]));
+            atomicAdd(dst + 1, make_float2(accv[2], accv[3]));
+            atomicAdd(dst + 2, make_float2(accv[4], accv[5]));
         }
     }
     __syncwarp();
@@ -1165,8 +1222,7 @@ __device__ __noinline__ void detail_backward(const DeviceScene &ds, uint32_t cel
     __syncwarp();
     if (lane < 24) {
         float t = 0.0f;
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) t += buf[l][lane];
+        for (unsigned mm = segm; mm; mm &= mm - 1) t += buf[__ffs(mm) - 1][lane];
         if (lane < 16) {
             if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cell + lane, t);
         } else if (lane - 16 < K && ds.g_disp) {
@@ -1174,15 +1230,21 @@ __device__ __noinline__ void detail_backward(const DeviceScene &ds, uint32_t cel
         }
     }
     __syncwarp();
+    // own-cell terms (rgb_i is unused by detail cells: no colour gradient)
+    float *accc = acc + 12 * (size_t)cell;
+    if (__popc(segm) == 1) {
+        if (seg) {
+            atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
+            atomicAdd(reinterpret_cast<float4 *>(accc) + 2, make_float4(0.0f, o.nx, o.ny, o.nz));
+            atomicAdd(reinterpret_cast<float4 *>(accc) + 1, make_float4(o.r, gs, 0.0f, 0.0f));
+        }
+    } else {
+        float v[16] = {o.px, o.py, o.pz, o.w, o.r, gs, 0, 0, 0, o.nx, o.ny, o.nz, 0, 0, 0, 0};
+        warp_reduce16_atomic<12>(v, accc, lane);
+    }
 }
 
 // Backward of one segment (lanes with seg) + scatter of the cell's gradients.
-struct BwdPixel {
-    float T, Cr, Cg, Cb;
-    float4 fin, G;
-    float GT_Tfin;
-};
-
 template <bool kDipole, bool kDetail>
 __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, bool seg,
                                                  const WarpStage &S, int j, BwdPixel &px,
@@ -1191,6 +1253,12 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
                                                  const DetailCtx *X, const float *om,
                                                  float (*buf)[33])
 {
+    if (kDetail) {
+        // (an fp32 instantiation for non-grazing warps measured slower on B200: the
+        // fp64 -> fp32 conversions cost more than the fp64 arithmetic they save)
+        detail_segment<double>(R, g, seg, S, j, px, ds, acc, lane, *X, om, buf);
+        return;
+    }
     constexpr bool dipole = kDipole;
     OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
     float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f, g_ts = 0.0f;
@@ -1215,16 +1283,11 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
         if (gdt != 0.0f) {
             const float rad = S.r[j];
             const uint32_t eb = S.eb[j];
-            end_grad<kDipole, kDetail>(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o,
-                                       dnrm, eb, g_ts);
-            end_grad<kDipole, kDetail>(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o,
-                                       dnrm, eb, g_ts);
+            end_grad<kDipole, false>(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o,
+                                     dnrm, eb, g_ts);
+            end_grad<kDipole, false>(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o,
+                                     dnrm, eb, g_ts);
         }
-    }
-    if (kDetail) {
-        // radiance gradients go to the detail sites; rgb_i is unused (gets none)
-        detail_backward(ds, S.cell[j], seg, *X, S.r[j], om, g_ts, gR, gG, gB, o, buf, lane);
-        gR = gG = gB = 0.0f;
     }
     // own-cell terms: one lane alone issues its atomics, else a transposing warp
     // reduction then one 9-lane atomic instruction
@@ -1251,7 +1314,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
 }  // namespace
 
 template <bool kDipole, bool kDetail>
-__global__ void __launch_bounds__(256, kDetail ? 2 : PF_K7_MINB)
+__global__ void __launch_bounds__(256, kDetail ? PF_K7D_MINB : PF_K7_MINB)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
             const float4 *__restrict__ saved, const float4 *__restrict__ grad_out,
@@ -1308,12 +1371,6 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             dpl = S.nrm[j];
         }
     };
-    auto shade = [&](int j, const Seg &g, bool seg, float &cr, float &cg, float &cb) {
-        if (kDetail && seg) {
-            X.tcol = X.G.parallel ? (double)__fadd_rn(g.tc, g.lo) : X.G.ts;
-            detail_color(ds, S.cell[j], X.d, X.c, X.tcol, om, cr, cg, cb);
-        }
-    };
     const uint32_t nchunks = wdone[(size_t)tile * kWarps + warp];
     const uint32_t c0 = chunk_off[tile];
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -1332,11 +1389,21 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 if (!__any_sync(0xffffffffu, hit)) continue;
                 float4 dpl;
                 float cr, cg, cb;
-                prepare(j, hit, dpl, cr, cg, cb);
-                clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
+                if (kDetail) {   // as K6: the face only where the interval is non-empty
+                    clip_interval<true, false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
+                    const bool pre = g.dt > 0.0f;
+                    prepare(j, pre, dpl, cr, cg, cb);
+                    if (__any_sync(0xffffffffu, pre)) {
+                        clip_plane<true>(P.R, dpl, kEndDipole, g);
+                        const float dt = __fsub_rn(g.hi, g.lo);
+                        g.dt = (pre && dt > 0.0f) ? dt : 0.0f;
+                    }
+                } else {
+                    prepare(j, hit, dpl, cr, cg, cb);
+                    clip_interval<true, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
+                }
                 const bool seg = g.dt > 0.0f;
                 if (!__any_sync(0xffffffffu, seg)) continue;
-                shade(j, g, seg, cr, cg, cb);
                 segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb,
                                                    dpl, &X, om, buf);
                 if (seg && px.T < kTStop) done = true;
@@ -1386,7 +1453,6 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 }
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
-            shade(j, g, seg, cr, cg, cb);
             segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb, dpl,
                                                &X, om, buf);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk

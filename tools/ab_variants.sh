@@ -4,6 +4,6 @@ mkdir -p gpurun_out
 for v in default "$@"; do
   if [ "$v" = default ]; then unset PF_LIBRARY_PATH; else export PF_LIBRARY_PATH=$PWD/$v; fi
   echo "== $v" >> gpurun_out/ab.log
-  timeout 600 python bench.py --warmup 3 --steps 10 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "
+  timeout 600 python bench.py --warmup 3 --steps 10 --no-cpu --no-e2e $BENCH_ARGS 2>&1 | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],1), round(d['fwd_fps'],1), {k:round(v,3) for k,v in d['stage_ms_per_step'].items() if k in ('K4_sort','K6_forward','K7_backward')})" >> gpurun_out/ab.log 2>&1
 done
