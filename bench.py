@@ -140,13 +140,19 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
-def flops_model(cnt):
+def flops_model(cnt, K=0):
     """Algorithmic FP32 work per view from the per-pixel counters:
     F_fwd = 8 X_s + 14 X_h + 16 X_p + 15 X_c;  F_bwd = F_fwd (replay) + 60 X_c
-    + 30 * (active plane endpoints, <= 2 X_c)."""
+    + 30 * (active plane endpoints, <= 2 X_c).  With K detail sites (NEXT-2,
+    DESIGN §13) each composited segment adds (40 + 86 K) forward (two chart points,
+    two K-site soft-Voronoi evaluations at 16 K, the 8-axis SV blend at 54 K) and
+    (558 + 46 K) more backward (the reverse chain, the outer product 24 K x 2)."""
     Xs, Xh, Xp, Xc = (float(v) for v in cnt)
     f_fwd = 8 * Xs + 14 * Xh + 16 * Xp + 15 * Xc
     f_bwd = f_fwd + 60 * Xc + 30 * 2 * Xc
+    if K:
+        f_fwd += (40 + 86 * K) * Xc
+        f_bwd += (40 + 86 * K) * Xc + (558 + 46 * K) * Xc
     return f_fwd, f_bwd
 
 
@@ -377,7 +383,7 @@ def main():
     for c in cams[:2]:
         cnt += r.debug_counters(c).sum(dim=(0, 1)).double().cpu().numpy()
     cnt /= min(2, len(cams))
-    f_fwd, f_bwd = flops_model(cnt)
+    f_fwd, f_bwd = flops_model(cnt, K=args.detail)
     peaks, peaks_kind = load_peaks()
     k6_ms, k6_n = stages["K6_forward"]
     k7_ms, k7_n = stages["K7_backward"]
@@ -388,7 +394,8 @@ def main():
     d_avg = d_ms / max(d_n, 1)
     d_flops = f_bwd if dom == "K7_backward" else f_fwd
     achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
-    traffic, traffic_src = load_traffic("k7_backward" if dom == "K7_backward" else "k6_forward")
+    traffic, traffic_src = load_traffic(("k7_backward" if dom == "K7_backward" else "k6_forward")
+                                        + ("_detail" if args.detail else ""))
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write)",

@@ -2,15 +2,24 @@
 # Run on the B200 box (gpurun): bench lines (default + other workloads), the
 # reference arm, the ncu launch list and full captures of the hot kernels.
 mkdir -p gpurun_out
+rm -f gpurun_out/prof_*.ncu-rep gpurun_out/launches.csv
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 python bench.py --dipoles --no-cpu > gpurun_out/bench_dipoles.json 2>&1
 timeout 900 python bench.py --workload mip360_1m --no-cpu > gpurun_out/bench_mip360.json 2>&1
 timeout 900 python bench.py --workload nerfsynth200k --no-cpu > gpurun_out/bench_nerfsynth.json 2>&1
 timeout 1500 python bench.py --workload sweep64_3m --no-cpu --no-e2e --steps 3 > gpurun_out/bench_sweep.json 2>&1
+timeout 900 python bench.py --fisheye --no-cpu > gpurun_out/bench_fisheye.json 2>&1
+timeout 900 python bench.py --workload nerfsynth200k --detail 8 --no-cpu > gpurun_out/bench_nerfsynth_detail.json 2>&1
+timeout 900 python bench.py --detail 8 --no-cpu --steps 5 > gpurun_out/bench_detail.json 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu \
     > gpurun_out/ncu_launch.log 2>&1
+for k in k7_backward k6_forward; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
+      -o gpurun_out/prof_${k}_detail python bench.py --workload nerfsynth200k --detail 8 --steps 1 \
+      --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_${k}_detail.log 2>&1
+done
 for k in k7_backward k6_forward k4_scatter c4_query; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
       -o gpurun_out/prof_$k python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_$k.log 2>&1
