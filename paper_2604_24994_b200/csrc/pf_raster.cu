@@ -397,6 +397,7 @@ struct DetailGeo {
     float delta;      // clamped displacement
     float dr;         // unclamped soft-Voronoi displacement
     bool parallel;    // d.m == 0: no base-face hit (reading R6e)
+    float w[kMaxDetail];   // the soft-Voronoi weights at x_bar (reused by K7)
 };
 
 // softmax_a(gamma d.a_a) of the pixel's ray
@@ -432,7 +433,14 @@ __device__ __forceinline__ float sqrt_approx(float x)
 // rho_k - rho_j = (s_j - s_k).(2q - s_k - s_j) / (rho_k + rho_j), which keeps
 // full relative precision when q is far from every site (grazing rays), where
 // rho_k - rho_j from two rounded distances would not.
-__device__ __forceinline__ void soft_voronoi(const float2 *__restrict__ uv, int K, double q0d,
+__device__ __forceinline__ void load_sites(const float2 *__restrict__ uv, int K,
+                                           float2 s[kMaxDetail])
+{
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) s[k] = k < K ? __ldg(uv + k) : make_float2(0.0f, 0.0f);
+}
+
+__device__ __forceinline__ void soft_voronoi(const float2 s[kMaxDetail], int K, double q0d,
                                              double q1d, float tau, float w[kMaxDetail])
 {
     const float q0 = __double2float_rn(q0d), q1 = __double2float_rn(q1d);
@@ -441,7 +449,7 @@ __device__ __forceinline__ void soft_voronoi(const float2 *__restrict__ uv, int 
 #pragma unroll
     for (int k = 0; k < kMaxDetail; ++k) {
         if (k < K) {
-            const float2 sk = __ldg(uv + k);
+            const float2 sk = s[k];
             sx[k] = sk.x;
             sy[k] = sk.y;
             const float dx = q0 - sk.x, dy = q1 - sk.y;
@@ -506,10 +514,11 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
                      y2 = __fma_rn(tb, d[2], -c[2]);
         const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
         const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
-        float w[kMaxDetail];
+        float *w = G.w;
         const int K = ds.K;
-        soft_voronoi(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
-                     ds.sv_tau, w);
+        float2 st[kMaxDetail];
+        load_sites(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, st);
+        soft_voronoi(st, K, q0, q1, ds.sv_tau, w);
         const float *dk = ds.ddisp + (size_t)K * cell;
         float dr = 0.0f;
 #pragma unroll
@@ -535,8 +544,9 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
     const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
     float w[kMaxDetail];
     const int K = ds.K;
-    soft_voronoi(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, q0, q1,
-                 ds.sv_tau, w);
+    float2 st[kMaxDetail];
+    load_sites(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, st);
+    soft_voronoi(st, K, q0, q1, ds.sv_tau, w);
     const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
     cr = cg = cb = 0.0f;
 #pragma unroll
@@ -967,14 +977,14 @@ struct DetailCtx {
 
 // unit vectors (q - s_k)/rho_k: fp64 (rsqrt + one Newton step, ~1e-14) or fp32
 template <typename T>
-__device__ __forceinline__ void sv_units(const float2 *__restrict__ uv, int K, double q0, double q1,
+__device__ __forceinline__ void sv_units(const float2 s[kMaxDetail], int K, double q0, double q1,
                                          T ux[kMaxDetail], T uy[kMaxDetail])
 {
 #pragma unroll
     for (int k = 0; k < kMaxDetail; ++k) {
         ux[k] = uy[k] = (T)0;
         if (k < K) {
-            const float2 sk = __ldg(uv + k);
+            const float2 sk = s[k];
             const T dx = (T)(q0 - (double)sk.x), dy = (T)(q1 - (double)sk.y);
             const T r2 = dx * dx + dy * dy;
             if (r2 > (T)0) {
@@ -1025,7 +1035,9 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
         const double qs0 = ys0 * u0 + ys1 * u1 + ys2 * u2;
         const double qs1 = ys0 * v0 + ys1 * v1 + ys2 * v2;
         float ws[kMaxDetail], dG[kMaxDetail];
-        soft_voronoi(uv, K, qs0, qs1, tau, ws);
+        float2 st[kMaxDetail];
+        load_sites(uv, K, st);
+        soft_voronoi(st, K, qs0, qs1, tau, ws);
         const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
         float cr = 0.0f, cg = 0.0f, cb = 0.0f;
 #pragma unroll
@@ -1094,13 +1106,15 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             wsum += w[k];
             sw += w[k] * (T)dG[k];
         }
-        sw /= wsum;   // renormalised: sum_k w_k (dG_k - sw) = 0 to working-precision rounding
-        sv_units<T>(uv, K, qs0, qs1, ux, uy);
+        const T iwsum = (T)1 / wsum;
+        sw *= iwsum;   // renormalised: sum_k w_k (dG_k - sw) = 0 to working-precision rounding
+        sv_units<T>(st, K, qs0, qs1, ux, uy);
         T gq0 = 0, gq1 = 0;
+        const T cq = -ttau * (T)wa * iwsum;
 #pragma unroll
         for (int k = 0; k < kMaxDetail; ++k) {
             if (k < K) {
-                const T grho = -ttau * (T)wa * (w[k] / wsum) * ((T)dG[k] - sw);
+                const T grho = cq * w[k] * ((T)dG[k] - sw);
                 gq0 += grho * ux[k];
                 gq1 += grho * uy[k];
                 guv[2 * k] -= (float)(grho * ux[k]);
@@ -1120,7 +1134,8 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             const T gts = (T)g_ts + gy0 * td0 + gy1 * td1 + gy2 * td2;
             gc0 = -gy0; gc1 = -gy1; gc2 = -gy2;
             // ts = (c.m + delta) / (d.m)
-            const T f = gts / tA;
+            const T iA = (T)1 / tA;
+            const T f = gts * iA;
             gc0 += f * tm0; gc1 += f * tm1; gc2 += f * tm2;
             gm0 = -f * s0; gm1 = -f * s1; gm2 = -f * s2;
             T gdr = 0;
@@ -1130,13 +1145,12 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             else gdr = f;
             // Eq. svdisp at the base-face hit (the chart point in fp64 as in the forward)
             const double B = X.c[0] * m0 + X.c[1] * m1 + X.c[2] * m2;
-            const double tb = B / X.G.A;
+            const double tb = B / X.G.A;   // as detail_plane
             const double y0 = tb * d0 - X.c[0], y1 = tb * d1 - X.c[1], y2 = tb * d2 - X.c[2];
             const double qb0 = y0 * u0 + y1 * u1 + y2 * u2;
             const double qb1 = y0 * v0 + y1 * v1 + y2 * v2;
-            float wb[kMaxDetail];
-            soft_voronoi(uv, K, qb0, qb1, tau, wb);
-            sv_units<T>(uv, K, qb0, qb1, ux, uy);
+            const float *wb = X.G.w;   // detail_plane's weights at x_bar
+            sv_units<T>(st, K, qb0, qb1, ux, uy);
             const float *dk = ds.ddisp + (size_t)K * cell;
             T dr = 0, bsum = 0, dv[kMaxDetail];
 #pragma unroll
@@ -1146,12 +1160,13 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
                 dv[k] = k < K ? (T)__ldg(dk + k) : (T)0;
                 dr += w[k] * dv[k];
             }
-            dr /= bsum;
+            const T ibsum = (T)1 / bsum;
+            dr *= ibsum;
             T gb0 = 0, gb1 = 0;
 #pragma unroll
             for (int k = 0; k < kMaxDetail; ++k) {
                 if (k < K) {
-                    const T wk = w[k] / bsum;
+                    const T wk = w[k] * ibsum;
                     gdisp[k] = (float)(wk * gdr);
                     const T grho = -ttau * wk * gdr * (dv[k] - dr);
                     gb0 += grho * ux[k];
@@ -1165,7 +1180,7 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
                     hy2 = gb0 * tu2 + gb1 * tv2;
             gu0 += gb0 * b0; gu1 += gb0 * b1; gu2 += gb0 * b2;
             gv0 += gb1 * b0; gv1 += gb1 * b1; gv2 += gb1 * b2;
-            const T f2 = (hy0 * td0 + hy1 * td1 + hy2 * td2) / tA;
+            const T f2 = (hy0 * td0 + hy1 * td1 + hy2 * td2) * iA;
             gc0 += f2 * tm0 - hy0; gc1 += f2 * tm1 - hy1; gc2 += f2 * tm2 - hy2;
             gm0 -= f2 * b0; gm1 -= f2 * b1; gm2 -= f2 * b2;
         }
