@@ -496,6 +496,7 @@ __device__ __forceinline__ double dot3d(const double a[3], double b0, double b1,
 
 // Eq. svdisp: base-face hit, displacement, displaced face.  Returns the face as
 // a clip plane (m, delta):  (x - p).m <= delta  <=>  a t' <= m.e + delta.
+template <int KT>
 __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t cell,
                                                const double d[3], const double c[3], float r,
                                                DetailGeo &G)
@@ -515,7 +516,7 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
         const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
         const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
         float *w = G.w;
-        const int K = ds.K;
+        const int K = KT == 8 ? 8 : ds.K;   // K == 8 (the paper's setting) known at compile time
         float2 st[kMaxDetail];
         load_sites(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, st);
         soft_voronoi(st, K, q0, q1, ds.sv_tau, w);
@@ -533,6 +534,7 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
 
 // Eq. svrad at the point Q + t d (t = the displaced-face hit, or the interval
 // entry for a parallel ray): sum_k w_k sum_a om_a v_{k,a}
+template <int KT>
 __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cell, const double d[3],
                                              const double c[3], double t, const float om[8],
                                              float &cr, float &cg, float &cb)
@@ -543,7 +545,7 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
     const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
     const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
     float w[kMaxDetail];
-    const int K = ds.K;
+    const int K = KT == 8 ? 8 : ds.K;   // K == 8 (the paper's setting) known at compile time
     float2 st[kMaxDetail];
     load_sites(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, st);
     soft_voronoi(st, K, q0, q1, ds.sv_tau, w);
@@ -614,8 +616,11 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K7D_MINB
 #define PF_K7D_MINB 2
 #endif
-template <bool kCount, bool kRecord, bool kDipole, bool kDetail>
-__global__ void __launch_bounds__(256, kDetail ? 2 : PF_K6_MINB)
+#ifndef PF_K6D_MINB
+#define PF_K6D_MINB 3
+#endif
+template <bool kCount, bool kRecord, bool kDipole, int kDetail>
+__global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB : PF_K6_MINB)
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
            float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
@@ -665,7 +670,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                     if (pre) {
                         dd[0] = PR.dx[threadIdx.x]; dd[1] = PR.dy[threadIdx.x]; dd[2] = PR.dz[threadIdx.x];
                         cell_c(ds, cam, S.cell[j], dc);
-                        dpl = detail_plane(ds, S.cell[j], dd, dc, S.r[j], G);
+                        dpl = detail_plane<kDetail>(ds, S.cell[j], dd, dc, S.r[j], G);
                     }
                     clip_plane<kRecord>(P.R, dpl, kEndDipole, g);
                     const float dt = __fsub_rn(g.hi, g.lo);
@@ -698,7 +703,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 const float Tk = T;
                 float cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
                 if (kDetail)
-                    detail_color(ds, S.cell[j], dd, dc,
+                    detail_color<kDetail>(ds, S.cell[j], dd, dc,
                                  G.parallel ? (double)__fadd_rn(g.tc, g.lo) : G.ts, om, cr, cg, cb);
                 composite_step(S.sig[j], g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
                 wk = __fmul_rn(Tk, alpha);
@@ -769,7 +774,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     }
 }
 
-template <bool kDipole, bool kDetail>
+template <bool kDipole, int kDetail>
 static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *counters,
                              uint32_t *rec_used, float *stc, float *stn, cudaStream_t st)
 {
@@ -798,12 +803,14 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
 {
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
-    if (s->ds.K)
-        launch_forward_t<true, true>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+    if (s->ds.K == 8)
+        launch_forward_t<true, 8>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+    else if (s->ds.K)
+        launch_forward_t<true, 1>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     else if (s->ds.cellN)
-        launch_forward_t<true, false>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<true, 0>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     else
-        launch_forward_t<false, false>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<false, 0>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
     ++s->launches;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();
@@ -1008,13 +1015,13 @@ struct BwdPixel {
 #else
 #define PF_DETAIL_FN __forceinline__
 #endif
-template <typename T>
+template <typename T, int KT>
 __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg,
                                             const WarpStage &S, int j, BwdPixel &px,
                                             const DeviceScene &ds, float *acc, int lane,
                                             const DetailCtx &X, const float *om, float (*buf)[33])
 {
-    const int K = ds.K;
+    const int K = KT == 8 ? 8 : ds.K;   // K == 8 (the paper's setting) known at compile time
     const uint32_t cell = S.cell[j];
     const float tau = ds.sv_tau;
     OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1260,7 +1267,7 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
 }
 
 // Backward of one segment (lanes with seg) + scatter of the cell's gradients.
-template <bool kDipole, bool kDetail>
+template <bool kDipole, int kDetail>
 __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, bool seg,
                                                  const WarpStage &S, int j, BwdPixel &px,
                                                  const DeviceScene &ds, float *acc, int lane,
@@ -1271,7 +1278,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
     if (kDetail) {
         // (an fp32 instantiation for non-grazing warps measured slower on B200: the
         // fp64 -> fp32 conversions cost more than the fp64 arithmetic they save)
-        detail_segment<double>(R, g, seg, S, j, px, ds, acc, lane, *X, om, buf);
+        detail_segment<double, kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, buf);
         return;
     }
     constexpr bool dipole = kDipole;
@@ -1328,7 +1335,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
 
 }  // namespace
 
-template <bool kDipole, bool kDetail>
+template <bool kDipole, int kDetail>
 __global__ void __launch_bounds__(256, kDetail ? PF_K7D_MINB : PF_K7_MINB)
 k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
@@ -1380,7 +1387,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
         if (kDetail) {
             if (active) {
                 cell_c(ds, cam, S.cell[j], X.c);
-                dpl = detail_plane(ds, S.cell[j], X.d, X.c, S.r[j], X.G);
+                dpl = detail_plane<kDetail>(ds, S.cell[j], X.d, X.c, S.r[j], X.G);
             }
         } else if (kDipole) {
             dpl = S.nrm[j];
@@ -1476,7 +1483,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     }
 }
 
-template <bool kDipole, bool kDetail>
+template <bool kDipole, int kDetail>
 static void launch_backward_t(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
@@ -1494,12 +1501,14 @@ cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cu
 {
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
-    if (s->ds.K)
-        launch_backward_t<true, true>(s, v, grad_out, st);
+    if (s->ds.K == 8)
+        launch_backward_t<true, 8>(s, v, grad_out, st);
+    else if (s->ds.K)
+        launch_backward_t<true, 1>(s, v, grad_out, st);
     else if (s->ds.cellN)
-        launch_backward_t<true, false>(s, v, grad_out, st);
+        launch_backward_t<true, 0>(s, v, grad_out, st);
     else
-        launch_backward_t<false, false>(s, v, grad_out, st);
+        launch_backward_t<false, 0>(s, v, grad_out, st);
     ++s->launches;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();
