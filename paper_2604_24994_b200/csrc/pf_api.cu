@@ -97,6 +97,8 @@ int reserve_view_bins(pf_scene *s, pf::ViewState &v)
     PF_CUDA(v.count.reserve(4 * N));
     PF_CUDA(v.keybits.reserve(4 * N));
     PF_CUDA(v.offsets.reserve(4 * N));
+    if (v.cam.model == PF_FISHEYE)
+        PF_CUDA(v.tdir.reserve(sizeof(double) * (3 * (size_t)v.cam.tiles_x * v.cam.tiles_y + 2)));
     return PF_OK;
 }
 
@@ -400,6 +402,7 @@ int pf_destroy(pf_scene *s)
         v.count.release();
         v.keybits.release();
         v.offsets.release();
+        v.tdir.release();
         v.saved.release();
         v.desc.release();
         v.wdone.release();
@@ -409,6 +412,7 @@ int pf_destroy(pf_scene *s)
     s->debug_view.count.release();
     s->debug_view.keybits.release();
     s->debug_view.offsets.release();
+    s->debug_view.tdir.release();
     s->vals_all.release();
     s->ranges_all.release();
     s->order_all.release();

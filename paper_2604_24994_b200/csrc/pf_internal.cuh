@@ -67,6 +67,7 @@ struct ViewState {
     CamParams cam{};
     int64_t P = 0;
     DevBuf rect, count, keybits, offsets;   // binning of this view (N-sized)
+    DevBuf tdir;                             // fisheye: tile-centre rays (3T doubles) + cos/sin(th)
     uint32_t *vals_p = nullptr;              // sorted cell ids (the call's shared array)
     uint2 *ranges_p = nullptr;               // this view's per-tile [start,end) into vals_p
     int64_t pair_off = 0;                    // first pair of this view in the shared arrays

@@ -223,14 +223,35 @@ __device__ __forceinline__ double fisheye_half_angle(const CamParams &cam)
     return sqrt(ax * ax + ay * ay);
 }
 
+// per-view table: the ray through every tile centre (3 doubles per tile), then
+// cos(th), sin(th) -- computed once per view instead of per (cell, tile)
+__global__ void __launch_bounds__(256) k1_fisheye_dirs(CamParams cam, double *__restrict__ tdir)
+{
+    const int T = cam.tiles_x * cam.tiles_y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < T) {
+        const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
+        double at[3];
+        fisheye_dir(cam, 16.0 * tx + 8.0, 16.0 * ty + 8.0, at);
+        tdir[3 * t] = at[0];
+        tdir[3 * t + 1] = at[1];
+        tdir[3 * t + 2] = at[2];
+    }
+    if (t == 0) {
+        const double th = fisheye_half_angle(cam);
+        tdir[3 * T] = cos(th);
+        tdir[3 * T + 1] = sin(th);
+    }
+}
+
 __device__ __forceinline__ bool fisheye_tile_pass(const CamParams &cam, const double c[3], double r,
-                                                  double cth, double sth, int tx, int ty)
+                                                  double cth, double sth, int tx, int ty,
+                                                  const double *__restrict__ tdir)
 {
     const double cc = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
     if (cc <= r * r) return true;
-    double at[3];
-    fisheye_dir(cam, 16.0 * tx + 8.0, 16.0 * ty + 8.0, at);
-    const double lhs = c[0] * at[0] + c[1] * at[1] + c[2] * at[2];
+    const double *at = tdir + 3 * (ty * cam.tiles_x + tx);
+    const double lhs = c[0] * __ldg(at) + c[1] * __ldg(at + 1) + c[2] * __ldg(at + 2);
     return lhs >= cth * sqrt(cc - r * r) - sth * r;
 }
 
@@ -295,7 +316,8 @@ __device__ __forceinline__ void camera_coords(const CamParams &cam, const float 
 __global__ void __launch_bounds__(256)
 k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights,
               const float *__restrict__ radii, int64_t N, CamParams cam, int4 *__restrict__ rect,
-              int *__restrict__ count, uint32_t *__restrict__ keybits)
+              int *__restrict__ count, uint32_t *__restrict__ keybits,
+              const double *__restrict__ tdir)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
@@ -320,12 +342,14 @@ k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights
         camera_coords(cam, sites + 3 * i, c);
         const double dist = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
         if ((r > 0.0f) && !(dist + r <= (double)cam.near_plane)) {
-            const double th = fisheye_half_angle(cam), cth = cos(th), sth = sin(th);
+            const int T = cam.tiles_x * cam.tiles_y;
+            const double th = fisheye_half_angle(cam), cth = __ldg(tdir + 3 * T),
+                         sth = __ldg(tdir + 3 * T + 1);
             int4 cand;
             fisheye_rect(cam, c, r, th, cand);
             for (int ty = cand.y; ty < cand.w; ++ty)
                 for (int tx = cand.x; tx < cand.z; ++tx)
-                    cnt += fisheye_tile_pass(cam, c, r, cth, sth, tx, ty) ? 1 : 0;
+                    cnt += fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir) ? 1 : 0;
             if (cnt) rc = cand;
         }
         rect[i] = rc;
@@ -352,9 +376,14 @@ cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st)
 {
     cudaEvent_t ev;
     stage_begin(s, 1, st, &ev);
+    if (v.cam.model == PF_FISHEYE) {
+        k1_fisheye_dirs<<<ceil_div((int64_t)v.cam.tiles_x * v.cam.tiles_y, 256), 256, 0, st>>>(
+            v.cam, v.tdir.as<double>());
+        ++s->launches;
+    }
     k1_preprocess<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
         s->ds.sites, s->ds.weights, s->ds.radii, s->ds.N, v.cam, v.rect.as<int4>(),
-        v.count.as<int>(), v.keybits.as<uint32_t>());
+        v.count.as<int>(), v.keybits.as<uint32_t>(), v.tdir.as<double>());
     ++s->launches;
     stage_end(s, 1, st, ev);
     return cudaGetLastError();
@@ -556,20 +585,22 @@ k3_emit_fisheye(int64_t N, CamParams cam, const float *__restrict__ sites,
                 const float *__restrict__ radii, const int4 *__restrict__ rect,
                 const int *__restrict__ count, const uint32_t *__restrict__ keybits,
                 const uint32_t *__restrict__ offs, unsigned long long *__restrict__ keys,
-                uint32_t *__restrict__ vals, unsigned long long view_key)
+                uint32_t *__restrict__ vals, unsigned long long view_key,
+                const double *__restrict__ tdir)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N || count[i] == 0) return;
     const int4 rc = rect[i];
     double c[3];
     camera_coords(cam, sites + 3 * i, c);
-    const double th = fisheye_half_angle(cam), cth = cos(th), sth = sin(th);
+    const int T = cam.tiles_x * cam.tiles_y;
+    const double cth = __ldg(tdir + 3 * T), sth = __ldg(tdir + 3 * T + 1);
     const double r = radii[i];
     const uint32_t k = keybits[i];
     uint32_t o = offs[i];
     for (int ty = rc.y; ty < rc.w; ++ty)
         for (int tx = rc.x; tx < rc.z; ++tx)
-            if (fisheye_tile_pass(cam, c, r, cth, sth, tx, ty)) {
+            if (fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir)) {
                 const unsigned long long tile = (unsigned long long)(ty * cam.tiles_x + tx);
                 keys[o] = view_key | (tile << 32) | k;
                 vals[o] = (uint32_t)i;
@@ -586,7 +617,7 @@ cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *val
         k3_emit_fisheye<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
             s->ds.N, v.cam, s->ds.sites, s->ds.radii, v.rect.as<int4>(), v.count.as<int>(),
             v.keybits.as<uint32_t>(), v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals,
-            (unsigned long long)view_key);
+            (unsigned long long)view_key, v.tdir.as<double>());
         ++s->launches;
         stage_end(s, 3, st, ev);
         return cudaGetLastError();
