@@ -319,7 +319,57 @@ k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights
               int *__restrict__ count, uint32_t *__restrict__ keybits,
               const double *__restrict__ tdir)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cam.model == PF_FISHEYE) {   // warp-uniform: every lane of the warp stays
+        const bool live = i < N;
+        const int lane = threadIdx.x & 31;
+        int4 cand = make_int4(0, 0, 0, 0);
+        double c[3] = {0.0, 0.0, 0.0};
+        double r = 0.0;
+        if (live) {
+            const float *M = cam.M;
+            const float v0 = __fsub_rn(sites[3 * i + 0], M[3]), v1 = __fsub_rn(sites[3 * i + 1], M[7]),
+                        v2 = __fsub_rn(sites[3 * i + 2], M[11]);
+            const float K = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)),
+                                                __fmul_rn(v2, v2)),
+                                      weights[i]);
+            keybits[i] = order_bits(K);
+            const float rf = radii[i];
+            r = rf;
+            camera_coords(cam, sites + 3 * i, c);
+            const double dist = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+            if ((rf > 0.0f) && !(dist + r <= (double)cam.near_plane))
+                fisheye_rect(cam, c, r, fisheye_half_angle(cam), cand);
+        }
+        // count the passing tiles: the warp's cells one after another, lanes over tiles
+        const int T = cam.tiles_x * cam.tiles_y;
+        const double cth = __ldg(tdir + 3 * T), sth = __ldg(tdir + 3 * T + 1);
+        const int w = cand.z - cand.x, n = w > 0 && cand.w > cand.y ? w * (cand.w - cand.y) : 0;
+        unsigned todo = __ballot_sync(0xffffffffu, n > 0);
+        int my_cnt = 0;
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int sx = __shfl_sync(0xffffffffu, cand.x, src), sy = __shfl_sync(0xffffffffu, cand.y, src);
+            const int sw = __shfl_sync(0xffffffffu, w, src), sn = __shfl_sync(0xffffffffu, n, src);
+            const double s0 = __shfl_sync(0xffffffffu, c[0], src), s1 = __shfl_sync(0xffffffffu, c[1], src),
+                         s2 = __shfl_sync(0xffffffffu, c[2], src), sr = __shfl_sync(0xffffffffu, r, src);
+            const double sc[3] = {s0, s1, s2};
+            int tot = 0;
+            for (int b = 0; b < sn; b += 32) {
+                const int t = b + lane;
+                const bool pass = t < sn && fisheye_tile_pass(cam, sc, sr, cth, sth, sx + t % sw,
+                                                              sy + t / sw, tdir);
+                tot += __popc(__ballot_sync(0xffffffffu, pass));
+            }
+            if (lane == src) my_cnt = tot;
+        }
+        if (live) {
+            rect[i] = my_cnt ? cand : make_int4(0, 0, 0, 0);
+            count[i] = my_cnt;
+        }
+        return;
+    }
     if (i >= N) return;
     const float *M = cam.M;
     float v0 = __fsub_rn(sites[3 * i + 0], M[3]);
@@ -337,25 +387,6 @@ k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights
     keybits[i] = order_bits(K);
     int4 rc = make_int4(0, 0, 0, 0);
     int cnt = 0;
-    if (cam.model == PF_FISHEYE) {
-        double c[3];
-        camera_coords(cam, sites + 3 * i, c);
-        const double dist = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
-        if ((r > 0.0f) && !(dist + r <= (double)cam.near_plane)) {
-            const int T = cam.tiles_x * cam.tiles_y;
-            const double th = fisheye_half_angle(cam), cth = __ldg(tdir + 3 * T),
-                         sth = __ldg(tdir + 3 * T + 1);
-            int4 cand;
-            fisheye_rect(cam, c, r, th, cand);
-            for (int ty = cand.y; ty < cand.w; ++ty)
-                for (int tx = cand.x; tx < cand.z; ++tx)
-                    cnt += fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir) ? 1 : 0;
-            if (cnt) rc = cand;
-        }
-        rect[i] = rc;
-        count[i] = cnt;
-        return;
-    }
     if ((__fadd_rn(cz, r) > cam.near_plane) && (r > 0.0f)) {
         bool in_front = __fsub_rn(cz, r) > cam.near_plane;
         float xlo, xhi, ylo, yhi;
@@ -578,8 +609,9 @@ k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__rest
     }
 }
 
-// fisheye emission: one thread per cell re-tests the tiles of its candidate
-// rectangle (the count from K1 is the number that pass)
+// fisheye emission: the warp's 32 cells one after another, the lanes over the
+// cell's candidate tiles (re-tested; the count from K1 is the number that pass),
+// passing tiles compacted by ballot so the key/value stores are contiguous
 __global__ void __launch_bounds__(256)
 k3_emit_fisheye(int64_t N, CamParams cam, const float *__restrict__ sites,
                 const float *__restrict__ radii, const int4 *__restrict__ rect,
@@ -588,24 +620,40 @@ k3_emit_fisheye(int64_t N, CamParams cam, const float *__restrict__ sites,
                 uint32_t *__restrict__ vals, unsigned long long view_key,
                 const double *__restrict__ tdir)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N || count[i] == 0) return;
-    const int4 rc = rect[i];
-    double c[3];
-    camera_coords(cam, sites + 3 * i, c);
+    const int lane = threadIdx.x & 31;
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
+    if (i0 >= N) return;
+    const int64_t i = i0 + lane;
+    int cnt = 0;
+    if (i < N) cnt = count[i];
+    unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);
     const int T = cam.tiles_x * cam.tiles_y;
     const double cth = __ldg(tdir + 3 * T), sth = __ldg(tdir + 3 * T + 1);
-    const double r = radii[i];
-    const uint32_t k = keybits[i];
-    uint32_t o = offs[i];
-    for (int ty = rc.y; ty < rc.w; ++ty)
-        for (int tx = rc.x; tx < rc.z; ++tx)
-            if (fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir)) {
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t cell = i0 + src;
+        const int4 rc = rect[cell];
+        double c[3];
+        camera_coords(cam, sites + 3 * cell, c);
+        const double r = radii[cell];
+        const uint32_t k = keybits[cell];
+        uint32_t o = offs[cell];
+        const int w = rc.z - rc.x, n = w * (rc.w - rc.y);
+        for (int b = 0; b < n; b += 32) {
+            const int t = b + lane;
+            const int tx = rc.x + (w ? t % w : 0), ty = rc.y + (w ? t / w : 0);
+            const bool pass = t < n && fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir);
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                const uint32_t q = o + __popc(m & ((1u << lane) - 1u));
                 const unsigned long long tile = (unsigned long long)(ty * cam.tiles_x + tx);
-                keys[o] = view_key | (tile << 32) | k;
-                vals[o] = (uint32_t)i;
-                ++o;
+                keys[q] = view_key | (tile << 32) | k;
+                vals[q] = (uint32_t)cell;
             }
+            o += __popc(m);
+        }
+    }
 }
 
 cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
