@@ -580,3 +580,83 @@ def test_detail_abi_errors():
     with pytest.raises(pf.PFError):       # misaligned (float4 loads need 16-byte alignment)
         pf.Renderer(s, w, rr, d, c, o, i, normals=n, detail=dict(det, sv=sv_off))
     base.close()
+
+
+# --------------------------------------------------------------- edge cases
+
+def _parity_one(sc, cams, mode=oracle.O3, seed=29, flags=None):
+    r = renderer(sc, flags)
+    H, W = cams[0].height, cams[0].width
+    out = r.forward(cams).cpu().numpy().astype(np.float64)
+    for v, cam in enumerate(cams):
+        ref = oracle.render(sc, cam, mode=mode)["out"]
+        assert np.abs(out[v] - ref).max() <= IMG_TOL
+    g = pf_synth.make_grad_out(len(cams), H, W, seed=seed)
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    ref = None
+    for v, cam in enumerate(cams):
+        o = oracle.backward(sc, cam, g[v], mode=mode)
+        ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
+    grad_check(got, ref)
+    r.close()
+    return out
+
+
+@pytest.mark.parametrize("W,H", [(37, 23), (1, 1), (17, 200), (130, 9)])
+def test_edge_odd_image_sizes(W, H):
+    """Images that are not multiples of the 16x16 tile nor of the 8x4 warp block."""
+    sc, cams = case("small")
+    cam = cams[0]
+    s = min(W / cam.width, H / cam.height)
+    c = pf_synth.Camera(W, H, cam.fx * s, cam.fy * s, W / 2.0, H / 2.0, cam.c2w.copy(), cam.near)
+    _parity_one(sc, [c])
+
+
+def test_edge_no_pairs_camera_looking_away():
+    """No cell in view: background with T = 1 everywhere and zero gradients."""
+    sc, cams = case("small")
+    cam = cams[0]
+    M = np.asarray(cam.c2w, np.float32).reshape(3, 4).copy()
+    M[:, :3] = -M[:, :3]          # flip the viewing direction (keeps a rotation: det = -1?)
+    M[:, 0] = -M[:, 0]            # restore a proper rotation
+    eye = M[:, 3]
+    M[:, 3] = eye * 3.0           # far outside the foam, looking outward
+    c = pf_synth.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, M.reshape(12), cam.near)
+    sc2 = sc.copy()
+    sc2.background = (0.25, 0.5, 0.75)
+    r = renderer(sc2)
+    out = r.forward([c]).cpu().numpy()
+    assert r.pair_counts(1) == [0]
+    assert np.array_equal(out[0, ..., 3], np.ones((c.height, c.width), np.float32))
+    assert np.allclose(out[0, ..., :3], np.float32([0.25, 0.5, 0.75]), atol=0)
+    g = torch.from_numpy(pf_synth.make_grad_out(1, c.height, c.width, seed=1)).cuda()
+    got = r.backward([c], g)
+    for k in ("sites", "weights", "radii", "density", "rgb"):
+        assert float(got[k].abs().max()) == 0.0
+    r.close()
+
+
+def test_edge_single_cell():
+    """N = 1, no neighbours (E = 0): the bounded cell is the sphere."""
+    from helpers import camera, scene_from
+    sc = scene_from([[0.05, -0.02, 0.1]], radii=[0.4], density=[3.0], rgb=[[0.2, 0.7, 0.4]],
+                    bg=(0.1, 0.1, 0.1))
+    _parity_one(sc, [camera(W=48, H=40, f=60.0)], mode=oracle.O1)
+
+
+def test_edge_dense_single_tile_long_list():
+    """Thousands of cells behind one 16x16 tile: a list spanning ~100 chunks of 32,
+    most of them culled per warp, and early termination deep in the list."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    P = rng.normal(scale=0.15, size=(n, 3)).astype(np.float32)
+    r, off, idx = pf_synth.knn_cech_lists(P, 8, rng, cech_filter=True)
+    from helpers import scene_from, camera
+    sc = scene_from(P, r, density=np.full(n, 25.0, np.float32),
+                    rgb=rng.uniform(0, 1, size=(n, 3)).astype(np.float32), lists=(off, idx))
+    cam = camera(W=16, H=16, f=30.0, eye=(0.0, 0.0, -2.0))
+    r_ = renderer(sc)
+    b = r_.debug_binning(cam)
+    assert b["P"] > 0.8 * n      # (nearly) every cell lands in the one tile
+    r_.close()
+    _parity_one(sc, [cam])
