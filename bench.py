@@ -346,18 +346,47 @@ def main():
     e2e = None
     if not args.no_e2e:
         g_host = grad_out.cpu().pin_memory() if train else None
-        res_host = (torch.empty(r.grad_size, dtype=torch.float32) if train
-                    else torch.empty(out.shape, dtype=torch.float32)).pin_memory()
-        g_dev = torch.empty_like(grad_out)
+        res_host = [(torch.empty(r.grad_size, dtype=torch.float32) if train
+                     else torch.empty(out.shape, dtype=torch.float32)).pin_memory()
+                    for _ in range(2)]
+        # double-buffered device copies; H2D and D2H on their own streams (PCIe is
+        # full duplex): the step's dL/dimage uploads while its forward runs (the
+        # forward does not read it), its gradients download while the next
+        # step's forward runs.  Every step still moves its own bytes both ways.
+        g_dev = [torch.empty_like(grad_out) for _ in range(2)]
+        flats = [flat, torch.zeros_like(flat)]
+        outs = [out, torch.empty_like(out)]
+        h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("h2d", "used", "d2h")}
+        for b in range(2):
+            for k in ev:
+                ev[k][b].record(stream)
+        step_no = [0]
 
         def e2e_step():
+            b = step_no[0] & 1
+            step_no[0] += 1
             if train:   # the step's dL/dimage arrives from the host, grads go back
-                g_dev.copy_(g_host, non_blocking=True)
-                pfd.train_step(r, cams, g_dev, flat, out=out)
-                res_host.copy_(flat, non_blocking=True)
+                with torch.cuda.stream(h2d):
+                    h2d.wait_event(ev["used"][b])        # step k-2's backward read g_dev[b]
+                    g_dev[b].copy_(g_host, non_blocking=True)
+                    ev["h2d"][b].record(h2d)
+                stream.wait_event(ev["d2h"][b])          # step k-2's download of flats[b]
+                pfd.train_step(r, cams, g_dev[b], flats[b], out=out,
+                               before_backward=lambda: stream.wait_event(ev["h2d"][b]))
+                ev["used"][b].record(stream)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(ev["used"][b])
+                    res_host[b].copy_(flats[b], non_blocking=True)
+                    ev["d2h"][b].record(d2h)
             else:       # forward-only: the rendered images go back to the host
-                r.forward(cams, out=out)
-                res_host.copy_(out, non_blocking=True)
+                stream.wait_event(ev["d2h"][b])
+                r.forward(cams, out=outs[b])
+                ev["used"][b].record(stream)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(ev["used"][b])
+                    res_host[b].copy_(outs[b], non_blocking=True)
+                    ev["d2h"][b].record(d2h)
 
         for _ in range(2):
             e2e_step()
@@ -366,6 +395,8 @@ def main():
         a0.record(stream)
         for _ in range(args.steps):
             e2e_step()
+        for b in range(2):                               # the last downloads are in the region
+            stream.wait_event(ev["d2h"][b])
         a1.record(stream)
         barrier()
         te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
@@ -373,9 +404,10 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": ws * nv / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(g_host.numel() * 4) if train else 64 * nv,
-               "d2h_bytes_per_step": int(res_host.numel() * 4),
-               "note": ("H2D of the step's dL/dimage from pinned host + fwd + bwd "
-                        "(+ all-reduce) + D2H of the per-cell gradients, every step") if train
+               "d2h_bytes_per_step": int(res_host[0].numel() * 4),
+               "note": ("H2D of the step's dL/dimage from pinned host (overlapping its "
+                        "forward) + fwd + bwd (+ all-reduce) + D2H of the per-cell gradients "
+                        "(overlapping the next forward), every step") if train
                else "fwd through the C-ABI (host cameras) + D2H of the rendered images, every step"}
 
     # ---------------- counters -> algorithmic flops, roofline ----------------

@@ -48,12 +48,17 @@ def sharded_backward(local_views: Sequence, backward_fn: Callable, flat: torch.T
 
 
 def train_step(renderer, cams_local: Sequence, grad_out_local: torch.Tensor, flat: torch.Tensor,
-               out: torch.Tensor | None = None, group=None):
+               out: torch.Tensor | None = None, group=None,
+               before_backward: Callable | None = None):
     """One data-parallel step on this rank: forward of the local views (one
-    batched call), backward into `flat` (f32[9N]), all-reduce of `flat`.
-    Returns (images, flat)."""
+    batched call), backward into `flat` (f32[grad_size]), all-reduce of `flat`.
+    before_backward() runs after the forward is enqueued (e.g. make the stream
+    wait for an asynchronous host->device copy of grad_out, which the forward
+    does not read).  Returns (images, flat)."""
     img = renderer.forward(list(cams_local), out=out)
     flat.zero_()
+    if before_backward is not None:
+        before_backward()
     renderer.backward(list(cams_local), grad_out_local, flat)
     allreduce_grads(flat, group)
     return img, flat
