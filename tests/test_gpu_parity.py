@@ -72,6 +72,12 @@ def grad_check(gpu, ref, tol=GRAD_TOL):
         rel = np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
         msgs.append(f"{k}: {rel:.2e}")
         assert rel <= tol, ", ".join(msgs)
+        # secondary, per cell: |g_i - g_ref,i| <= 1e-3 |g_ref,i| + 1e-5 max |g_ref|
+        N = ref["density"].shape[0]
+        ac, bc = a.reshape(N, -1), b.reshape(N, -1)
+        ni = np.linalg.norm(bc, axis=1)
+        bad = np.linalg.norm(ac - bc, axis=1) > 1e-3 * ni + 1e-5 * ni.max()
+        assert bad.sum() <= 1e-3 * (ni > 0).sum(), (k, np.flatnonzero(bad)[:10])
     return msgs
 
 
