@@ -6,8 +6,9 @@
 //            (2) exclusive scan of that array (the K2 scan kernels),
 //            (3) stable scatter: warp-level multisplit ranking with
 //                __match_any_sync, per-warp digit counters in shared memory,
-//                block prefix over warps, global base from the scan.
-// Stability: warp w of block b owns keys [b*4096 + w*32*I, +32*I) in I rounds of
+//                block prefix over warps, then a block-local shuffle through
+//                shared memory so each digit's run is stored contiguously.
+// Stability: warp w of block b owns keys [b*TILE + w*32*I, +32*I) in I rounds of
 // 32 consecutive keys; ranks follow (round, lane) = input order.
 #include <cuda_runtime.h>
 
@@ -21,7 +22,10 @@ cudaError_t exclusive_scan_counts(pf_scene *s, const int *cnt, int64_t n, uint32
 #ifndef PF_SORT_THREADS
 #define PF_SORT_THREADS 512
 #endif
-constexpr int kSortThreads = PF_SORT_THREADS, kSortItems = 4096 / PF_SORT_THREADS,
+#ifndef PF_SORT_TILE
+#define PF_SORT_TILE 4096
+#endif
+constexpr int kSortThreads = PF_SORT_THREADS, kSortItems = PF_SORT_TILE / PF_SORT_THREADS,
               kSortTile = kSortThreads * kSortItems, kSortWarps = kSortThreads / 32;
 constexpr int kRadixBits = 8, kRadix = 1 << kRadixBits;
 
@@ -51,17 +55,32 @@ k4_histogram(const unsigned long long *__restrict__ keys, int64_t n, int shift, 
     }
 }
 
+// Scatter with a block-local shuffle: every key gets its position inside the
+// block's digit-sorted tile (digit start + warp prefix + rank), the tile is
+// staged in shared memory, and the threads then write it out in tile order, so
+// each digit's run (about 16 keys per block) goes to consecutive addresses:
+// coalesced stores instead of one scattered 8-byte store per key.
+constexpr size_t kScatterSmem = (size_t)kSortTile * (sizeof(unsigned long long) + sizeof(uint32_t)) +
+                                (size_t)kSortWarps * kRadix * sizeof(uint32_t) +
+                                2 * kRadix * sizeof(uint32_t);
+
 __global__ void __launch_bounds__(kSortThreads)
 k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restrict__ vin,
            unsigned long long *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
            int shift, int nb, const uint32_t *__restrict__ digit_offs)
 {
-    __shared__ uint32_t wh[kSortWarps][kRadix];
+    extern __shared__ __align__(16) unsigned char sort_smem[];
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(sort_smem);
+    uint32_t *sv = reinterpret_cast<uint32_t *>(sk + kSortTile);
+    uint32_t(*wh)[kRadix] = reinterpret_cast<uint32_t(*)[kRadix]>(sv + kSortTile);
+    uint32_t *dstart = reinterpret_cast<uint32_t *>(wh + kSortWarps);
+    uint32_t *gbase = dstart + kRadix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int q = threadIdx.x; q < kSortWarps * kRadix; q += kSortThreads) (&wh[0][0])[q] = 0;
     __syncthreads();
     const unsigned lt_mask = (1u << lane) - 1u;
-    int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (32 * kSortItems);
+    const int64_t bbase = (int64_t)blockIdx.x * kSortTile;
+    const int64_t wbase = bbase + (int64_t)warp * (32 * kSortItems);
     unsigned long long key[kSortItems];
     uint32_t val[kSortItems], rank[kSortItems];
     int dig[kSortItems];
@@ -86,23 +105,56 @@ k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restric
         dig[r] = d;
     }
     __syncthreads();
+    // per digit: warp prefixes, block total, global base of this block's run
     for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
-        uint32_t run = digit_offs[(int64_t)d * nb + blockIdx.x];
+        uint32_t run = 0;
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
-            uint32_t c = wh[w][d];
+            const uint32_t c = wh[w][d];
             wh[w][d] = run;
             run += c;
+        }
+        dstart[d] = run;
+        gbase[d] = digit_offs[(int64_t)d * nb + blockIdx.x];
+    }
+    __syncthreads();
+    if (warp == 0) {   // exclusive scan of the 256 digit totals (8 per lane)
+        uint32_t v[kRadix / 32], sum = 0;
+#pragma unroll
+        for (int q = 0; q < kRadix / 32; ++q) {
+            v[q] = dstart[lane * (kRadix / 32) + q];
+            sum += v[q];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int q = 0; q < kRadix / 32; ++q) {
+            dstart[lane * (kRadix / 32) + q] = run;
+            run += v[q];
         }
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         if (dig[r] < kRadix) {
-            uint32_t pos = wh[warp][dig[r]] + rank[r];
-            kout[pos] = key[r];
-            vout[pos] = val[r];
+            const uint32_t lp = dstart[dig[r]] + wh[warp][dig[r]] + rank[r];
+            sk[lp] = key[r];
+            sv[lp] = val[r];
         }
+    }
+    __syncthreads();
+    const int nvalid = (int)min((int64_t)kSortTile, n - bbase);
+    for (int q = threadIdx.x; q < nvalid; q += kSortThreads) {
+        const unsigned long long k = sk[q];
+        const int d = (int)((k >> shift) & (kRadix - 1));
+        const uint32_t pos = gbase[d] + ((uint32_t)q - dstart[d]);
+        kout[pos] = k;
+        vout[pos] = sv[q];
     }
 }
 
@@ -124,13 +176,14 @@ cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64
     uint32_t *va = vals, *vb = vals_alt;
     bool alt = false;
     cudaEvent_t ev;
+    cudaFuncSetAttribute(k4_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem);
     stage_begin(s, 4, st, &ev);
     for (int shift = 0; shift < end_bit; shift += kRadixBits) {
         k4_histogram<<<nb, kSortThreads, 0, st>>>(ka, n, shift, nb, hist);
         ++s->launches;
         err = exclusive_scan_counts(s, hist, (int64_t)hist_n, offs, dummy_total, st);
         if (err != cudaSuccess) return err;
-        k4_scatter<<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, nb, offs);
+        k4_scatter<<<nb, kSortThreads, kScatterSmem, st>>>(ka, va, kb, vb, n, shift, nb, offs);
         ++s->launches;
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
