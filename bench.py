@@ -449,6 +449,27 @@ def main():
     sort_gbs = sort_bytes / (sort_ms / max(sort_n, 1) / 1e3) / 1e9 if sort_ms > 0 else None
     hbm = float(peaks.get("hbm_gbs", 6650.0))
 
+    # ---------------- whole-step rooflines (SURVEY §8(d) byte and flop models) -------
+    bcount = r.debug_binning(cams[0])["count"]
+    n_vis = float((bcount > 0).sum().item())
+    deg_mean = sc.num_edges / max(N, 1)
+    T_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+    pix = W * H
+    b_view = (36 * N + 8 * N + 16 * n_vis + 12 * P + 8 * P + 8 * T_tiles
+              + n_vis * (48 + 16 * deg_mean) + 4 * P + 24 * pix)
+    if train:
+        b_view += n_vis * (48 + 16 * deg_mean) + 4 * P + 24 * pix + 72 * n_vis + 16 * pix
+    b_step = nv * b_view + sort_bytes
+    f_step = nv * (f_bwd if train else f_fwd)
+    step_s = (ms_step if train else float(tf.item())) / 1e3   # this rank's step
+    roofline_step = {
+        "fp32_frac": f_step / step_s / (fp32_peak * 1e12),
+        "hbm_frac": b_step / step_s / (hbm * 1e9),
+        "flops_per_step": f_step, "bytes_per_step": b_step,
+        "model": "SURVEY 8(d): B_K1..K6 (+ backward) per view + the measured sort passes; "
+                 "F_fwd/F_bwd from the counters; N_vis from view 0's binning",
+    }
+
     # ---------------- NEXT-3: GPU Čech graph build of this scene (extra) --------
     cech = None
     try:
@@ -493,9 +514,11 @@ def main():
                        "global_batch_views": nv * ws, "width": W, "height": H,
                        "pass": "fwd+bwd" if train else "fwd",
                        "parallelism": f"dp{ws} (views sharded, per-cell grad all-reduce)",
-                       "l2": "inputs larger than L2 (scene records+edges+grad_out > 126 MB)"},
+                       "l2": "inputs larger than L2 (scene records+edges+grad_out > 126 MB)",
+                       "k0_policy": "edge records rebuilt every step (training)" if train
+                       else "static scene: edge records built once at creation"},
             "clocks": clocks, "gpu_launches": int(launches),
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": roofline, "roofline_step": roofline_step, "cpu_baseline": cpu,
             "fwd_fps": fwd_fps, "fwdbwd_fps": fps if train else None,
             "mpix_s": (fps if train else fwd_fps) * W * H / 1e6, "fwd_mpix_s": fwd_fps * W * H / 1e6,
             "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
