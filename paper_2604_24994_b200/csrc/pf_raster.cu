@@ -613,6 +613,9 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K7_MINB
 #define PF_K7_MINB 4
 #endif
+#ifndef PF_K7_DIRECT_MAX   // up to this many segment lanes: per-lane atomics, no warp reduction
+#define PF_K7_DIRECT_MAX 10
+#endif
 #ifndef PF_K7D_MINB
 #define PF_K7D_MINB 2
 #endif
@@ -1254,7 +1257,7 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
     __syncwarp();
     // own-cell terms (rgb_i is unused by detail cells: no colour gradient)
     float *accc = acc + 12 * (size_t)cell;
-    if (__popc(segm) == 1) {
+    if (__popc(segm) <= PF_K7_DIRECT_MAX) {
         if (seg) {
             atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
             atomicAdd(reinterpret_cast<float4 *>(accc) + 2, make_float4(0.0f, o.nx, o.ny, o.nz));
@@ -1315,7 +1318,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
     // reduction then one 9-lane atomic instruction
     float *accc = acc + 12 * (size_t)S.cell[j];
     const unsigned sm = __ballot_sync(0xffffffffu, seg);
-    if (__popc(sm) == 1) {
+    if (__popc(sm) <= PF_K7_DIRECT_MAX) {
         if (seg) {
             atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
             if (dipole)
