@@ -109,11 +109,16 @@ int reserve_view_bins(pf_scene *s, pf::ViewState &v)
 int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
                      uint64_t **keys_out)
 {
+    // Views are sorted in batches of up to kSortViews: the view id takes the bits
+    // above the tile id, and more than 8 views would add a radix pass for every
+    // pair (51 bits = 7 passes for 64 views at 1080p instead of 48 = 6).
+    constexpr int kSortViews = 8;
     const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     const int tb = tile_bits(T);
+    const int Vb = V < kSortViews ? V : kSortViews;
     int vb = 0;
-    while ((1 << vb) < V) ++vb;
-    if (32 + tb + vb > 64) return fail(PF_ERR_INVALID_ARGUMENT, "too many views for 64-bit keys");
+    while ((1 << vb) < Vb) ++vb;
+    if (32 + tb + vb > 64) return fail(PF_ERR_INVALID_ARGUMENT, "too many tiles for 64-bit keys");
     int64_t Ptot = 0;
     for (int v = 0; v < V; ++v) {
         views[v].pair_off = Ptot;
@@ -129,24 +134,36 @@ int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
     PF_CUDA(s->ranges_all.reserve(sizeof(uint2) * (size_t)T * V));
     uint64_t *k0 = s->keys0.as<uint64_t>(), *k1 = s->keys1.as<uint64_t>();
     uint32_t *v0 = s->vals_all.as<uint32_t>(), *v1 = s->vals1.as<uint32_t>();
-    for (int v = 0; v < V; ++v) {
-        if (views[v].P == 0) continue;
-        PF_CUDA(pf::launch_emit(s, views[v], k0 + views[v].pair_off, v0 + views[v].pair_off,
-                                (uint64_t)v << (32 + tb), st));
-    }
-    bool alt = false;
-    if (Ptot > 0) {
-        PF_CUDA(pf::radix_sort_pairs(s, k0, v0, k1, v1, Ptot, 32 + tb + vb, &alt, st));
-        if (alt) PF_CUDA(cudaMemcpyAsync(v0, v1, 4 * (size_t)Ptot, cudaMemcpyDeviceToDevice, st));
-    }
-    uint64_t *ks = alt ? k1 : k0;
     uint2 *rall = s->ranges_all.as<uint2>();
-    PF_CUDA(pf::launch_ranges(s, ks, Ptot, T, tb, rall, V, st));
+    uint64_t *ks = k0;
+    for (int b0 = 0; b0 < V; b0 += kSortViews) {
+        const int b1 = (b0 + kSortViews < V) ? b0 + kSortViews : V;
+        const int64_t off = views[b0].pair_off;
+        const int64_t Pb = views[b1 - 1].pair_off + views[b1 - 1].P - off;
+        for (int v = b0; v < b1; ++v) {
+            if (views[v].P == 0) continue;
+            PF_CUDA(pf::launch_emit(s, views[v], k0 + views[v].pair_off, v0 + views[v].pair_off,
+                                    (uint64_t)(v - b0) << (32 + tb), st));
+        }
+        bool alt = false;
+        if (Pb > 0) {
+            PF_CUDA(pf::radix_sort_pairs(s, k0 + off, v0 + off, k1 + off, v1 + off, Pb, 32 + tb + vb,
+                                         &alt, st));
+            if (alt) {
+                PF_CUDA(cudaMemcpyAsync(v0 + off, v1 + off, 4 * (size_t)Pb, cudaMemcpyDeviceToDevice, st));
+                PF_CUDA(cudaMemcpyAsync(k0 + off, k1 + off, 8 * (size_t)Pb, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        // ranges of this batch's views, relative to the batch's first pair
+        PF_CUDA(pf::launch_ranges(s, k0 + off, Pb, T, tb, rall + (size_t)b0 * T, b1 - b0, st));
+        for (int v = b0; v < b1; ++v) {
+            views[v].vals_p = v0 + off;
+            views[v].ranges_p = rall + (size_t)v * T;
+        }
+    }
     PF_CUDA(s->order_all.reserve(sizeof(uint32_t) * (size_t)T * V));
     PF_CUDA(s->chunk_off_all.reserve(sizeof(uint32_t) * (size_t)T * V));
     for (int v = 0; v < V; ++v) {
-        views[v].vals_p = v0;
-        views[v].ranges_p = rall + (size_t)v * T;
         views[v].order = s->order_all.as<uint32_t>() + (size_t)v * T;
         views[v].chunk_off = s->chunk_off_all.as<uint32_t>() + (size_t)v * T;
     }

@@ -171,6 +171,33 @@ def test_multiview_equals_single_view_and_deterministic():
     r.close()
 
 
+def test_many_views_in_one_call_batched_sorts():
+    """More than 8 views in one call are sorted in batches of 8 (DESIGN §6 K4): every
+    view equals its single-view render bit for bit, and the multi-view backward
+    equals the sum of the single-view backwards (up to atomic summation order)."""
+    sc, _ = case("small360")
+    cams = pf_synth.make_cameras("small360", n=11)
+    r = renderer(sc)
+    multi = r.forward(cams).cpu().numpy()
+    for v, cam in enumerate(cams):
+        single = r.forward([cam]).cpu().numpy()[0]
+        assert np.array_equal(single, multi[v]), v
+    H, W = cams[0].height, cams[0].width
+    g = torch.from_numpy(pf_synth.make_grad_out(len(cams), H, W, seed=5)).cuda()
+    r.forward(cams)
+    got = {k: v.clone() for k, v in r.backward(cams, g).items()}
+    acc = None
+    for v, cam in enumerate(cams):
+        r.forward([cam])
+        one = r.backward([cam], g[v:v + 1].contiguous())
+        acc = {k: x.clone() for k, x in one.items()} if acc is None else \
+            {k: acc[k] + one[k] for k in acc}
+    for k in got:
+        a, b = got[k].double(), acc[k].double()
+        assert float((a - b).norm()) <= 1e-5 * float(b.norm()) + 1e-12, k
+    r.close()
+
+
 # --------------------------------------------------------------- backward
 
 @pytest.mark.parametrize("name,variant", [("tiny", "outside"), ("tiny", "inside"),
