@@ -234,8 +234,9 @@ def cpu_baseline(sc, cam, seconds, train=True, calib=None):
                       f"-> {frame:.1f}s per frame"}
 
 
-def load_traffic(kernel_tag):
-    """DRAM bytes per launch of a kernel from the newest committed ncu export."""
+def load_traffic(kernel_tag, full=False):
+    """DRAM bytes per launch of a kernel from the newest committed ncu export
+    (full=True: the whole record, incl. the warp-instruction count)."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
     for f in reversed(files):
@@ -244,8 +245,10 @@ def load_traffic(kernel_tag):
         except Exception:
             continue
         if kernel_tag in d:
+            if full:
+                return d[kernel_tag]
             return d[kernel_tag]["traffic_bytes"], d[kernel_tag]["source"]
-    return None, None
+    return None if full else (None, None)
 
 
 # ----------------------------------------------------------------------------
@@ -428,8 +431,9 @@ def main():
     d_avg = d_ms / max(d_n, 1)
     d_flops = f_bwd if dom == "K7_backward" else f_fwd
     achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
-    traffic, traffic_src = load_traffic(("k7_backward" if dom == "K7_backward" else "k6_forward")
-                                        + ("_detail" if args.detail else ""))
+    ktag = ("k7_backward" if dom == "K7_backward" else "k6_forward") + ("_detail" if args.detail else "")
+    traffic, traffic_src = load_traffic(ktag)
+    prof = load_traffic(ktag, full=True) or {}
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write)",
@@ -438,6 +442,19 @@ def main():
                              f"{sm_max:.0f} MHz (guide unit counts; no tensor-core path)",
                 "avg_launch_ms": d_avg,
                 "algorithmic_flops_per_launch": d_flops}
+    if prof.get("warp_inst") and d_avg > 0:
+        # the SM issue roofline: 4 schedulers x 148 SMs x clock warp-instructions/s
+        issue_peak = 4 * SM_COUNT * sm_max * 1e6
+        roofline["issue"] = {
+            "warp_inst_per_launch": prof["warp_inst"],
+            "achieved_ginst_s": prof["warp_inst"] / (d_avg / 1e3) / 1e9,
+            "peak_ginst_s": issue_peak / 1e9,
+            "frac": prof["warp_inst"] / (d_avg / 1e3) / issue_peak,
+            "ncu_issue_pct": prof.get("issue_pct_of_peak"),
+            "note": "instruction count of one launch from the committed ncu capture "
+                    "(same kernel, same workload); the FP32 fraction is below this because "
+                    "the plane test is ~17 instructions for 16 algorithmic flops "
+                    "(selects, min/max, MUFU rcp)"}
     sort_ms, sort_n = stages["K4_sort"]
     pairs = r.pair_counts(nv)
     P = float(np.mean(pairs))

@@ -74,7 +74,8 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
        "smsp__issue_active.avg.pct_of_peak_sustained_active",
        "smsp__thread_inst_executed_per_inst_executed.ratio",
-       "sm__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+       "smsp__inst_executed.sum", "sm__inst_executed.sum.pct_of_peak_sustained_elapsed",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum"]
 traffic = OrderedDict()
 for rep in sorted(f for f in os.listdir(src) if f.startswith("prof_") and f.endswith(".ncu-rep")):
@@ -124,5 +125,10 @@ for rep in sorted(f for f in os.listdir(src) if f.startswith("prof_") and f.ends
                          "source": f"profiles/{tag}_{name}_full.txt (ncu --set full, 1 launch)"}
         traffic[name]["traffic_bytes"] = (traffic[name]["dram_read_bytes"]
                                           + traffic[name]["dram_write_bytes"])
+        if "smsp__inst_executed.sum" in vals:
+            traffic[name]["warp_inst"] = float(vals["smsp__inst_executed.sum"][0].replace(",", ""))
+        if "sm__inst_executed.sum.pct_of_peak_sustained_elapsed" in vals:
+            traffic[name]["issue_pct_of_peak"] = float(
+                vals["sm__inst_executed.sum.pct_of_peak_sustained_elapsed"][0].replace(",", ""))
 json.dump(traffic, open(os.path.join(out, f"{tag}_traffic.json"), "w"), indent=1)
 print("wrote", sorted(os.listdir(out)))
