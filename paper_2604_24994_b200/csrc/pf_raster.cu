@@ -15,6 +15,7 @@
 // atomic per warp, neighbour terms as float4 atomics.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "pf_internal.cuh"
 
@@ -88,6 +89,7 @@ struct WarpStage {
     float sig[32], cr[32], cg[32], cb[32];
     float4 *nrm;                    // dipole normals (NEXT-1) of the slots: separate smem, or null
     uint32_t eb[32], deg[32], cell[32];
+    float smax[32], rhom[32];       // K6 plane cull: chord bound and rho + M/|n| (cull_planes)
 };
 
 // Per-pixel exact ray (fp64), read only by the near-tangent path.
@@ -98,6 +100,8 @@ struct PixelRays {
 struct WarpCtx {           // one per warp, in shared memory
     double wx, wy, wz;     // warp-centre direction d_w
     double cos_t, sin_t;   // half-angle of the cone containing the warp's pixel rays
+    float fwx, fwy, fwz;   // d_w rounded to fp32 (plane cull)
+    float tan_t;           // tan of the half-angle, rounded up (plane cull)
 };
 
 // ---- the per-(pixel, cell) math shared verbatim by K6 and K7 -------------
@@ -225,6 +229,110 @@ __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__rest
     g.dt = (active && dt > 0.0f) ? dt : 0.0f;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-level plane cull (K6).  All rays of the warp lie in the cone (d_w, th),
+// so every chord point x of cell i seen by the warp lies in the cylinder
+//   x - p_i = t' d_w - e0 + v,   |t'| <= s_max,  v _|_ d_w,  |v| <= rho,
+//   rho = (t0 + r) tan(th),  s_max = sqrt(r^2 - max(0, |e0| - rho)^2)
+// (axial coordinate of a ball point <= t0 + r; radial <= axial tan(th)).  On it
+// the plane function f = a t' - b of neighbour j (a = d.n, b = k + n.e; the
+// cell keeps f <= 0) ranges within  -b +- (|d_w.n| s_max + rho |n|)  with
+// b_w = k + n.e0.  Lane k tests plane k at once:
+//   sup f < -M  : plane k cannot bind for any pixel of the warp -> dropped
+//                 (fminf/fmaxf with a strictly non-binding value is the identity,
+//                 so the interval is bit-identical to clipping by every plane);
+//   inf f >  M  : the warp's beam through B_i lies in j's cell: every pixel's
+//                 interval is empty -> the whole cell is skipped.
+// The ball radius is inflated by 1e-5 (|t0| + |e0| + r) and M = 1e-5 (|k| +
+// |n| (|e0| + r + |t0|)) so fp32 rounding of the staged frame, the lanes' own
+// rounding and the fp64 near-tangent path (exact centre) are all covered.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float sqrt_apx(float x)   // sqrt.approx (rel. error ~1e-7)
+{
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+struct PlaneBuf {
+    float4 E[32];          // kept edge records (n, k) of the current cell
+    uint8_t q[32];         // their index in the cell's neighbour list
+};
+
+// Per-slot constants of the plane cull, computed by the staging lane.
+__device__ __forceinline__ void cull_consts(WarpStage &S, int slot, const WarpCtx &W)
+{
+    const float t0 = S.t0[slot], ex = S.e0x[slot], ey = S.e0y[slot], ez = S.e0z[slot];
+    const float en = sqrt_apx(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
+    const float r = S.r[slot] + 1e-5f * (fabsf(t0) + en + S.r[slot]);
+    const float rho = fmaxf(t0 + r, 0.0f) * W.tan_t * 1.00001f;
+    const float off = fmaxf(en - rho - 1e-5f * (en + rho), 0.0f);
+    S.smax[slot] = sqrt_apx(fmaxf(r - off, 0.0f) * (r + off)) * 1.00001f;
+    S.rhom[slot] = fmaf(1e-5f, en + r + fabsf(t0), rho);   // rho + M / |n| (see above)
+}
+
+// Lane k tests plane k of slot j (deg <= 32) and the kept planes are compacted
+// into B in list order (an odd count is padded with a copy of the last plane:
+// min/max are idempotent and the tracking is strict, so the copy changes
+// nothing).  Returns -1 if every pixel's interval is empty, else the padded count.
+__device__ __forceinline__ int cull_planes(const WarpStage &S, int j, const WarpCtx &W,
+                                           const float4 *__restrict__ edges, PlaneBuf &B, int lane)
+{
+    const uint32_t deg = S.deg[j];
+    const float ex = S.e0x[j], ey = S.e0y[j], ez = S.e0z[j], smax = S.smax[j], rhom = S.rhom[j];
+    bool keep = false, kill = false;
+    float4 E = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if ((uint32_t)lane < deg) {
+        E = __ldg(edges + S.eb[j] + lane);
+        const float aw = fmaf(W.fwx, E.x, fmaf(W.fwy, E.y, W.fwz * E.z));
+        const float bw = fmaf(E.x, ex, fmaf(E.y, ey, fmaf(E.z, ez, E.w)));
+        const float nn = sqrt_apx(fmaf(E.x, E.x, fmaf(E.y, E.y, E.z * E.z)));
+        const float thr = fmaf(fabsf(aw), smax, fmaf(nn, rhom, 1e-5f * fabsf(E.w)));
+        keep = bw <= thr;
+        kill = bw < -thr;
+    }
+    if (__any_sync(0xffffffffu, kill)) return -1;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int n = __popc(m);
+    if (keep) {
+        const int p = __popc(m & ((1u << lane) - 1u));
+        B.E[p] = E;
+        B.q[p] = (uint8_t)lane;
+        if (p == n - 1 && (n & 1)) {
+            B.E[n] = E;
+            B.q[n] = (uint8_t)lane;
+        }
+    }
+    __syncwarp();
+    return (n + 1) & ~1;
+}
+
+// a9 over the planes kept by cull_planes (same per-plane math and order as
+// clip_interval; the tracked code is 2 + the plane's list index)
+template <bool kTrack, bool kDipole>
+__device__ __forceinline__ void clip_interval_kept(const Ray &R, const PlaneBuf &B, int n, Seg &g,
+                                                   bool active, const float4 &dplane)
+{
+    g.lo = -g.s;
+    g.lo_q = kEndSphere;
+    const float tnl = __fsub_rn(R.tnear, g.tc);
+    if (tnl > g.lo) {
+        g.lo = tnl;
+        g.lo_q = kEndNear;
+    }
+    g.hi = g.s;
+    g.hi_q = kEndSphere;
+    for (int k = 0; k < n; k += 2) {   // n is even (padded)
+        const float4 E0 = B.E[k], E1 = B.E[k + 1];
+        const uint32_t qq = kTrack ? *reinterpret_cast<const uint16_t *>(B.q + k) : 0u;
+        clip_plane<kTrack>(R, E0, (int)(qq & 0xffu) + 2, g);
+        clip_plane<kTrack>(R, E1, (int)(qq >> 8) + 2, g);
+    }
+    if (kDipole) clip_plane<kTrack>(R, dplane, kEndDipole, g);
+    const float dt = __fsub_rn(g.hi, g.lo);
+    g.dt = (active && dt > 0.0f) ? dt : 0.0f;
+}
+
 // a10: one front-to-back compositing step (alpha = 1 - exp(-sigma dt))
 __device__ __forceinline__ void composite_step(float sig, float dt, float cr, float cg, float cb,
                                                float &T, float &Cr, float &Cg, float &Cb,
@@ -283,6 +391,10 @@ __device__ __forceinline__ void setup_pixel(const CamParams &cam, int tile, Pixe
         W.wz = dw[2];
         W.cos_t = cs;
         W.sin_t = sqrt(fmax(0.0, 1.0 - cs * cs));
+        W.fwx = (float)dw[0];
+        W.fwy = (float)dw[1];
+        W.fwz = (float)dw[2];
+        W.tan_t = (float)(W.sin_t / fmax(cs, 1e-3) * (1.0 + 1e-6));
     }
     double d[3], tn;
     bool in_circle;
@@ -351,7 +463,7 @@ __device__ __forceinline__ double cell_offset(const CamParams &cam, const float4
 // Cone test: the sphere (c, r) meets the cone (axis d_w, half-angle th) iff
 // the angle between c and d_w is <= th + asin(r/|c|), i.e. (|c| > r)
 // d_w.c >= cos(th) sqrt(|c|^2 - r^2) - sin(th) r;  always if |c| <= r.
-template <bool kDipole>
+template <bool kDipole, bool kCull = false>
 __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene &ds,
                                                 const CamParams &cam,
                                                 const uint32_t *__restrict__ vals, uint32_t e,
@@ -376,7 +488,10 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
         }
     }
     const unsigned m = __ballot_sync(0xffffffffu, pass);
-    if (pass) stage_slot<kDipole>(S, lane, ds, cell, A, c0, c1, c2, t, W);
+    if (pass) {
+        stage_slot<kDipole>(S, lane, ds, cell, A, c0, c1, c2, t, W);
+        if (kCull) cull_consts(S, lane, W);
+    }
     __syncwarp();
     return m;
 }
@@ -592,8 +707,9 @@ constexpr uint32_t kOverflow = 0xffffffffu;
 constexpr int kRecWords = 18;   // mask, pos, 32 x u16 codes
 
 struct WarpRec {
-    uint32_t mask[32], pos[32];
+    uint32_t mask[32];
     uint32_t code[32][16];      // 32 lanes x u16, as 16 words
+    uint8_t pos[32];            // slot (list position within the chunk)
 };
 
 __device__ __forceinline__ uint32_t end_code(int q)
@@ -609,6 +725,9 @@ __device__ __forceinline__ uint32_t end_code(int q)
 // ------------------------------------------------------------------------
 #ifndef PF_K6_MINB
 #define PF_K6_MINB 4
+#endif
+#ifndef PF_K6_PCULL   // warp-level plane cull in K6 (cull_planes)
+#define PF_K6_PCULL 1
 #endif
 #ifndef PF_K7_MINB
 #define PF_K7_MINB 4
@@ -629,13 +748,18 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
            const uint32_t *__restrict__ chunk_off, uint2 *__restrict__ desc,
            uint32_t *__restrict__ wdone, uint32_t *__restrict__ rec, uint32_t *__restrict__ rec_used,
-           uint32_t rec_cap, float *__restrict__ st_contrib, float *__restrict__ st_normal)
+           uint32_t rec_cap, float *__restrict__ st_contrib, float *__restrict__ st_normal,
+           int cull_on)
 {
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
     __shared__ WarpRec WR[kRecord ? kWarps : 1];
     __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
+    // warp plane cull (plane_mask); the counting build evaluates every list plane
+    // so its X_p stays the SURVEY 8(d) work count
+    constexpr bool kCull = PF_K6_PCULL && !kCount;
+    extern __shared__ PlaneBuf PB[];   // kWarps entries when kCull (dynamic: static smem is full)
     const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
@@ -652,7 +776,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     uint32_t chunks = 0;
     for (uint32_t base = rg.x; base < rg.y; base += 32, ++chunks) {
         if (__all_sync(0xffffffffu, done)) break;
-        unsigned m = stage_chunk<kDipole>(S, ds, cam, vals, base + lane, rg.y, W, lane);
+        unsigned m = stage_chunk<kDipole, kCull>(S, ds, cam, vals, base + lane, rg.y, W, lane);
         int nrec = 0;
         while (m) {
             const int j = __ffs(m) - 1;
@@ -661,13 +785,26 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             bool hit = false;
             if (!done) hit = sphere_hit(P.R, S, j, g, ds, cam, PR);
             if (!__any_sync(0xffffffffu, hit)) continue;
+            if (kCount && hit) {
+                ++xh;
+                xp += S.deg[j];
+            }
+            int kept = 0;
+            const bool culled = kCull && cull_on && S.deg[j] <= 32u;
+            if (culled) {
+                kept = cull_planes(S, j, W, ds.edges, PB[warp], lane);
+                if (kept < 0) continue;   // the warp's beam misses cell i: every interval is empty
+            }
             float4 dpl = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             DetailGeo G;
             double dd[3], dc[3];
             if (kDetail) {
                 // neighbour planes first; the displaced face (its chart evaluation is
                 // the expensive part) only where the interval is still non-empty
-                clip_interval<kRecord, false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
+                if (culled)
+                    clip_interval_kept<kRecord, false>(P.R, PB[warp], kept, g, hit, dpl);
+                else
+                    clip_interval<kRecord, false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
                 const bool pre = g.dt > 0.0f;
                 if (__any_sync(0xffffffffu, pre)) {
                     if (pre) {
@@ -681,11 +818,10 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 }
             } else {
                 if (kDipole) dpl = S.nrm[j];
-                clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
-            }
-            if (kCount && hit) {
-                ++xh;
-                xp += S.deg[j];
+                if (culled)
+                    clip_interval_kept<kRecord, kDipole>(P.R, PB[warp], kept, g, hit, dpl);
+                else
+                    clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
             }
             const bool seg = g.dt > 0.0f;
             if (kRecord) {
@@ -695,7 +831,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                     reinterpret_cast<uint16_t *>(Rb.code[nrec])[lane] = (uint16_t)c;
                     if (lane == 0) {
                         Rb.mask[nrec] = sm;
-                        Rb.pos[nrec] = (uint32_t)j;
+                        Rb.pos[nrec] = (uint8_t)j;
                     }
                     ++nrec;
                 }
@@ -747,7 +883,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 if ((uint64_t)b0 + nrec <= rec_cap) {
                     for (int w = lane; w < nrec * kRecWords; w += 32) {
                         const int k = w / kRecWords, o = w - k * kRecWords;
-                        const uint32_t v = o == 0 ? Rb.mask[k] : (o == 1 ? Rb.pos[k] : Rb.code[k][o - 2]);
+                        const uint32_t v = o == 0 ? Rb.mask[k] : (o == 1 ? (uint32_t)Rb.pos[k] : Rb.code[k][o - 2]);
                         rec[(size_t)(b0 + k) * kRecWords + o] = v;
                     }
                     d = make_uint2(b0, (uint32_t)nrec);
@@ -782,22 +918,32 @@ static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *cou
                              uint32_t *rec_used, float *stc, float *stn, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
+    // the plane-cull buffers are dynamic shared memory (static + dynamic may pass 48 KB)
+    const size_t dyn = PF_K6_PCULL ? kWarps * sizeof(PlaneBuf) : 0;
+    const char *e = getenv("PF_PLANE_CULL");   // debug knob: 0 clips by every list plane
+    const int cull = (e && e[0] == '0') ? 0 : 1;
+    if (dyn) {   // per call: the attribute is per device
+        cudaFuncSetAttribute(k6_forward<false, true, kDipole, kDetail>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k6_forward<false, false, kDipole, kDetail>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    }
     if (counters)
         k6_forward<true, false, kDipole, kDetail><<<T, 256, 0, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
-            nullptr, 0u, nullptr, nullptr);
+            nullptr, 0u, nullptr, nullptr, 0);
     else if (rec_used)
-        k6_forward<false, true, kDipole, kDetail><<<T, 256, 0, st>>>(
+        k6_forward<false, true, kDipole, kDetail><<<T, 256, dyn, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
-            (uint32_t)v.rec_cap, stc, stn);
+            (uint32_t)v.rec_cap, stc, stn, cull);
     else
-        k6_forward<false, false, kDipole, kDetail><<<T, 256, 0, st>>>(
+        k6_forward<false, false, kDipole, kDetail><<<T, 256, dyn, st>>>(
             s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
             (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
-            stc, stn);
+            stc, stn, cull);
 }
 
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,

@@ -260,6 +260,35 @@ def test_inference_forward_equals_training_forward():
     ri.close()
 
 
+@pytest.mark.parametrize("name,variant,fish", [("tiny", "inside", False), ("small360", None, False),
+                                               ("small+dipoles", None, False),
+                                               ("small+detail", None, False),
+                                               ("small360", None, True),
+                                               ("nerfsynth200k", None, False)])
+def test_plane_cull_is_exact(monkeypatch, name, variant, fish):
+    """K6's warp-level plane cull drops only planes that cannot bind for
+    any pixel of the warp and skips only cells whose every interval is empty, so the
+    image is bit-identical to clipping by every list plane (PF_PLANE_CULL=0) and the
+    backward (driven by the same K6 records) agrees up to atomic summation order."""
+    sc, cams = _fisheye_case(name, variant) if fish else case(name, variant)
+    cams = cams[:2]
+    H, W = cams[0].height, cams[0].width
+    g = torch.from_numpy(pf_synth.make_grad_out(len(cams), H, W, seed=29)).cuda()
+    res = {}
+    for knob in ("1", "0"):
+        monkeypatch.setenv("PF_PLANE_CULL", knob)
+        r = renderer(sc)
+        out = r.forward(cams).cpu().numpy()
+        grads = {k: v.detach().cpu().numpy().astype(np.float64)
+                 for k, v in r.backward(cams, g).items()}
+        res[knob] = (out, grads)
+        r.close()
+    assert np.array_equal(res["1"][0], res["0"][0])
+    for k, a in res["1"][1].items():
+        b = res["0"][1][k]
+        assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
+
+
 def test_backward_record_overflow_fallback(monkeypatch):
     """K6->K7 record arena too small: overflowed chunks are recomputed in full by
     K7; gradients must be unchanged (parity with the oracle)."""
