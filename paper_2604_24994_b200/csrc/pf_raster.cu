@@ -254,9 +254,12 @@ __device__ __forceinline__ float sqrt_apx(float x)   // sqrt.approx (rel. error 
     return r;
 }
 
+#ifndef PF_KEPT_PAD   // kept planes padded to a multiple of this (1, 2, 4; 0: no unrolling)
+#define PF_KEPT_PAD 1
+#endif
 struct PlaneBuf {
-    float4 E[32];          // kept edge records (n, k) of the current cell
-    uint8_t q[32];         // their index in the cell's neighbour list
+    float4 E[32 + 3];      // kept edge records (n, k) of the current cell (+ padding)
+    uint8_t q[32 + 4];     // their index in the cell's neighbour list
 };
 
 // Per-slot constants of the plane cull, computed by the staging lane.
@@ -298,13 +301,21 @@ __device__ __forceinline__ int cull_planes(const WarpStage &S, int j, const Warp
         const int p = __popc(m & ((1u << lane) - 1u));
         B.E[p] = E;
         B.q[p] = (uint8_t)lane;
+#if PF_KEPT_PAD == 4
+        if (p == n - 1)
+            for (int k = n; k < ((n + 3) & ~3); ++k) {
+                B.E[k] = E;
+                B.q[k] = (uint8_t)lane;
+            }
+#elif PF_KEPT_PAD == 2
         if (p == n - 1 && (n & 1)) {
             B.E[n] = E;
             B.q[n] = (uint8_t)lane;
         }
+#endif
     }
     __syncwarp();
-    return (n + 1) & ~1;
+    return PF_KEPT_PAD > 1 ? (n + PF_KEPT_PAD - 1) & ~(PF_KEPT_PAD - 1) : n;
 }
 
 // a9 over the planes kept by cull_planes (same per-plane math and order as
@@ -322,12 +333,34 @@ __device__ __forceinline__ void clip_interval_kept(const Ray &R, const PlaneBuf 
     }
     g.hi = g.s;
     g.hi_q = kEndSphere;
+#if PF_KEPT_PAD == 4
+    for (int k = 0; k < n; k += 4) {   // n is a multiple of 4 (padded)
+        const float4 E0 = B.E[k], E1 = B.E[k + 1], E2 = B.E[k + 2], E3 = B.E[k + 3];
+        const uint32_t qq = kTrack ? *reinterpret_cast<const uint32_t *>(B.q + k) : 0u;
+        clip_plane<kTrack>(R, E0, (int)(qq & 0xffu) + 2, g);
+        clip_plane<kTrack>(R, E1, (int)((qq >> 8) & 0xffu) + 2, g);
+        clip_plane<kTrack>(R, E2, (int)((qq >> 16) & 0xffu) + 2, g);
+        clip_plane<kTrack>(R, E3, (int)(qq >> 24) + 2, g);
+    }
+#elif PF_KEPT_PAD == 2
     for (int k = 0; k < n; k += 2) {   // n is even (padded)
         const float4 E0 = B.E[k], E1 = B.E[k + 1];
         const uint32_t qq = kTrack ? *reinterpret_cast<const uint16_t *>(B.q + k) : 0u;
         clip_plane<kTrack>(R, E0, (int)(qq & 0xffu) + 2, g);
         clip_plane<kTrack>(R, E1, (int)(qq >> 8) + 2, g);
     }
+#elif PF_KEPT_PAD == 0
+    for (int k = 0; k < n; ++k) clip_plane<kTrack>(R, B.E[k], kTrack ? (int)B.q[k] + 2 : 0, g);
+#else
+    int k = 0;
+    for (; k + 2 <= n; k += 2) {
+        const float4 E0 = B.E[k], E1 = B.E[k + 1];
+        const uint32_t qq = kTrack ? *reinterpret_cast<const uint16_t *>(B.q + k) : 0u;
+        clip_plane<kTrack>(R, E0, (int)(qq & 0xffu) + 2, g);
+        clip_plane<kTrack>(R, E1, (int)(qq >> 8) + 2, g);
+    }
+    if (k < n) clip_plane<kTrack>(R, B.E[k], kTrack ? (int)B.q[k] + 2 : 0, g);
+#endif
     if (kDipole) clip_plane<kTrack>(R, dplane, kEndDipole, g);
     const float dt = __fsub_rn(g.hi, g.lo);
     g.dt = (active && dt > 0.0f) ? dt : 0.0f;
@@ -726,6 +759,9 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K6_MINB
 #define PF_K6_MINB 4
 #endif
+#ifndef PF_K6I_MINB   // K6 without records (inference, counting): 5 CTAs/SM measured faster
+#define PF_K6I_MINB 5
+#endif
 #ifndef PF_K6_PCULL   // warp-level plane cull in K6 (cull_planes)
 #define PF_K6_PCULL 1
 #endif
@@ -742,7 +778,7 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #define PF_K6D_MINB 3
 #endif
 template <bool kCount, bool kRecord, bool kDipole, int kDetail>
-__global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB : PF_K6_MINB)
+__global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB : (kRecord ? PF_K6_MINB : PF_K6I_MINB))
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
            float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
