@@ -53,6 +53,9 @@ def parse():
                     help="K detail sites per dipole face (NEXT-2; implies --dipoles)")
     ap.add_argument("--fisheye", action="store_true",
                     help="equidistant fisheye cameras (NEXT-4), 200 deg image circle")
+    ap.add_argument("--lists", default="cech", choices=["cech", "knn"],
+                    help="neighbour lists: Čech-filtered (default) or unfiltered sym-16NN "
+                         "(the paper's extraneous-edge comparison, P:236)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -172,7 +175,7 @@ def run_reference(args):
     import oracle
     import pf_synth
     wl = args.workload
-    sc = pf_synth.make_scene(wl, dipoles=args.dipoles, detail=args.detail)
+    sc = pf_synth.make_scene(wl, variant=args.lists, dipoles=args.dipoles, detail=args.detail)
     nv = args.views or default_views(wl)
     cams = workload_cameras(wl, nv, 1, 0)
     train = wl not in ("mip360_1m", "sweep64_3m")
@@ -271,7 +274,7 @@ def main():
     wl = args.workload
     nv = args.views or default_views(wl)
     t_gen = time.perf_counter()
-    sc = pf_synth.make_scene(wl, dipoles=args.dipoles, detail=args.detail)
+    sc = pf_synth.make_scene(wl, variant=args.lists, dipoles=args.dipoles, detail=args.detail)
     cams = workload_cameras(wl, nv, ws, rank)
     if args.fisheye:
         cams = [pf_synth.fisheye(c, 200.0) for c in cams]
@@ -526,7 +529,8 @@ def main():
             "data": "synthetic (pf_synth seeded generator, random-init foam)",
             "config": {"workload": wl + ("+dipoles" if args.dipoles and not args.detail else "") +
                                    (f"+detail{args.detail}" if args.detail else "") +
-                                   ("+fisheye" if args.fisheye else ""), "cells": N,
+                                   ("+fisheye" if args.fisheye else "") +
+                                   ("+knn_lists" if args.lists == "knn" else ""), "cells": N,
                        "edges": sc.num_edges, "views_per_gpu": nv,
                        "global_batch_views": nv * ws, "width": W, "height": H,
                        "pass": "fwd+bwd" if train else "fwd",

@@ -236,8 +236,8 @@ __device__ __forceinline__ void clip_interval(const Ray &R, const float4 *__rest
 //   rho = (t0 + r) tan(th),  s_max = sqrt(r^2 - max(0, |e0| - rho)^2)
 // (axial coordinate of a ball point <= t0 + r; radial <= axial tan(th)).  On it
 // the plane function f = a t' - b of neighbour j (a = d.n, b = k + n.e; the
-// cell keeps f <= 0) ranges within  -b +- (|d_w.n| s_max + rho |n|)  with
-// b_w = k + n.e0.  Lane k tests plane k at once:
+// cell keeps f <= 0) ranges within  -b_w +- (|d_w.n| s_max + rho |n|)  with
+// b_w = k + n.e0.  After a hit, lane k tests plane k of the cell at once:
 //   sup f < -M  : plane k cannot bind for any pixel of the warp -> dropped
 //                 (fminf/fmaxf with a strictly non-binding value is the identity,
 //                 so the interval is bit-identical to clipping by every plane);
@@ -777,8 +777,11 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K6D_MINB
 #define PF_K6D_MINB 3
 #endif
-template <bool kCount, bool kRecord, bool kDipole, int kDetail>
-__global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB : (kRecord ? PF_K6_MINB : PF_K6I_MINB))
+// kWide: the non-recording launch for wide-cone (fisheye) views, at 4 CTAs/SM
+// (measured: 5 CTAs/SM is faster for pinhole views, slower for fisheye ones)
+template <bool kCount, bool kRecord, bool kDipole, int kDetail, bool kWide = false>
+__global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB
+                                               : (kRecord || kWide ? PF_K6_MINB : PF_K6I_MINB))
 k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
            float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
@@ -957,6 +960,7 @@ static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *cou
     // the plane-cull buffers are dynamic shared memory (static + dynamic may pass 48 KB)
     const size_t dyn = PF_K6_PCULL ? kWarps * sizeof(PlaneBuf) : 0;
     const char *e = getenv("PF_PLANE_CULL");   // debug knob: 0 clips by every list plane
+    const bool wide = v.cam.model == PF_FISHEYE;
     const int cull = (e && e[0] == '0') ? 0 : 1;
     if (dyn) {   // per call: the attribute is per device
         cudaFuncSetAttribute(k6_forward<false, true, kDipole, kDetail>,
@@ -975,11 +979,14 @@ static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *cou
             (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
             v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
             (uint32_t)v.rec_cap, stc, stn, cull);
-    else
-        k6_forward<false, false, kDipole, kDetail><<<T, 256, dyn, st>>>(
-            s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
-            (float4 *)out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
-            stc, stn, cull);
+    else {
+        auto kern = k6_forward<false, false, kDipole, kDetail>;
+        if constexpr (!kDetail)
+            if (wide) kern = k6_forward<false, false, kDipole, kDetail, true>;
+        kern<<<T, 256, dyn, st>>>(s->ds, v.cam, v.ranges_p, v.order, v.vals_p, (float4 *)out,
+                                  nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                  0u, stc, stn, cull);
+    }
 }
 
 cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,

@@ -263,18 +263,18 @@ def _scene_tiny(seed, variant="sym8"):
     return sc
 
 
-def _scene_object(N, seed, bg, K=16, frac_obj=0.85, name="nerfsynth"):
+def _scene_object(N, seed, bg, K=16, frac_obj=0.85, name="nerfsynth", cech_filter=True):
     rng = np.random.default_rng(seed)
     n_obj = int(round(frac_obj * N))
     pts = _object_surface(n_obj, rng) + rng.normal(0.0, 0.004, size=(n_obj, 3))
     box = rng.uniform(-1.5, 1.5, size=(N - n_obj, 3))
     sites = np.concatenate([pts, box]).astype(np.float32)
     sites = sites[rng.permutation(N)]
-    radii, offs, nbrs = knn_cech_lists(sites, K, rng, cech_filter=True)
+    radii, offs, nbrs = knn_cech_lists(sites, K, rng, cech_filter=cech_filter)
     return _finish(sites, radii, offs, nbrs, rng, bg, name)
 
 
-def _scene_mip360(N, seed, K=16, name="mip360"):
+def _scene_mip360(N, seed, K=16, name="mip360", cech_filter=True):
     rng = np.random.default_rng(seed)
     n_obj = int(round(0.45 * N))
     n_gnd = int(round(0.20 * N))
@@ -294,7 +294,7 @@ def _scene_mip360(N, seed, K=16, name="mip360"):
                           np.full(n_bg, 2, np.int8)])
     perm = rng.permutation(N)
     sites, cls = sites[perm], cls[perm]
-    radii, offs, nbrs = knn_cech_lists(sites, K, rng, cech_filter=True)
+    radii, offs, nbrs = knn_cech_lists(sites, K, rng, cech_filter=cech_filter)
     dens = _densities(radii, rng)
     m = cls == 2
     sr_bg = rng.uniform(0.01, 0.5, m.sum())
@@ -412,18 +412,34 @@ def make_scene(preset: str, seed: int | None = None, variant: str | None = None,
 def _make_scene(preset, seed, variant, num_cells):
     if preset == "tiny":
         return _scene_tiny(0 if seed is None else seed, variant or "sym8")
+    # variant "knn": the unfiltered sym-16NN lists (a superset of the Čech lists by
+    # Lemma L3; same sites, radii and appearance) -- the paper's extraneous-edge
+    # comparison
+    if variant not in (None, "cech", "knn"):
+        raise ValueError(variant)
+    cf = variant != "knn"
+    sc = _make_scene_lists(preset, seed, num_cells, cf)
+    if not cf:
+        sc.meta["variant"] = "knn"
+    return sc
+
+
+def _make_scene_lists(preset, seed, num_cells, cf):
     if preset == "small":   # test-size nerfsynth-shaped foam
         return _scene_object(num_cells or 3000, 5 if seed is None else seed, (1.0, 1.0, 1.0),
-                             name="small")
+                             name="small", cech_filter=cf)
     if preset == "small360":  # test-size mip360-shaped foam
-        return _scene_mip360(num_cells or 20000, 6 if seed is None else seed, name="small360")
+        return _scene_mip360(num_cells or 20000, 6 if seed is None else seed, name="small360",
+                             cech_filter=cf)
     if preset == "nerfsynth200k":
         return _scene_object(num_cells or 200_000, 1 if seed is None else seed, (1.0, 1.0, 1.0),
-                             name=preset)
+                             name=preset, cech_filter=cf)
     if preset in ("mip360_1m", "train8_1m"):
-        return _scene_mip360(num_cells or 1_000_000, 2 if seed is None else seed, name=preset)
+        return _scene_mip360(num_cells or 1_000_000, 2 if seed is None else seed, name=preset,
+                             cech_filter=cf)
     if preset == "sweep64_3m":
-        return _scene_mip360(num_cells or 3_000_000, 3 if seed is None else seed, name=preset)
+        return _scene_mip360(num_cells or 3_000_000, 3 if seed is None else seed, name=preset,
+                             cech_filter=cf)
     raise ValueError(f"unknown preset {preset}")
 
 

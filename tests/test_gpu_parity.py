@@ -289,6 +289,26 @@ def test_plane_cull_is_exact(monkeypatch, name, variant, fish):
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
 
 
+def test_unfiltered_knn_lists_render_the_same():
+    """Extra (non-Čech) neighbours never bind inside B_i (Lemma L1): the
+    image with unfiltered sym-16NN lists equals the Čech-list image up to rounding and
+    the oracle within the image bar; gradients within the gradient bar."""
+    sc, cams = case("small360")
+    sk = pf_synth.make_scene("small360", variant="knn")
+    cams = cams[:2]
+    H, W = cams[0].height, cams[0].width
+    g = torch.from_numpy(pf_synth.make_grad_out(len(cams), H, W, seed=31)).cuda()
+    r, rk = renderer(sc), renderer(sk)
+    a, b = r.forward(cams).cpu().numpy(), rk.forward(cams).cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-5
+    ref = oracle.render(sk, cams[0], mode=oracle.O3)["out"]
+    assert np.abs(b[0] - ref).max() <= IMG_TOL
+    ga = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in r.backward(cams, g).items()}
+    grad_check(rk.backward(cams, g), ga)
+    r.close()
+    rk.close()
+
+
 def test_backward_record_overflow_fallback(monkeypatch):
     """K6->K7 record arena too small: overflowed chunks are recomputed in full by
     K7; gradients must be unchanged (parity with the oracle)."""

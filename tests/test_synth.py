@@ -34,3 +34,17 @@ def test_tiny_sym8_contains_cech():
         for j in range(sc.num_cells):
             if j != i and np.linalg.norm(P[i] - P[j]) < r[i] + r[j]:
                 assert j in nb
+
+
+def test_unfiltered_knn_variant_contains_cech_lists():
+    """variant="knn" (bench --lists knn, the P:236 extraneous-edge comparison): same
+    scene, lists = unfiltered sym-16NN, a strict superset of the Čech lists (Lemma L3)."""
+    a = pf_synth.make_scene("small", num_cells=1500)
+    b = pf_synth.make_scene("small", num_cells=1500, variant="knn")
+    for f in ("sites", "weights", "radii", "density", "rgb"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
+    assert b.num_edges > 1.3 * a.num_edges
+    for i in range(a.num_cells):
+        ca = set(a.nbr_indices[a.nbr_offsets[i]:a.nbr_offsets[i + 1]].tolist())
+        cb = b.nbr_indices[b.nbr_offsets[i]:b.nbr_offsets[i + 1]].tolist()
+        assert ca <= set(cb) and i not in cb and len(cb) == len(set(cb))
