@@ -456,8 +456,10 @@ def main():
             "ncu_issue_pct": prof.get("issue_pct_of_peak"),
             "note": "instruction count of one launch from the committed ncu capture "
                     "(same kernel, same workload); the FP32 fraction is below this because "
-                    "the plane test is ~17 instructions for 16 algorithmic flops "
-                    "(selects, min/max, MUFU rcp)"}
+                    "the path is not FMA-shaped (a plane test is ~17 instructions for 16 "
+                    "flops) and the per-(warp, cell) lockstep work serves ~3.4 hit pixels "
+                    "of 32 on average (DESIGN 9); the algorithmic flops count every list "
+                    "plane, the warp plane cull executes ~1 per hit cell"}
     sort_ms, sort_n = stages["K4_sort"]
     pairs = r.pair_counts(nv)
     P = float(np.mean(pairs))

@@ -745,10 +745,14 @@ struct WarpRec {
     uint8_t pos[32];            // slot (list position within the chunk)
 };
 
+template <bool kDipole>
 __device__ __forceinline__ uint32_t end_code(int q)
 {
-    // tracked codes are already record codes; only the dipole and planes >= 252 remap
-    return q == kEndDipole ? 254u : min((uint32_t)q, 255u);
+    // tracked codes are already record codes (0 sphere, 1 near, 2 + plane index);
+    // 255 = not representable (K7 replays the entry in full).  With dipoles 254 is
+    // the dipole face, so plane 252 must not produce it.
+    if (!kDipole) return min((uint32_t)q, 255u);
+    return q == kEndDipole ? 254u : ((uint32_t)q >= 254u ? 255u : (uint32_t)q);
 }
 
 }  // namespace
@@ -866,7 +870,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             if (kRecord) {
                 const unsigned sm = __ballot_sync(0xffffffffu, seg);
                 if (sm) {
-                    const uint32_t c = seg ? (end_code(g.lo_q) | (end_code(g.hi_q) << 8)) : 0u;
+                    const uint32_t c = seg ? (end_code<kDipole>(g.lo_q) | (end_code<kDipole>(g.hi_q) << 8)) : 0u;
                     reinterpret_cast<uint16_t *>(Rb.code[nrec])[lane] = (uint16_t)c;
                     if (lane == 0) {
                         Rb.mask[nrec] = sm;
