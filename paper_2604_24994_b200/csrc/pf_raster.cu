@@ -775,6 +775,9 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #ifndef PF_K7_DIRECT_MAX   // up to this many segment lanes: per-lane atomics, no warp reduction
 #define PF_K7_DIRECT_MAX 10
 #endif
+#ifndef PF_K7_GROUP   // K7: up to this many consecutive disjoint-mask records per pass
+#define PF_K7_GROUP 4
+#endif
 #ifndef PF_K7D_MINB
 #define PF_K7D_MINB 2
 #endif
@@ -1469,7 +1472,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
                                                  const DeviceScene &ds, float *acc, int lane,
                                                  float cr, float cg, float cb, const float4 &dnrm,
                                                  const DetailCtx *X, const float *om,
-                                                 float (*buf)[33])
+                                                 float (*buf)[33], bool grouped = false)
 {
     if (kDetail) {
         // (an fp32 instantiation for non-grazing warps measured slower on B200: the
@@ -1511,7 +1514,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
     // reduction then one 9-lane atomic instruction
     float *accc = acc + 12 * (size_t)S.cell[j];
     const unsigned sm = __ballot_sync(0xffffffffu, seg);
-    if (__popc(sm) <= PF_K7_DIRECT_MAX) {
+    if (grouped || __popc(sm) <= PF_K7_DIRECT_MAX) {   // (a group spans several cells)
         if (seg) {
             atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
             if (dipole)
@@ -1589,6 +1592,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             dpl = S.nrm[j];
         }
     };
+    constexpr bool kGroup = !kDetail && PF_K7_GROUP > 1;   // detail: warp-level per-cell reductions
     const uint32_t nchunks = wdone[(size_t)tile * kWarps + warp];
     const uint32_t c0 = chunk_off[tile];
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -1644,11 +1648,30 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             stage_slot<kDipole>(S, lane, ds, cell, A, x0, x1, x2, t, W);
         }
         __syncwarp();
-        for (uint32_t k = 0; k < nrec; ++k) {
-            const uint32_t mask = __shfl_sync(0xffffffffu, my_mask, (int)k);
-            const uint32_t code = __ldg(reinterpret_cast<const uint16_t *>(R0 + (size_t)k * kRecWords + 2) + lane);
-            const bool seg = (mask >> lane) & 1u;
-            const int j = (int)k;
+        for (uint32_t k = 0; k < nrec;) {
+            // one pass over a group of consecutive records whose lane masks are
+            // pairwise disjoint: each lane takes the record holding it (at most one),
+            // so every pixel still replays its own segments in list order
+            uint32_t uni = __shfl_sync(0xffffffffu, my_mask, (int)k);
+            int jl = ((uni >> lane) & 1u) ? (int)k : -1;
+            uint32_t k1 = k + 1;
+            if (kGroup) {
+                while (k1 < nrec && k1 - k < (uint32_t)PF_K7_GROUP) {
+                    const uint32_t m2 = __shfl_sync(0xffffffffu, my_mask, (int)k1);
+                    if (m2 & uni) break;
+                    uni |= m2;
+                    if ((m2 >> lane) & 1u) jl = (int)k1;
+                    ++k1;
+                }
+            }
+            const bool grouped = k1 - k > 1u;
+            const bool seg = jl >= 0;
+            // lanes without a segment take the group's first record (a single-record
+            // group's warp reduction reads S.cell[j] on any lane)
+            const int j = seg ? jl : (int)k;
+            k = k1;
+            const uint32_t code =
+                seg ? __ldg(reinterpret_cast<const uint16_t *>(R0 + (size_t)j * kRecWords + 2) + lane) : 0u;
             Seg g;
             g.dt = 0.0f;
             float4 dpl;
@@ -1672,7 +1695,7 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
             segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb, dpl,
-                                               &X, om, buf);
+                                               &X, om, buf, grouped);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();
