@@ -739,10 +739,8 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
 constexpr uint32_t kOverflow = 0xffffffffu;
 constexpr int kRecWords = 18;   // mask, pos, 32 x u16 codes
 
-struct WarpRec {
-    uint32_t mask[32];
-    uint32_t code[32][16];      // 32 lanes x u16, as 16 words
-    uint8_t pos[32];            // slot (list position within the chunk)
+struct WarpRec {                 // a chunk's records in their global layout (flushed as is)
+    uint32_t w[32 * kRecWords];  // per record: mask, pos (slot), 32 lanes x u16 codes
 };
 
 template <bool kDipole>
@@ -874,10 +872,10 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 const unsigned sm = __ballot_sync(0xffffffffu, seg);
                 if (sm) {
                     const uint32_t c = seg ? (end_code<kDipole>(g.lo_q) | (end_code<kDipole>(g.hi_q) << 8)) : 0u;
-                    reinterpret_cast<uint16_t *>(Rb.code[nrec])[lane] = (uint16_t)c;
+                    reinterpret_cast<uint16_t *>(Rb.w + nrec * kRecWords + 2)[lane] = (uint16_t)c;
                     if (lane == 0) {
-                        Rb.mask[nrec] = sm;
-                        Rb.pos[nrec] = (uint8_t)j;
+                        Rb.w[nrec * kRecWords] = sm;
+                        Rb.w[nrec * kRecWords + 1] = (uint32_t)j;
                     }
                     ++nrec;
                 }
@@ -927,11 +925,8 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 if (lane == 0) b0 = atomicAdd(rec_used, (uint32_t)nrec);
                 b0 = __shfl_sync(0xffffffffu, b0, 0);
                 if ((uint64_t)b0 + nrec <= rec_cap) {
-                    for (int w = lane; w < nrec * kRecWords; w += 32) {
-                        const int k = w / kRecWords, o = w - k * kRecWords;
-                        const uint32_t v = o == 0 ? Rb.mask[k] : (o == 1 ? (uint32_t)Rb.pos[k] : Rb.code[k][o - 2]);
-                        rec[(size_t)(b0 + k) * kRecWords + o] = v;
-                    }
+                    uint32_t *dst = rec + (size_t)b0 * kRecWords;
+                    for (int w = lane; w < nrec * kRecWords; w += 32) dst[w] = Rb.w[w];
                     d = make_uint2(b0, (uint32_t)nrec);
                 } else {
                     d = make_uint2(0u, kOverflow);
