@@ -777,7 +777,7 @@ __device__ __forceinline__ uint32_t end_code(int q)
 #define PF_K7_GROUP 4
 #endif
 #ifndef PF_K7D_MINB
-#define PF_K7D_MINB 2
+#define PF_K7D_MINB 1
 #endif
 #ifndef PF_K6D_MINB
 #define PF_K6D_MINB 3
