@@ -264,13 +264,19 @@ def test_inference_forward_equals_training_forward():
                                                ("small+dipoles", None, False),
                                                ("small+detail", None, False),
                                                ("small360", None, True),
-                                               ("nerfsynth200k", None, False)])
+                                               ("small360", "knn", False),
+                                               ("tiny_w0", None, False),
+                                               ("nerfsynth200k", None, False),
+                                               ("train8_1m", None, False)])
 def test_plane_cull_is_exact(monkeypatch, name, variant, fish):
     """K6's warp-level plane cull drops only planes that cannot bind for
     any pixel of the warp and skips only cells whose every interval is empty, so the
     image is bit-identical to clipping by every list plane (PF_PLANE_CULL=0) and the
     backward (driven by the same K6 records) agrees up to atomic summation order."""
-    sc, cams = _fisheye_case(name, variant) if fish else case(name, variant)
+    if variant == "knn":   # unfiltered lists: many extra, never-binding planes
+        sc, cams = pf_synth.make_scene(name, variant="knn"), case(name)[1]
+    else:
+        sc, cams = _fisheye_case(name, variant) if fish else case(name, variant)
     cams = cams[:2]
     H, W = cams[0].height, cams[0].width
     g = torch.from_numpy(pf_synth.make_grad_out(len(cams), H, W, seed=29)).cuda()
