@@ -254,12 +254,9 @@ __device__ __forceinline__ float sqrt_apx(float x)   // sqrt.approx (rel. error 
     return r;
 }
 
-#ifndef PF_KEPT_PAD   // kept planes padded to a multiple of this (1, 2, 4; 0: no unrolling)
-#define PF_KEPT_PAD 1
-#endif
 struct PlaneBuf {
-    float4 E[32 + 3];      // kept edge records (n, k) of the current cell (+ padding)
-    uint8_t q[32 + 4];     // their index in the cell's neighbour list
+    float4 E[32];          // kept edge records (n, k) of the current cell
+    uint8_t q[32];         // their index in the cell's neighbour list
 };
 
 // Per-slot constants of the plane cull, computed by the staging lane.
@@ -275,9 +272,8 @@ __device__ __forceinline__ void cull_consts(WarpStage &S, int slot, const WarpCt
 }
 
 // Lane k tests plane k of slot j (deg <= 32) and the kept planes are compacted
-// into B in list order (an odd count is padded with a copy of the last plane:
-// min/max are idempotent and the tracking is strict, so the copy changes
-// nothing).  Returns -1 if every pixel's interval is empty, else the padded count.
+// into B in list order.  Returns -1 if every pixel's interval is empty, else the
+// number of kept planes.
 __device__ __forceinline__ int cull_planes(const WarpStage &S, int j, const WarpCtx &W,
                                            const float4 *__restrict__ edges, PlaneBuf &B, int lane)
 {
@@ -301,21 +297,9 @@ __device__ __forceinline__ int cull_planes(const WarpStage &S, int j, const Warp
         const int p = __popc(m & ((1u << lane) - 1u));
         B.E[p] = E;
         B.q[p] = (uint8_t)lane;
-#if PF_KEPT_PAD == 4
-        if (p == n - 1)
-            for (int k = n; k < ((n + 3) & ~3); ++k) {
-                B.E[k] = E;
-                B.q[k] = (uint8_t)lane;
-            }
-#elif PF_KEPT_PAD == 2
-        if (p == n - 1 && (n & 1)) {
-            B.E[n] = E;
-            B.q[n] = (uint8_t)lane;
-        }
-#endif
     }
     __syncwarp();
-    return PF_KEPT_PAD > 1 ? (n + PF_KEPT_PAD - 1) & ~(PF_KEPT_PAD - 1) : n;
+    return n;
 }
 
 // a9 over the planes kept by cull_planes (same per-plane math and order as
@@ -333,25 +317,6 @@ __device__ __forceinline__ void clip_interval_kept(const Ray &R, const PlaneBuf 
     }
     g.hi = g.s;
     g.hi_q = kEndSphere;
-#if PF_KEPT_PAD == 4
-    for (int k = 0; k < n; k += 4) {   // n is a multiple of 4 (padded)
-        const float4 E0 = B.E[k], E1 = B.E[k + 1], E2 = B.E[k + 2], E3 = B.E[k + 3];
-        const uint32_t qq = kTrack ? *reinterpret_cast<const uint32_t *>(B.q + k) : 0u;
-        clip_plane<kTrack>(R, E0, (int)(qq & 0xffu) + 2, g);
-        clip_plane<kTrack>(R, E1, (int)((qq >> 8) & 0xffu) + 2, g);
-        clip_plane<kTrack>(R, E2, (int)((qq >> 16) & 0xffu) + 2, g);
-        clip_plane<kTrack>(R, E3, (int)(qq >> 24) + 2, g);
-    }
-#elif PF_KEPT_PAD == 2
-    for (int k = 0; k < n; k += 2) {   // n is even (padded)
-        const float4 E0 = B.E[k], E1 = B.E[k + 1];
-        const uint32_t qq = kTrack ? *reinterpret_cast<const uint16_t *>(B.q + k) : 0u;
-        clip_plane<kTrack>(R, E0, (int)(qq & 0xffu) + 2, g);
-        clip_plane<kTrack>(R, E1, (int)(qq >> 8) + 2, g);
-    }
-#elif PF_KEPT_PAD == 0
-    for (int k = 0; k < n; ++k) clip_plane<kTrack>(R, B.E[k], kTrack ? (int)B.q[k] + 2 : 0, g);
-#else
     int k = 0;
     for (; k + 2 <= n; k += 2) {
         const float4 E0 = B.E[k], E1 = B.E[k + 1];
@@ -360,7 +325,6 @@ __device__ __forceinline__ void clip_interval_kept(const Ray &R, const PlaneBuf 
         clip_plane<kTrack>(R, E1, (int)(qq >> 8) + 2, g);
     }
     if (k < n) clip_plane<kTrack>(R, B.E[k], kTrack ? (int)B.q[k] + 2 : 0, g);
-#endif
     if (kDipole) clip_plane<kTrack>(R, dplane, kEndDipole, g);
     const float dt = __fsub_rn(g.hi, g.lo);
     g.dt = (active && dt > 0.0f) ? dt : 0.0f;
