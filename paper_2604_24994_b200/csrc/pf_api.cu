@@ -442,6 +442,9 @@ int pf_destroy(pf_scene *s)
         cudaEventDestroy(e.b);
     }
     for (auto e : s->event_pool) cudaEventDestroy(e);
+    if (s->side) cudaStreamDestroy(s->side);
+    if (s->side_fork) cudaEventDestroy(s->side_fork);
+    if (s->side_join) cudaEventDestroy(s->side_join);
     delete s;
     return PF_OK;
 }
@@ -467,8 +470,28 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     s->fwd_views = 0;
+    bool k0_side = false;
     if (!(s->flags & PF_STATIC_SCENE) || !s->edges_built) {
-        PF_CUDA(pf::launch_edge_records(s, st));
+        // K0 (edge records, read only by K6/K7) on a side stream, concurrent with the
+        // binning and sort of K1-K5; joined before the first K6
+        if (!s->side) {
+            if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&s->side_fork, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&s->side_join, cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                if (s->side) cudaStreamDestroy(s->side);
+                s->side = nullptr;
+            }
+        }
+        if (s->side) {
+            PF_CUDA(cudaEventRecord(s->side_fork, st));
+            PF_CUDA(cudaStreamWaitEvent(s->side, s->side_fork, 0));
+            PF_CUDA(pf::launch_edge_records(s, s->side));
+            PF_CUDA(cudaEventRecord(s->side_join, s->side));
+            k0_side = true;
+        } else {
+            PF_CUDA(pf::launch_edge_records(s, st));
+        }
         s->edges_built = true;
     }
     if ((int)s->views.size() < V) s->views.resize(V);
@@ -493,6 +516,7 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
     uint64_t *ks_all = nullptr;
     rc = emit_sort_ranges(s, s->views.data(), V, st, &ks_all);
     if (rc) return rc;
+    if (k0_side) PF_CUDA(cudaStreamWaitEvent(st, s->side_join, 0));
     for (int v = 0; v < V; ++v) {
         pf::ViewState &vs = s->views[v];
         uint32_t *used = nullptr;

@@ -111,6 +111,8 @@ struct pf_scene {
     int pinned_n = 0;
     int64_t launches = 0;
     bool profiling = false;
+    cudaStream_t side = nullptr;    // K0 of a training forward runs here, beside K1-K5
+    cudaEvent_t side_fork = nullptr, side_join = nullptr;
     std::vector<pf::StageEvent> events;
     std::vector<cudaEvent_t> event_pool;
 };
