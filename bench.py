@@ -186,11 +186,17 @@ def run_reference(args):
                          calib=res["calib"])
         steps.append(r["value"])
     val = float(np.median(steps)) if steps else res["value"]
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * nv / val,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl, "cells": sc.num_cells, "views": nv,
-                       "width": cams[0].width, "height": cams[0].height},
+            "config": {"workload": wl + ("+dipoles" if args.dipoles and not args.detail else "") +
+                                   (f"+detail{args.detail}" if args.detail else "") +
+                                   ("+knn_lists" if args.lists == "knn" else ""),
+                       "cells": sc.num_cells, "edges": sc.num_edges, "views_per_gpu": nv,
+                       "global_batch_views": nv * ws, "width": cams[0].width,
+                       "height": cams[0].height, "pass": "fwd+bwd" if train else "fwd",
+                       "parallelism": "oracle on the host cores of rank 0 (CPU, double)"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": res["cores"],
                              "kind": "oracle", "sample": res["sample"]},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
