@@ -80,6 +80,8 @@ pf::CamParams cam_params(const pf_camera &c)
     for (int k = 0; k < 12; ++k) p.M[k] = c.c2w[k];
     p.near_plane = c.near_plane;
     p.model = c.model;
+    p.ifx = 1.0 / (double)c.fx;
+    p.ify = 1.0 / (double)c.fy;
     return p;
 }
 

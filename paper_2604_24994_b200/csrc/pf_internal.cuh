@@ -23,6 +23,7 @@ struct CamParams {
     float M[12];     // c2w row-major
     float near_plane;
     int model;       // PF_PINHOLE / PF_FISHEYE
+    double ifx, ify; // 1 / fx, 1 / fy (fp64, host-computed; K6/K7 pixel rays)
 };
 
 // Device-side records built by K0 from the caller's arrays.

@@ -19,6 +19,10 @@
 
 #include "pf_internal.cuh"
 
+#ifndef PF_RAY_FAST   // pixel rays without fp64 divides (ray_dir)
+#define PF_RAY_FAST 1
+#endif
+
 namespace pf {
 
 namespace {
@@ -42,8 +46,15 @@ __device__ __forceinline__ void ray_dir(const CamParams &cam, double u, double v
                                         double *tnear, bool *valid = nullptr)
 {
     // explicit IEEE double intrinsics: K6 and K7 must produce bit-identical rays
+    // (multiplications by the host's 1/f and one rsqrt instead of fp64 divides:
+    // the ray differs from the exact one by a few fp64 ulps, far below fp32)
+#if PF_RAY_FAST
+    double a = __dmul_rn(__dsub_rn(u, (double)cam.cx), cam.ifx);
+    double b = __dmul_rn(__dsub_rn(v, (double)cam.cy), cam.ify);
+#else
     double a = __ddiv_rn(__dsub_rn(u, (double)cam.cx), (double)cam.fx);
     double b = __ddiv_rn(__dsub_rn(v, (double)cam.cy), (double)cam.fy);
+#endif
     double c = 1.0;
     if (cam.model == PF_FISHEYE) {
         const double th = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
@@ -64,10 +75,17 @@ __device__ __forceinline__ void ray_dir(const CamParams &cam, double u, double v
     double w0 = __fma_rn((double)cam.M[2], c, __fma_rn((double)cam.M[0], a, __dmul_rn((double)cam.M[1], b)));
     double w1 = __fma_rn((double)cam.M[6], c, __fma_rn((double)cam.M[4], a, __dmul_rn((double)cam.M[5], b)));
     double w2 = __fma_rn((double)cam.M[10], c, __fma_rn((double)cam.M[8], a, __dmul_rn((double)cam.M[9], b)));
+#if PF_RAY_FAST
+    const double inrm = rsqrt(__fma_rn(w0, w0, __fma_rn(w1, w1, __dmul_rn(w2, w2))));
+    d[0] = __dmul_rn(w0, inrm);
+    d[1] = __dmul_rn(w1, inrm);
+    d[2] = __dmul_rn(w2, inrm);
+#else
     double nrm = __dsqrt_rn(__fma_rn(w0, w0, __fma_rn(w1, w1, __dmul_rn(w2, w2))));
     d[0] = __ddiv_rn(w0, nrm);
     d[1] = __ddiv_rn(w1, nrm);
     d[2] = __ddiv_rn(w2, nrm);
+#endif
     if (tnear)
         *tnear = cam.model == PF_FISHEYE
                      ? (double)cam.near_plane
