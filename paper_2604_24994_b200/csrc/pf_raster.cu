@@ -498,8 +498,14 @@ __device__ __forceinline__ unsigned stage_chunk(WarpStage &S, const DeviceScene 
         if (cc <= r2) {
             pass = true;
         } else {
+#if PF_RAY_FAST   // x rsqrt(x): a few fp64 ulps, far inside the 1e-7 |c| margin
+            const double q = cc - r2;
+            const double lim = W.cos_t * (q * rsqrt(q)) - W.sin_t * rr;
+            pass = t >= lim - 1e-7 * (cc * rsqrt(cc));
+#else
             const double lim = W.cos_t * sqrt(cc - r2) - W.sin_t * rr;
             pass = t >= lim - 1e-7 * sqrt(cc);
+#endif
         }
     }
     const unsigned m = __ballot_sync(0xffffffffu, pass);
