@@ -788,7 +788,7 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     __shared__ WarpCtx WC[kWarps];
     __shared__ WarpRec WR[kRecord ? kWarps : 1];
     __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
-    // warp plane cull (plane_mask); the counting build evaluates every list plane
+    // warp plane cull (cull_planes); the counting build evaluates every list plane
     // so its X_p stays the SURVEY 8(d) work count
     constexpr bool kCull = PF_K6_PCULL && !kCount;
     extern __shared__ PlaneBuf PB[];   // kWarps entries when kCull (dynamic: static smem is full)
