@@ -315,6 +315,29 @@ def test_unfiltered_knn_lists_render_the_same():
     rk.close()
 
 
+def test_in_place_parameter_update_between_forwards():
+    """Without PF_STATIC_SCENE the edge records (K0) are rebuilt every forward, on a
+    side stream forked from the caller's stream: an in-place update of the sites and
+    weights enqueued on the caller's stream right before the forward must be seen
+    (the image equals a fresh renderer's on the moved scene, bit for bit)."""
+    import copy
+    sc, cams = case("small360")
+    cams = cams[:2]
+    r = renderer(sc, flags=0)
+    r.forward(cams)
+    moved = copy.deepcopy(sc)
+    rng = np.random.default_rng(3)
+    moved.sites = (sc.sites + rng.normal(0, 2e-3, sc.sites.shape)).astype(np.float32)
+    moved.weights = (sc.weights * np.float32(1.01)).astype(np.float32)
+    s_t, w_t = r.params()[0], r.params()[1]
+    s_t.copy_(torch.from_numpy(moved.sites).to(s_t.device), non_blocking=True)
+    w_t.copy_(torch.from_numpy(moved.weights).to(w_t.device), non_blocking=True)
+    got = r.forward(cams).cpu().numpy()
+    ref = renderer(moved, flags=0).forward(cams).cpu().numpy()
+    assert np.array_equal(got, ref)
+    r.close()
+
+
 def test_backward_record_overflow_fallback(monkeypatch):
     """K6->K7 record arena too small: overflowed chunks are recomputed in full by
     K7; gradients must be unchanged (parity with the oracle)."""
