@@ -646,7 +646,8 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
     G.dr = 0.0f;
     G.ts = 0.0;
     if (!G.parallel) {
-        const double tb = __ddiv_rn(B, G.A);
+        const double iA = __drcp_rn(G.A);   // one reciprocal for both face hits
+        const double tb = __dmul_rn(B, iA);
         const double y0 = __fma_rn(tb, d[0], -c[0]), y1 = __fma_rn(tb, d[1], -c[1]),
                      y2 = __fma_rn(tb, d[2], -c[2]);
         const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
@@ -663,7 +664,7 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
             if (k < K) dr = fmaf(w[k], __ldg(dk + k), dr);
         G.dr = dr;
         G.delta = fminf(fmaxf(dr, -r), r);
-        G.ts = __ddiv_rn(__dadd_rn(B, (double)G.delta), G.A);
+        G.ts = __dmul_rn(__dadd_rn(B, (double)G.delta), iA);
     }
     return make_float4(__double2float_rn(m0), __double2float_rn(m1), __double2float_rn(m2), G.delta);
 }
