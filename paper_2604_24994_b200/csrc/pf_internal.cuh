@@ -49,7 +49,7 @@ struct DeviceScene {
     float sv_gamma = 0.0f, sv_tau = 0.0f;
     float sv_axes[24] = {};
     const float *duv = nullptr, *ddisp = nullptr, *dsv = nullptr;
-    double *cellF = nullptr;          // per cell: m(3) u(3) v(3) |n| |e_k x m| k  (fp64)
+    double *cellF = nullptr;          // per cell: m(3) u(3) v(3) 1/|n| 1/|e_k x m| k  (fp64)
     float *g_uv = nullptr, *g_disp = nullptr, *g_sv = nullptr;   // backward outputs (+=)
 };
 constexpr int kMaxDetail = 8;

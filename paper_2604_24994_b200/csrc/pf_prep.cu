@@ -17,7 +17,7 @@ namespace pf {
 // ------------------------------------------------------------------------
 // Face chart of a detail cell (NEXT-2; the frame of SPEC S:186-189), fp64:
 // m = n/|n|, k = the axis of the smallest |n_k| (ties to the higher index),
-// u = (e_k x m)/|e_k x m|, v = m x u.  cellF[i] = (m, u, v, |n|, |e_k x m|, k).
+// u = (e_k x m)/|e_k x m|, v = m x u.  cellF[i] = (m, u, v, 1/|n|, 1/|e_k x m|, k).
 __device__ __forceinline__ void face_frame(const DeviceScene &ds, int64_t i)
 {
     const float fx = ds.normals[3 * i], fy = ds.normals[3 * i + 1], fz = ds.normals[3 * i + 2];
@@ -37,7 +37,7 @@ __device__ __forceinline__ void face_frame(const DeviceScene &ds, int64_t i)
     F[6] = m1 * u2 - m2 * u1;
     F[7] = m2 * u0 - m0 * u2;
     F[8] = m0 * u1 - m1 * u0;
-    F[9] = nn; F[10] = wl; F[11] = (double)k;
+    F[9] = 1.0 / nn; F[10] = 1.0 / wl; F[11] = (double)k;   // reciprocals: read by K7 only
 }
 
 __global__ void __launch_bounds__(256) k0_edge_records(DeviceScene ds)

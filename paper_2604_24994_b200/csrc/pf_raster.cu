@@ -1335,7 +1335,7 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             else gdr = f;
             // Eq. svdisp at the base-face hit (the chart point in fp64 as in the forward)
             const double B = X.c[0] * m0 + X.c[1] * m1 + X.c[2] * m2;
-            const double tb = B / X.G.A;   // as detail_plane
+            const double tb = B * __drcp_rn(X.G.A);   // as detail_plane
             const double y0 = tb * d0 - X.c[0], y1 = tb * d1 - X.c[1], y2 = tb * d2 - X.c[2];
             const double qb0 = y0 * u0 + y1 * u1 + y2 * u2;
             const double qb1 = y0 * v0 + y1 * v1 + y2 * v2;
@@ -1381,7 +1381,7 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
         gu0 += gv1 * tm2 - gv2 * tm1;           // gv x m
         gu1 += gv2 * tm0 - gv0 * tm2;
         gu2 += gv0 * tm1 - gv1 * tm0;
-        const T iwl = (T)(1.0 / __ldg(F + 10)), inn = (T)(1.0 / __ldg(F + 9));
+        const T iwl = (T)__ldg(F + 10), inn = (T)__ldg(F + 9);   // stored as reciprocals
         const int kax = (int)__ldg(F + 11);
         const T ug = tu0 * gu0 + tu1 * gu1 + tu2 * gu2;
         const T gw0 = (gu0 - tu0 * ug) * iwl, gw1 = (gu1 - tu1 * ug) * iwl,
