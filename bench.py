@@ -1,17 +1,22 @@
 #!/usr/bin/env python
 """bench.py -- Power Foam rasterizer throughput on B200 (BASELINE.json metric).
 
-Default workload: train8_1m (1M-cell Mip-NeRF-360-shaped foam, 8 views at
-1920x1080 per GPU, forward + backward, per-cell gradient all-reduce over NCCL
+Default workload: train8_1m (1M-cell Mip-NeRF-360-shaped foam, a batch of 8
+views at 1920x1080, forward + backward, per-cell gradient all-reduce over NCCL
 when N > 1).  One step = one pass of the whole hot path (K0 edge records, K1
 projection/binning, K2 scan, K3 emit, K4 radix sort, K5 ranges, K6 forward
-blend, K7 backward, K8 unpack, + all-reduce) over one batch of 8 views.
+blend, K7 backward, K8 unpack, + all-reduce) over one batch of views.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Rank 0 prints ONE JSON line.  `value` = frames (views) per second of fwd+bwd
-for the whole job (all ranks; weak scaling: each rank owns 8 distinct views).
+`--gpus N` without torchrun re-launches itself under torch.distributed.run with
+N ranks (one per GPU).  Multi-GPU scaling follows SURVEY §8(e): the batch is
+FIXED (train8_1m: 8 views, sweep64_3m: 64 views) and dealt round-robin over the
+ranks (rank r renders views r, r+N, ...) -- "scaling": "strong"; `--scaling
+weak` gives every rank its own full batch instead, and at N > 1 the strong run
+also reports a weak-scaling figure as an extra field.  Rank 0 prints ONE JSON
+line; `value` = frames (views) per second of the whole job.
 """
 from __future__ import annotations
 
@@ -46,7 +51,12 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="train8_1m",
                     choices=["train8_1m", "mip360_1m", "nerfsynth200k", "sweep64_3m", "small360"])
-    ap.add_argument("--views", type=int, default=None, help="views per GPU (default: preset)")
+    ap.add_argument("--views", type=int, default=None,
+                    help="views per step: the whole batch (strong) or per GPU (weak); "
+                         "default: the preset's batch")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (SURVEY 8(e)): the preset's batch dealt over the ranks; "
+                         "weak: every rank renders a full batch of its own")
     ap.add_argument("--dipoles", action="store_true",
                     help="oriented-point dipole cells (NEXT-1) on the workload's foam")
     ap.add_argument("--detail", type=int, default=0, metavar="K",
@@ -69,19 +79,46 @@ def dist_env():
     return ws, rank, local
 
 
-def workload_cameras(name, n_views, world, rank):
-    """Weak scaling: rank r renders views r, r+N, ... of an orbit of n_views*N cameras."""
+def orbit_cameras(name, total):
+    """The workload's batch of `total` views (an orbit around the scene)."""
     import pf_synth
-    total = n_views * world
     if name in ("train8_1m", "mip360_1m", "sweep64_3m"):
         step = math.radians(5.625) if name == "sweep64_3m" else 2 * math.pi / total
-        cams = pf_synth._cams_mip360(total, 1920, 1080, az_step=step,
+        return pf_synth._cams_mip360(total, 1920, 1080, az_step=step,
                                      jitter=0.3 if name == "sweep64_3m" else 0.0, seed=3)
-    elif name == "nerfsynth200k":
-        cams = pf_synth._cams_nerfsynth(total, 800, 800)
-    else:
-        cams = pf_synth.make_cameras(name, n=total)
-    return cams[rank::world]
+    if name == "nerfsynth200k":
+        return pf_synth._cams_nerfsynth(total, 800, 800)
+    return pf_synth.make_cameras(name, n=total)
+
+
+def plan_views(name, views, scaling, world, rank):
+    """The view deal of SURVEY §8(e).  Returns (total views of the job, indices of
+    this rank's views in the job's orbit).  strong: the batch (`views`, default the
+    preset's) is fixed and dealt round-robin -- rank r gets r, r+N, ...; weak: the
+    orbit has views*N cameras, dealt the same way (views per rank fixed)."""
+    per = views or default_views(name)
+    total = per * world if scaling == "weak" else per
+    if total < world:
+        raise SystemExit(f"bench.py: {total} views cannot be dealt over {world} ranks "
+                         f"(every rank needs at least one view)")
+    if world < 1 or not (0 <= rank < world):
+        raise SystemExit("bench.py: bad world size / rank")
+    return total, list(range(total))[rank::world]
+
+
+def workload_cameras(name, views, scaling, world, rank):
+    total, idx = plan_views(name, views, scaling, world, rank)
+    cams = orbit_cameras(name, total)
+    return [cams[i] for i in idx], total
+
+
+def aggregate_fps(n_local_views, ms_local, reduce_sum=None, reduce_max=None):
+    """Whole-job frames/s: the views ALL ranks processed in one step divided by the
+    slowest rank's step time (max over ranks).  reduce_* are the collectives
+    (identity on one process)."""
+    n = reduce_sum(n_local_views) if reduce_sum else n_local_views
+    ms = reduce_max(ms_local) if reduce_max else ms_local
+    return n / (ms / 1e3), n, ms
 
 
 def default_views(name):
@@ -166,9 +203,38 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def workload_tag(args):
+    return (args.workload + ("+dipoles" if args.dipoles and not args.detail else "") +
+            (f"+detail{args.detail}" if args.detail else "") +
+            ("+fisheye" if args.fisheye else "") +
+            ("+knn_lists" if args.lists == "knn" else ""))
+
+
+def is_train(workload):
+    return workload not in ("mip360_1m", "sweep64_3m")   # forward render-FPS workloads
+
+
+def make_config(args, sc, W, H, total_views, ws):
+    """The JSON line's `config` -- built identically by both arms."""
+    train = is_train(args.workload)
+    return {"workload": workload_tag(args), "cells": sc.num_cells, "edges": sc.num_edges,
+            "batch_views": total_views, "views_per_gpu": total_views / ws,
+            "global_batch_views": total_views, "view_deal": "round-robin (rank r: r, r+N, ...)",
+            "width": W, "height": H, "pass": "fwd+bwd" if train else "fwd",
+            "parallelism": f"dp{ws} (views sharded, per-cell grad all-reduce)",
+            "l2": "inputs larger than L2 (scene records+edges+grad_out > 126 MB)",
+            "k0_policy": "edge records rebuilt every step (training)" if train
+            else "static scene: edge records built once at creation"}
+
+
 # ----------------------------------------------------------------------------
 def run_reference(args):
-    """The oracle (CPU, double) timed on this host on a bounded sample."""
+    """The reference arm = the oracle (CPU, double, O3 tile lists, all host cores),
+    as it stands, on the workload's own scene and views.  Every step (warm-up and
+    timed) renders ONE WHOLE view of the batch (forward, + backward for training
+    workloads) -- a bounded sample of the workload's step -- cycling through the
+    batch; frames/s = views rendered / time, measured, not extrapolated.  Under
+    torchrun only rank 0 works."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
@@ -176,30 +242,43 @@ def run_reference(args):
     import pf_synth
     wl = args.workload
     sc = pf_synth.make_scene(wl, variant=args.lists, dipoles=args.dipoles, detail=args.detail)
-    nv = args.views or default_views(wl)
-    cams = workload_cameras(wl, nv, 1, 0)
-    train = wl not in ("mip360_1m", "sweep64_3m")
-    res = cpu_baseline(sc, cams[0], args.cpu_seconds, train=train)
-    steps = []
+    total, _ = plan_views(wl, args.views, args.scaling, ws, 0)
+    cams = orbit_cameras(wl, total)
+    if args.fisheye:
+        cams = [pf_synth.fisheye(c, 200.0) for c in cams]
+    train = is_train(wl)
+    H, W = cams[0].height, cams[0].width
+    g = pf_synth.make_grad_out(1, H, W, seed=12)[0] if train else None
+
+    def one_view(k):
+        cam = cams[k % len(cams)]
+        oracle.render(sc, cam, mode=oracle.O3)
+        if train:
+            oracle.backward(sc, cam, g, mode=oracle.O3)
+
+    k = 0
+    for _ in range(args.warmup):
+        one_view(k)
+        k += 1
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = cpu_baseline(sc, cams[0], args.cpu_seconds / max(args.steps, 1), train=train,
-                         calib=res["calib"])
-        steps.append(r["value"])
-    val = float(np.median(steps)) if steps else res["value"]
+        one_view(k)
+        k += 1
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    val = 1.0 / dt
+    cores = oracle.num_threads()
+    sample = (f"each step = one whole {W}x{H} view of the {total}-view batch (views cycled), "
+              f"oracle O3 {'forward+backward' if train else 'forward'} in double on "
+              f"{cores} host threads: {dt:.2f} s per view")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * nv / val,
-            "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl + ("+dipoles" if args.dipoles and not args.detail else "") +
-                                   (f"+detail{args.detail}" if args.detail else "") +
-                                   ("+knn_lists" if args.lists == "knn" else ""),
-                       "cells": sc.num_cells, "edges": sc.num_edges, "views_per_gpu": nv,
-                       "global_batch_views": nv * ws, "width": cams[0].width,
-                       "height": cams[0].height, "pass": "fwd+bwd" if train else "fwd",
-                       "parallelism": "oracle on the host cores of rank 0 (CPU, double)"},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": res["cores"],
-                             "kind": "oracle", "sample": res["sample"]},
-            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt,
+            "step_views": 1, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": make_config(args, sc, W, H, total, ws),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "the oracle on rank 0's host cores; ms_per_step is one view (step_views)"}
     print(json.dumps(line), flush=True)
 
 
@@ -261,8 +340,44 @@ def load_traffic(kernel_tag, full=False):
 
 
 # ----------------------------------------------------------------------------
+def _free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def self_launch(args):
+    """`--gpus N` outside torchrun: re-exec under torch.distributed.run with N ranks
+    (one per GPU, rendezvous on 127.0.0.1).  Fails loudly if fewer than N GPUs are
+    visible, or if a torchrun world size disagrees with --gpus."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None:
+        if int(ws_env) != args.gpus and not (args.gpus == 1 and args.impl == "reference"):
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                         f"found {n}")
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # keep the communicator INIT lines visible
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execvpe(sys.executable, cmd, env)
+
+
 def main():
     args = parse()
+    self_launch(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -276,22 +391,36 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
+
+    def red(x, op):
+        if ws == 1:
+            return x
+        t = torch.tensor([float(x)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    red_sum = lambda x: red(x, dist.ReduceOp.SUM)
+    red_max = lambda x: red(x, dist.ReduceOp.MAX)
     wl = args.workload
-    nv = args.views or default_views(wl)
     t_gen = time.perf_counter()
     sc = pf_synth.make_scene(wl, variant=args.lists, dipoles=args.dipoles, detail=args.detail)
-    cams = workload_cameras(wl, nv, ws, rank)
+    cams, total = workload_cameras(wl, args.views, args.scaling, ws, rank)
     if args.fisheye:
         cams = [pf_synth.fisheye(c, 200.0) for c in cams]
+    nv = len(cams)
     t_gen = time.perf_counter() - t_gen
     H, W = cams[0].height, cams[0].width
-    train = wl not in ("mip360_1m", "sweep64_3m")   # forward render-FPS workloads
+    train = is_train(wl)
     # render-FPS workloads draw a fixed scene: its edge records (K0) are built once at
     # creation (PF_STATIC_SCENE); training workloads rebuild them every step
     r = pf.Renderer.from_scene(sc, dev, flags=0 if train else pf.PF_INFERENCE | pf.PF_STATIC_SCENE)
-    # render-only handle on the same tensors (no backward state saved)
-    r_inf = r.sibling(pf.PF_INFERENCE)
+    # render-only handle for the training workloads' forward-only figure (no backward
+    # state saved; edge records still rebuilt per call, as in training).  The render
+    # workloads time `r` itself, so value, ms_per_step and k0_policy describe one run.
+    r_inf = r.sibling(pf.PF_INFERENCE) if train else r
     N = sc.num_cells
     grad_out = torch.from_numpy(pf_synth.make_grad_out(nv, H, W, seed=12 + rank)).to(dev)
     flat = torch.zeros(r.grad_size, device=dev, dtype=torch.float32)
@@ -333,13 +462,7 @@ def main():
     launches = r.launch_count() - l0
     stages = r.stage_times()
     r.set_profiling(False)
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    ms_step = ms / args.steps
-    fps = ws * nv / (ms_step / 1e3)
+    fps, n_all, ms_step = aggregate_fps(nv, e0.elapsed_time(e1) / args.steps, red_sum, red_max)
 
     # ---------------- forward-only throughput (extra) ------------------------
     for _ in range(2):
@@ -351,10 +474,50 @@ def main():
         r_inf.forward(cams, out=out)
     f1.record(stream)
     barrier()
-    tf = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
-    if ws > 1:
-        dist.all_reduce(tf, op=dist.ReduceOp.MAX)
-    fwd_fps = ws * nv / (float(tf.item()) / 1e3)
+    fwd_fps, _, fwd_ms = aggregate_fps(nv, f0.elapsed_time(f1) / args.steps, red_sum, red_max)
+
+    # ---------------- the all-reduce alone (N > 1): time and bus bandwidth ----
+    allreduce = None
+    if ws > 1 and train:
+        for _ in range(3):
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(args.steps):
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+        q1.record(stream)
+        barrier()
+        ar_ms = red_max(q0.elapsed_time(q1) / args.steps)
+        nbytes = flat.numel() * 4
+        allreduce = {"ms": ar_ms, "bytes": nbytes,
+                     "busbw_gbs": 2 * (ws - 1) / ws * nbytes / (ar_ms / 1e3) / 1e9,
+                     "algbw_gbs": nbytes / (ar_ms / 1e3) / 1e9,
+                     "note": "one dist.all_reduce(SUM) of the flat f32 gradient buffer over "
+                             "NCCL, max over ranks; busbw = 2(N-1)/N * bytes / t"}
+
+    # ---------------- weak-scaling figure at N > 1 (extra) --------------------
+    weak = None
+    if ws > 1 and args.scaling == "strong" and train:
+        wcams, wtotal = workload_cameras(wl, args.views, "weak", ws, rank)
+        if args.fisheye:
+            wcams = [pf_synth.fisheye(c, 200.0) for c in wcams]
+        wnv = len(wcams)
+        wg = torch.from_numpy(pf_synth.make_grad_out(wnv, H, W, seed=12 + rank)).to(dev)
+        wout = torch.empty((wnv, H, W, 4), device=dev, dtype=torch.float32)
+        for _ in range(2):
+            pfd.train_step(r, wcams, wg, flat, out=wout)
+        barrier()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for _ in range(args.steps):
+            pfd.train_step(r, wcams, wg, flat, out=wout)
+        w1.record(stream)
+        barrier()
+        wfps, wn, wms = aggregate_fps(wnv, w0.elapsed_time(w1) / args.steps, red_sum, red_max)
+        weak = {"value": wfps, "unit": UNIT, "views_per_gpu": wnv, "global_batch_views": wn,
+                "ms_per_step": wms, "note": "every rank renders its own full batch"}
+        del wg, wout
 
     # ---------------- end to end: host buffers through the public API -------
     e2e = None
@@ -413,10 +576,8 @@ def main():
             stream.wait_event(ev["d2h"][b])
         a1.record(stream)
         barrier()
-        te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
-        if ws > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * nv / (float(te.item()) / 1e3), "unit": UNIT,
+        e2e_fps, _, _ = aggregate_fps(nv, a0.elapsed_time(a1) / args.steps, red_sum, red_max)
+        e2e = {"value": e2e_fps, "unit": UNIT,
                "h2d_bytes_per_step": int(g_host.numel() * 4) if train else 64 * nv,
                "d2h_bytes_per_step": int(res_host[0].numel() * 4),
                "note": ("H2D of the step's dL/dimage from pinned host (overlapping its "
@@ -489,7 +650,7 @@ def main():
         b_view += n_vis * (48 + 16 * deg_mean) + 4 * P + 24 * pix + 72 * n_vis + 16 * pix
     b_step = nv * b_view + sort_bytes
     f_step = nv * (f_bwd if train else f_fwd)
-    step_s = (ms_step if train else float(tf.item())) / 1e3   # this rank's step
+    step_s = ms_step / 1e3   # the slowest rank's step
     roofline_step = {
         "fp32_frac": f_step / step_s / (fp32_peak * 1e12),
         "hbm_frac": b_step / step_s / (hbm * 1e9),
@@ -531,25 +692,17 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": fps if train else fwd_fps, "unit": UNIT, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (pf_synth seeded generator, random-init foam)",
-            "config": {"workload": wl + ("+dipoles" if args.dipoles and not args.detail else "") +
-                                   (f"+detail{args.detail}" if args.detail else "") +
-                                   ("+fisheye" if args.fisheye else "") +
-                                   ("+knn_lists" if args.lists == "knn" else ""), "cells": N,
-                       "edges": sc.num_edges, "views_per_gpu": nv,
-                       "global_batch_views": nv * ws, "width": W, "height": H,
-                       "pass": "fwd+bwd" if train else "fwd",
-                       "parallelism": f"dp{ws} (views sharded, per-cell grad all-reduce)",
-                       "l2": "inputs larger than L2 (scene records+edges+grad_out > 126 MB)",
-                       "k0_policy": "edge records rebuilt every step (training)" if train
-                       else "static scene: edge records built once at creation"},
+            "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (pf_synth seeded generator, random-init foam)",
+            "config": make_config(args, sc, W, H, total, ws),
+            "views_this_rank": nv, "allreduce": allreduce, "weak_scaling": weak,
             "clocks": clocks, "gpu_launches": int(launches),
             "e2e": e2e, "roofline": roofline, "roofline_step": roofline_step, "cpu_baseline": cpu,
             "fwd_fps": fwd_fps, "fwdbwd_fps": fps if train else None,
-            "mpix_s": (fps if train else fwd_fps) * W * H / 1e6, "fwd_mpix_s": fwd_fps * W * H / 1e6,
+            "mpix_s": fps * W * H / 1e6, "fwd_mpix_s": fwd_fps * W * H / 1e6,
             "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
             "stage_launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
             "pairs_per_view": P, "counters_per_view": {"X_s": cnt[0], "X_h": cnt[1],
@@ -561,7 +714,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     r.close()
-    r_inf.close()
+    if r_inf is not r:
+        r_inf.close()
     if ws > 1:
         dist.destroy_process_group()
 

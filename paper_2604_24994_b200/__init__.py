@@ -144,12 +144,16 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
-def _dev_f32(t, shape=None):
+def _dev_f32(t, shape=None, device=None, name="tensor"):
+    """Pointer of a contiguous f32 CUDA tensor; checks its shape and (if given) device,
+    since the kernels write/read exactly the sizes the handle was created with."""
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
             and t.is_contiguous()):
-        raise TypeError("expected a contiguous float32 CUDA tensor")
+        raise TypeError(f"{name}: expected a contiguous float32 CUDA tensor")
     if shape is not None and tuple(t.shape) != tuple(shape):
-        raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, the scene is on {device}")
     return C.c_void_p(t.data_ptr())
 
 
@@ -172,17 +176,30 @@ class Renderer:
         self.detail = detail
         self.K = 0 if detail is None else int(detail["uv"].shape[1])
         self._tensors = (sites, weights, radii, density, rgb, nbr_offsets, nbr_indices, normals)
-        for t in (sites, weights, radii, density, rgb) + ((normals,) if self.has_normals else ()):
-            _dev_f32(t)
+        N, dev = self.N, self.device
+        _dev_f32(sites, (N, 3), dev, "sites")
+        _dev_f32(weights, (N,), dev, "weights")
+        _dev_f32(radii, (N,), dev, "radii")
+        _dev_f32(density, (N,), dev, "density")
+        _dev_f32(rgb, (N, 3), dev, "rgb")
+        if self.has_normals:
+            _dev_f32(normals, (N, 3), dev, "normals")
         if detail is not None:
             K = self.K
-            _dev_f32(detail["uv"], (self.N, K, 2))
-            _dev_f32(detail["disp"], (self.N, K))
-            _dev_f32(detail["sv"], (self.N, K, 8, 3))
+            _dev_f32(detail["uv"], (N, K, 2), dev, "detail uv")
+            _dev_f32(detail["disp"], (N, K), dev, "detail disp")
+            _dev_f32(detail["sv"], (N, K, 8, 3), dev, "detail sv")
         if nbr_offsets.dtype != torch.int64 or nbr_indices.dtype != torch.int32:
             raise TypeError("nbr_offsets must be int64 and nbr_indices int32")
         if not (nbr_offsets.is_cuda and nbr_indices.is_cuda):
             raise TypeError("neighbour lists must be CUDA tensors")
+        if nbr_offsets.device != dev or nbr_indices.device != dev:
+            raise ValueError("neighbour lists must be on the scene's device")
+        if not (nbr_offsets.is_contiguous() and nbr_indices.is_contiguous()):
+            raise TypeError("neighbour lists must be contiguous")
+        if nbr_offsets.dim() != 1 or nbr_offsets.numel() != N + 1:
+            raise ValueError(f"nbr_offsets: expected {N + 1} entries, got "
+                             f"{tuple(nbr_offsets.shape)}")
         E = int(nbr_indices.numel()) if num_edges is None else int(num_edges)
         d = _SceneDesc()
         d.num_cells = self.N
@@ -270,11 +287,13 @@ class Renderer:
         H, W = arr[0].height, arr[0].width
         if out is None:
             out = torch.empty((V, H, W, 4), device=self.device, dtype=torch.float32)
-        _dev_f32(out, (V, H, W, 4))
+        _dev_f32(out, (V, H, W, 4), self.device, "out")
         ex = None
         if stats is not None:
-            ex = (C.c_void_p * 2)(_dev_f32(stats["contrib"], (self.N,)).value,
-                                  _dev_f32(stats["normal"], (self.N,)).value
+            ex = (C.c_void_p * 2)(_dev_f32(stats["contrib"], (self.N,), self.device,
+                                           "stats contrib").value,
+                                  _dev_f32(stats["normal"], (self.N,), self.device,
+                                           "stats normal").value
                                   if stats.get("normal") is not None else None)
         _check(self._L.pf_render_forward_ex(self._h, arr, V, C.c_void_p(out.data_ptr()),
                                             ex, _stream(stream)))
@@ -285,19 +304,37 @@ class Renderer:
         zeros if None)."""
         arr, V = _cams(cams)
         H, W = arr[0].height, arr[0].width
-        _dev_f32(grad_out, (V, H, W, 4))
+        _dev_f32(grad_out, (V, H, W, 4), self.device, "grad_out")
         if grads is None:
             grads = torch.zeros(self.grad_size, device=self.device, dtype=torch.float32)
-        views = self.grad_views(grads) if isinstance(grads, torch.Tensor) else grads
+        if isinstance(grads, torch.Tensor):
+            _dev_f32(grads, (self.grad_size,), self.device, "flat grads")
+            views = self.grad_views(grads)
+        else:
+            views = grads
+        shapes = self.grad_shapes()
         g = _Grads()
         for k in ("sites", "weights", "radii", "density", "rgb"):
-            setattr(g, k, _dev_f32(views[k]).value)
-        g.normals = _dev_f32(views["normals"]).value if "normals" in views else None
+            setattr(g, k, _dev_f32(views[k], shapes[k], self.device, f"grads[{k!r}]").value)
+        g.normals = (_dev_f32(views["normals"], shapes["normals"], self.device,
+                              "grads['normals']").value
+                     if self.has_normals and "normals" in views else None)
         for k in ("detail_uv", "detail_disp", "detail_sv"):
-            setattr(g, k, _dev_f32(views[k]).value if k in views else None)
+            setattr(g, k, _dev_f32(views[k], shapes[k], self.device, f"grads[{k!r}]").value
+                    if self.K and k in views else None)
         _check(self._L.pf_render_backward_ex(self._h, arr, V, C.c_void_p(grad_out.data_ptr()),
                                              C.byref(g), _stream(stream)))
         return views
+
+    def grad_shapes(self):
+        """Shape of every gradient array the backward writes (param_names order)."""
+        N, K = self.N, self.K
+        sh = {"sites": (N, 3), "weights": (N,), "radii": (N,), "density": (N,), "rgb": (N, 3)}
+        if self.has_normals:
+            sh["normals"] = (N, 3)
+        if K:
+            sh.update(detail_uv=(N, K, 2), detail_disp=(N, K), detail_sv=(N, K, 8, 3))
+        return sh
 
     def grad_views(self, flat):
         """Views of a flat gradient buffer as the parameter arrays (one NCCL buffer)."""

@@ -503,13 +503,14 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
     const size_t npix = (size_t)cams[0].width * cams[0].height;
     const bool record = !(s->flags & PF_INFERENCE);
     if (record) {
-        // adapt the record-arena size to what the previous forward used
+        // adapt the record-arena size to what the previous forward used (records per
+        // pair of THAT forward: bin_views has already overwritten views[v].P)
         if (s->rec_seen_views > 0 && !s->rec_ratio_fixed) {
             for (int v = 0; v < s->rec_seen_views; ++v) {
-                const pf::ViewState &pv = s->views[v];
+                const int64_t prevP = s->rec_prev_P[v];
                 const uint32_t used = s->pinned_rec[v];
-                if (pv.P > 0 && used > 0)
-                    s->rec_ratio = fmax(s->rec_ratio * 0.98, 1.3 * (double)used / (double)pv.P);
+                if (prevP > 0 && used > 0)
+                    s->rec_ratio = fmax(s->rec_ratio * 0.98, 1.3 * (double)used / (double)prevP);
             }
         }
         PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * (size_t)V));
@@ -546,6 +547,8 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
         }
         PF_CUDA(cudaMemcpyAsync(s->pinned_rec, s->rec_used.ptr, sizeof(uint32_t) * (size_t)V,
                                 cudaMemcpyDeviceToHost, st));
+        s->rec_prev_P.resize(V);
+        for (int v = 0; v < V; ++v) s->rec_prev_P[v] = s->views[v].P;
         s->rec_seen_views = V;   // read at the next forward, after its sync
     }
     s->fwd_cams.assign(cams, cams + V);

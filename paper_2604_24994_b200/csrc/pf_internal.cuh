@@ -103,6 +103,7 @@ struct pf_scene {
     double rec_ratio = 3.0;         // arena capacity in records per (tile, cell) pair
     uint32_t *pinned_rec = nullptr; // host copy of rec_used from the previous forward
     int pinned_rec_n = 0, rec_seen_views = 0;
+    std::vector<int64_t> rec_prev_P; // per-view pair counts of the forward pinned_rec came from
     bool rec_ratio_fixed = false;   // PF_REC_RATIO set (tests of the overflow path)
     std::vector<pf::ViewState> views;
     pf::ViewState debug_view;       // pf_debug_* scratch (leaves the forward state intact)

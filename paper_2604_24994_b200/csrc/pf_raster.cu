@@ -1221,9 +1221,11 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
         const float2 *uv = reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell;
         // ---- forward: Eq. svrad at x (the interval entry for a parallel ray)
         const double tcol = X.G.parallel ? (double)__fadd_rn(g.tc, g.lo) : X.G.ts;
-        const double ys0 = tcol * d0 - X.c[0], ys1 = tcol * d1 - X.c[1], ys2 = tcol * d2 - X.c[2];
-        const double qs0 = ys0 * u0 + ys1 * u1 + ys2 * u2;
-        const double qs1 = ys0 * v0 + ys1 * v1 + ys2 * v2;
+        // the chart point by detail_color's explicit op sequence (bit-identical weights)
+        const double ys0 = __fma_rn(tcol, d0, -X.c[0]), ys1 = __fma_rn(tcol, d1, -X.c[1]),
+                     ys2 = __fma_rn(tcol, d2, -X.c[2]);
+        const double qs0 = __fma_rn(ys0, u0, __fma_rn(ys1, u1, __dmul_rn(ys2, u2)));
+        const double qs1 = __fma_rn(ys0, v0, __fma_rn(ys1, v1, __dmul_rn(ys2, v2)));
         float ws[kMaxDetail], dG[kMaxDetail];
         float2 st[kMaxDetail];
         load_sites(uv, K, st);
@@ -1334,11 +1336,14 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             else if (X.G.dr < -r) o.r -= (float)f;      // delta = -r
             else gdr = f;
             // Eq. svdisp at the base-face hit (the chart point in fp64 as in the forward)
-            const double B = X.c[0] * m0 + X.c[1] * m1 + X.c[2] * m2;
-            const double tb = B * __drcp_rn(X.G.A);   // as detail_plane
-            const double y0 = tb * d0 - X.c[0], y1 = tb * d1 - X.c[1], y2 = tb * d2 - X.c[2];
-            const double qb0 = y0 * u0 + y1 * u1 + y2 * u2;
-            const double qb1 = y0 * v0 + y1 * v1 + y2 * v2;
+            // detail_plane's explicit op sequence, so x_bar (and the unit vectors taken
+            // there) is bit-identical to the forward's
+            const double B = dot3d(X.c, m0, m1, m2);
+            const double tb = __dmul_rn(B, __drcp_rn(X.G.A));
+            const double y0 = __fma_rn(tb, d0, -X.c[0]), y1 = __fma_rn(tb, d1, -X.c[1]),
+                         y2 = __fma_rn(tb, d2, -X.c[2]);
+            const double qb0 = __fma_rn(y0, u0, __fma_rn(y1, u1, __dmul_rn(y2, u2)));
+            const double qb1 = __fma_rn(y0, v0, __fma_rn(y1, v1, __dmul_rn(y2, v2)));
             const float *wb = X.G.w;   // detail_plane's weights at x_bar
             sv_units<T>(st, K, qb0, qb1, ux, uy);
             const float *dk = ds.ddisp + (size_t)K * cell;

@@ -87,3 +87,70 @@ def test_sharded_allreduce_equals_single_process_sum():
     for _, _, flat in res:   # every rank holds the same reduced gradient
         np.testing.assert_allclose(flat, ref.numpy(), rtol=1e-12, atol=1e-15)
     assert np.abs(ref.numpy()).max() > 0
+
+
+def _bench_worker(rank, ws, port, q):
+    """bench.py's own view deal and whole-job FPS arithmetic under a real
+    2-rank process group (gloo stands in for NCCL)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import bench
+
+    def red(x, op):
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    res = {}
+    for wl, scaling in (("train8_1m", "strong"), ("sweep64_3m", "strong"),
+                        ("train8_1m", "weak"), ("nerfsynth200k", "strong")):
+        total, idx = bench.plan_views(wl, None, scaling, ws, rank)
+        cams, total2 = bench.workload_cameras(wl, None, scaling, ws, rank)
+        assert total2 == total and len(cams) == len(idx)
+        ms_local = 10.0 + 5.0 * rank          # rank 1 is the slow one
+        fps, n, ms = bench.aggregate_fps(len(idx), ms_local,
+                                         lambda x: red(x, dist.ReduceOp.SUM),
+                                         lambda x: red(x, dist.ReduceOp.MAX))
+        res[(wl, scaling)] = (total, idx, fps, n, ms,
+                              [float(c.c2w[3]) for c in cams])
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_view_deal_and_fps_arithmetic_two_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    import bench
+    expect_total = {("train8_1m", "strong"): 8, ("sweep64_3m", "strong"): 64,
+                    ("train8_1m", "weak"): 16, ("nerfsynth200k", "strong"): 8}
+    for key, total in expect_total.items():
+        r0, r1 = res[0][key], res[1][key]
+        assert r0[0] == r1[0] == total
+        # SURVEY 8(e): rank r gets v = r (mod N); together a partition of the batch
+        assert r0[1] == list(range(0, total, 2)) and r1[1] == list(range(1, total, 2))
+        # whole-job frames/s = all views / the slowest rank's step (max over ranks)
+        for r in (r0, r1):
+            assert r[3] == total and r[4] == 15.0
+            assert abs(r[2] - total / 0.015) < 1e-9
+        # the dealt cameras are the single-process batch's cameras at those indices
+        cams = bench.orbit_cameras(key[0], total)
+        got = dict(zip(r0[1], r0[5]))
+        got.update(zip(r1[1], r1[5]))
+        assert [got[i] for i in range(total)] == [float(c.c2w[3]) for c in cams]
+    # strong scaling: the 8-view batch is the 1-GPU batch (same cameras at any N)
+    one, _ = bench.plan_views("train8_1m", None, "strong", 1, 0)
+    assert one == 8
+    with pytest.raises(SystemExit):
+        bench.plan_views("mip360_1m", None, "strong", 2, 0)   # 1 view over 2 ranks
