@@ -78,6 +78,9 @@ def lib():
         L.oracle_pixel_ray.argtypes = [P, C.c_int32, C.c_int32, P, P, P]
         L.oracle_composite.argtypes = [i64, P, P, P, P, P]
         L.oracle_composite.restype = i64
+        L.oracle_trace.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, i64, P, P, P, C.c_int]
+        L.oracle_trace_cells.argtypes = [i64, P, P, P, P, P, P, P, C.c_double, P, i64]
+        L.oracle_trace_cells.restype = i64
         L.oracle_num_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -318,6 +321,37 @@ def composite(sigma, dt, rgb, bg=(0.0, 0.0, 0.0)):
     out = np.zeros(4)
     K = lib().oracle_composite(len(sigma), _p(sigma), _p(dt), _p(rgb), _p(bga), _p(out))
     return out, int(K)
+
+
+def trace(sc, cam, pixels=None, nthreads=0):
+    """NEXT-4 adjacency-walk ray tracer (double): dict(out f64[n,4] or [H,W,4],
+    stats i64[n,3] = (cells visited, locate calls, composited segments))."""
+    A = _SceneArrays(sc)
+    oc = make_camera(cam)
+    if pixels is None:
+        n = cam.width * cam.height
+        pix = None
+    else:
+        pix = _c(np.asarray(pixels).reshape(-1, 2), np.int32)
+        n = pix.shape[0]
+    out = np.zeros((n, 4), np.float64)
+    st = np.zeros((n, 3), np.int64)
+    lib().oracle_trace(*A.args(), C.byref(oc), n, _p(pix), _p(out), _p(st), nthreads)
+    if pixels is None:
+        out = out.reshape(cam.height, cam.width, 4)
+        st = st.reshape(cam.height, cam.width, 3)
+    return dict(out=out, stats=st)
+
+
+def trace_cells(sc, Q, d, t_near=0.0, cap=4096):
+    """The cells the tracer's walk visits along the ray Q + t d, in order."""
+    A = _SceneArrays(sc)
+    Qa = _c(Q, np.float64)
+    da = _c(d, np.float64)
+    cells = np.zeros(cap, np.int32)
+    n = lib().oracle_trace_cells(A.N, _p(A.sites), _p(A.weights), _p(A.radii), _p(A.off),
+                                 _p(A.idx), _p(Qa), _p(da), float(t_near), _p(cells), cap)
+    return [int(c) for c in cells[:min(n, cap)]]
 
 
 def num_threads() -> int:

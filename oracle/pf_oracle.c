@@ -1368,6 +1368,179 @@ int oracle_num_threads(void)
 }
 
 /* ======================================================================== */
+/* NEXT-4: the adjacency-walk ray tracer (§3.1, §3.2,        */
+/* P:687-689 App. C)                                                        */
+/* ======================================================================== */
+/*
+ * The paper traces by walking from cell to cell: "the adjacency information
+ * ... allows a ray to walk from one cell to the next by checking all faces"
+ * (P:157), with the Delaunay graph "replaced with the dual graph of the power
+ * diagram, in addition to considering the sphere bounds in the computation of
+ * intersection lengths".  Reading R7: the paper walks
+ * the UNBOUNDED diagram's dual (the regular triangulation), which is out
+ * of scope; a bounded cell's interval, however, only ends on a radical plane of
+ * a Čech neighbour (the face's owner is the next cell) or on its own
+ * bounding sphere.  With the paper's weights w = r^2 no other ball
+ * contains a sphere-exit point (there pow_c = 0 <= pow_k), so the ray is in a
+ * gap of the union of balls and the walk resumes at the next point of the union
+ * (a "gap jump"; here by brute force over every ball).  Step by step:
+ *   t <- t_near;  c <- locate(t)
+ *   loop:  walk interval [t_in, t_out] of c (sphere, near, c's list planes;
+ *          O2 semantics) and the constraint that ends it;
+ *          the occupied segment (the dipole / detail clip applied, exactly the
+ *          interval the rasterizer composites) -> front-to-back compositing,
+ *          stop after the segment that makes T < 1e-4;
+ *          exit on the plane of neighbour j: c <- j, t <- t_out;
+ *          exit on the sphere: t <- t_out, c <- locate(t, excluding c).
+ *   locate(t): among the balls whose chord ends after t, the smallest
+ *          max(t_entry, t); ties by the smaller power pow(x, b) at that point
+ *          (a point inside several balls belongs to the argmin-power cell), then
+ *          by the lower index.
+ * A step that makes no progress (a degenerate crossing through an edge or a
+ * vertex, measure zero) falls back to locate(t, excluding c); a step budget
+ * of 4N + 64 guards termination.
+ * Per pixel the stats are (cells visited, locate calls, composited segments).
+ */
+static int64_t trace_locate(const oc_scene *S, const double Q[3], const double d[3], double t,
+                            int64_t excl, double *t_at)
+{
+    int64_t best = -1;
+    double bt = 0.0, bp = 0.0;
+    for (int64_t b = 0; b < S->N; ++b) {
+        if (b == excl) continue;
+        const float *p = S->sites + 3 * b;
+        double c[3] = {p[0] - Q[0], p[1] - Q[1], p[2] - Q[2]};
+        double tc = d[0] * c[0] + d[1] * c[1] + d[2] * c[2];
+        double e[3] = {c[0] - tc * d[0], c[1] - tc * d[1], c[2] - tc * d[2]};
+        double r = (double)S->radii[b];
+        double h = r * r - (e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+        if (!(h > 0.0)) continue;
+        double sq = sqrt(h);
+        if (!(tc + sq > t)) continue;
+        double tt = tc - sq > t ? tc - sq : t;
+        double x[3] = {Q[0] + tt * d[0], Q[1] + tt * d[1], Q[2] + tt * d[2]};
+        double pw = powd(x, p, S->weights[b]);
+        if (best < 0 || tt < bt || (tt == bt && pw < bp)) {
+            best = b;
+            bt = tt;
+            bp = pw;
+        }
+    }
+    *t_at = bt;
+    return best;
+}
+
+static void trace_pixel(const oc_scene *S, const double Q[3], const double d[3], double tn,
+                        double out[4], int64_t st[3])
+{
+    oc_scene W = *S; /* the walk's geometry: the power cell inside the ball, no dipole clip */
+    W.normals = NULL;
+    W.det = NULL;
+    double T = 1.0, C[3] = {0.0, 0.0, 0.0};
+    int64_t visited = 0, located = 0, nseg = 0;
+    double t = tn, tl;
+    int64_t c = trace_locate(S, Q, d, t, -1, &tl);
+    ++located;
+    const int64_t budget = 4 * S->N + 64;
+    for (int64_t step = 0; c >= 0 && step < budget; ++step) {
+        oc_seg w, o;
+        int64_t np = 0;
+        const int hit = cell_interval(&W, O2_LIST_PLANES, c, Q, d, tn, &w, &np);
+        if (!hit || !(w.t_out > w.t_in) || !(w.t_out > t)) {
+            /* no progress in c (degenerate crossing): locate past it */
+            const int64_t prev = c;
+            c = trace_locate(S, Q, d, t, prev, &tl);
+            ++located;
+            continue;
+        }
+        ++visited;
+        if (cell_interval(S, O2_LIST_PLANES, c, Q, d, tn, &o, &np) && o.t_out > o.t_in) {
+            const double sig = (double)S->density[c];
+            const double tau = sig * (o.t_out - o.t_in);
+            const double alpha = 1.0 - exp(-tau);
+            for (int k = 0; k < 3; ++k) C[k] += T * alpha * o.col[k];
+            T *= exp(-tau);
+            ++nseg;
+            if (T < T_STOP) break;
+        }
+        t = w.t_out;
+        if (w.kout == END_PLANE) {
+            c = w.jout;
+        } else {
+            const int64_t prev = c;
+            c = trace_locate(S, Q, d, t, prev, &tl);
+            ++located;
+        }
+    }
+    for (int k = 0; k < 3; ++k) out[k] = C[k] + T * S->bg[k];
+    out[3] = T;
+    st[0] = visited;
+    st[1] = located;
+    st[2] = nseg;
+}
+
+/* Trace npix pixels (pix_xy = int32 (x,y) pairs; NULL = the full image).
+ * out double[npix*4] = (C + T bg, T); stats int64[npix*3] (may be NULL). */
+int oracle_trace(int64_t N, const float *sites, const float *weights, const float *radii,
+                 const float *density, const float *rgb, const int64_t *nbr_off,
+                 const int32_t *nbr_idx, const float *bg, const float *normals,
+                 const oc_detail *det, const oc_camera *cam, int64_t npix, const int32_t *pix_xy,
+                 double *out, int64_t *stats, int nthreads)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, density, rgb, nbr_off, nbr_idx, bg, normals, det);
+    if (!pix_xy) npix = (int64_t)cam->width * cam->height;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < npix; ++q) {
+        int x = pix_xy ? pix_xy[2 * q] : (int)(q % cam->width);
+        int y = pix_xy ? pix_xy[2 * q + 1] : (int)(q / cam->width);
+        double Q[3], d[3], tn;
+        int64_t st[3] = {0, 0, 0};
+        if (pixel_ray(cam, x + 0.5, y + 0.5, Q, d, &tn)) {
+            trace_pixel(&S, Q, d, tn, out + 4 * q, st);
+        } else {
+            for (int k = 0; k < 3; ++k) out[4 * q + k] = S.bg[k];
+            out[4 * q + 3] = 1.0;
+        }
+        if (stats)
+            for (int k = 0; k < 3; ++k) stats[3 * q + k] = st[k];
+    }
+    return 0;
+}
+
+/* The walk of one ray (Q, d, t_near): the visited cells in order (up to cap),
+ * returns their number (the sequence test against the argmin-power sampler). */
+int64_t oracle_trace_cells(int64_t N, const float *sites, const float *weights,
+                           const float *radii, const int64_t *nbr_off, const int32_t *nbr_idx,
+                           const double *Q, const double *d, double tn, int32_t *cells,
+                           int64_t cap)
+{
+    oc_scene S;
+    make_scene(&S, N, sites, weights, radii, NULL, NULL, nbr_off, nbr_idx, NULL, NULL, NULL);
+    int64_t n = 0;
+    double t = tn, tl;
+    int64_t c = trace_locate(&S, Q, d, t, -1, &tl);
+    const int64_t budget = 4 * N + 64;
+    for (int64_t step = 0; c >= 0 && step < budget; ++step) {
+        oc_seg w;
+        int64_t np = 0;
+        if (!cell_interval(&S, O2_LIST_PLANES, c, Q, d, tn, &w, &np) || !(w.t_out > w.t_in) ||
+            !(w.t_out > t)) {
+            c = trace_locate(&S, Q, d, t, c, &tl);
+            continue;
+        }
+        if (n < cap) cells[n] = (int32_t)c;
+        ++n;
+        t = w.t_out;
+        c = (w.kout == END_PLANE) ? w.jout : trace_locate(&S, Q, d, t, c, &tl);
+    }
+    return n;
+}
+
+/* ======================================================================== */
 /* NEXT-3: the Čech graph ("the graph of all overlapping spheres")    */
 /* ======================================================================== */
 

@@ -41,6 +41,12 @@ def case(name, variant=None):
         elif name == "train8_1m":
             sc = pf_synth.make_scene("train8_1m")
             cams = pf_synth.make_cameras("train8_1m")
+        elif name == "mip360_1m":
+            sc = pf_synth.make_scene("mip360_1m")
+            cams = pf_synth.make_cameras("mip360_1m")
+        elif name == "sweep64_3m":
+            sc = pf_synth.make_scene("sweep64_3m")
+            cams = pf_synth.make_cameras("sweep64_3m")
         elif name.endswith("+detail"):
             base, bcams = case(name[:-len("+detail")], variant)
             sc = pf_synth.add_detail(base.copy())
@@ -60,11 +66,89 @@ def renderer(sc, flags=None):
     return pf.Renderer.from_scene(sc, "cuda", flags=pf.PF_VALIDATE if flags is None else flags)
 
 
-def grad_check(gpu, ref, tol=GRAD_TOL):
+COND_LIMIT = 0.05   # a per-cell C17 failure must come with a min(s/r, |a|/|n|) below this
+
+
+def _pixel_rays(cam, pix):
+    """Rays (Q, d[n,3], t_near[n]) of pixels pix[n,2]: the oracle's pixel_ray."""
+    Q = None
+    D = np.zeros((len(pix), 3))
+    tn = np.zeros(len(pix))
+    for k, (x, y) in enumerate(pix):
+        Q, D[k], tn[k] = oracle.pixel_ray(cam, int(x), int(y))
+    return Q, D, tn
+
+
+def _all_pixels(cam):
+    ys, xs = np.mgrid[0:cam.height, 0:cam.width]
+    return np.stack([xs.ravel(), ys.ravel()], 1)
+
+
+def conditioning(sc, views, cell, mode=None):
+    """SURVEY C17 conditioning of one cell over the pixels that carry gradient:
+    views = [(cam, pix or None)].  For every composited segment in which `cell` is
+    the segment's cell or the binding neighbour: s/r of a sphere endpoint (s the
+    half chord, R1) and |a|/|n| = |d.n|/|n| of a binding plane (or dipole face).
+    Returns (min s/r, min |a|/|n|, pixels seen)."""
+    P = sc.sites.astype(np.float64)
+    r = sc.radii.astype(np.float64)
+    best_s, best_a, npix = np.inf, np.inf, 0
+    for cam, pix in views:
+        pix = _all_pixels(cam) if pix is None else np.asarray(pix)
+        if cam.model == 0:
+            M = np.asarray(cam.c2w, np.float64).reshape(3, 4)
+            dc = np.stack([(pix[:, 0] + 0.5 - cam.cx) / cam.fx, (pix[:, 1] + 0.5 - cam.cy) / cam.fy,
+                           np.ones(len(pix))], 1)
+            D = dc @ M[:, :3].T
+            D /= np.linalg.norm(D, axis=1, keepdims=True)
+            Q = M[:, 3]
+        else:
+            Q, D, _ = _pixel_rays(cam, pix)
+        c = P[cell] - Q
+        tc = D @ c
+        rho2 = c @ c - tc * tc
+        cand = pix[rho2 < r[cell] ** 2 * (1 + 1e-9)]
+        m = (oracle.O1 if sc.num_cells <= 4096 else oracle.O2) if mode is None else mode
+        for x, y in cand:
+            segs = oracle.pixel_segments(sc, cam, int(x), int(y), mode=m)
+            Qp, d, _ = oracle.pixel_ray(cam, int(x), int(y))
+            for sg in segs:
+                i = int(sg["cell"])
+                roles = []
+                if i == cell:
+                    roles = [("in", sg["kin"], sg["jin"]), ("out", sg["kout"], sg["jout"])]
+                else:
+                    roles = [(e, k, j) for e, k, j in (("in", sg["kin"], sg["jin"]),
+                                                       ("out", sg["kout"], sg["jout"]))
+                             if int(k) == 2 and int(j) == cell]
+                if not roles:
+                    continue
+                npix += 1
+                for _, kind, j in roles:
+                    kind, j = int(kind), int(j)
+                    if kind == 0:        # sphere endpoint of cell i: s/r
+                        ci = P[i] - Qp
+                        h = r[i] ** 2 - (ci @ ci - (d @ ci) ** 2)
+                        best_s = min(best_s, np.sqrt(max(h, 0.0)) / r[i])
+                    elif kind == 2:      # plane between i and j
+                        n = P[j] - P[i]
+                        best_a = min(best_a, abs(d @ n) / np.linalg.norm(n))
+                    elif kind == 3 and sc.normals is not None:
+                        nv = sc.normals[i].astype(np.float64)
+                        best_a = min(best_a, abs(d @ nv) / np.linalg.norm(nv))
+    return best_s, best_a, npix
+
+
+def grad_check(gpu, ref, tol=GRAD_TOL, ctx=None):
+    """normwise per array <= tol; per cell |g_i - g_ref,i| <= 1e-3 |g_ref,i|
+    + 1e-5 max |g_ref|.  Every cell that fails the per-cell bar is LISTED with its
+    conditioning (ctx = (scene, [(cam, pixels-or-None)])) and must be ill-conditioned
+    (min(s/r, |a|/|n|) < COND_LIMIT); without ctx no per-cell failure is accepted."""
     msgs = []
     keys = ("sites", "weights", "radii", "density", "rgb") + (("normals",) if "normals" in ref
                                                                else ())
     keys += tuple(k for k in ("detail_uv", "detail_disp", "detail_sv") if k in ref)
+    failing = {}
     for k in keys:
         a = gpu[k].detach().cpu().numpy().astype(np.float64).reshape(-1)
         b = ref[k].reshape(-1)
@@ -72,12 +156,24 @@ def grad_check(gpu, ref, tol=GRAD_TOL):
         rel = np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
         msgs.append(f"{k}: {rel:.2e}")
         assert rel <= tol, ", ".join(msgs)
-        # secondary, per cell: |g_i - g_ref,i| <= 1e-3 |g_ref,i| + 1e-5 max |g_ref|
         N = ref["density"].shape[0]
         ac, bc = a.reshape(N, -1), b.reshape(N, -1)
         ni = np.linalg.norm(bc, axis=1)
-        bad = np.linalg.norm(ac - bc, axis=1) > 1e-3 * ni + 1e-5 * ni.max()
-        assert bad.sum() <= 1e-3 * (ni > 0).sum(), (k, np.flatnonzero(bad)[:10])
+        err = np.linalg.norm(ac - bc, axis=1)
+        bad = err > 1e-3 * ni + 1e-5 * ni.max()
+        for c in np.flatnonzero(bad):
+            failing.setdefault(int(c), []).append((k, float(err[c] / max(ni[c], 1e-30))))
+    if failing:
+        assert ctx is not None, f"per-cell C17 failures (no conditioning context): {failing}"
+        sc, views = ctx
+        lines = []
+        for c, what in sorted(failing.items()):
+            s_r, a_n, npx = conditioning(sc, views, c)
+            lines.append(f"cell {c}: {what} min s/r {s_r:.2e} min |a|/|n| {a_n:.2e} "
+                         f"({npx} segments)")
+            assert min(s_r, a_n) < COND_LIMIT, "well-conditioned cell fails C17: " + lines[-1]
+        print("per-cell C17 failures (ill-conditioned, listed):\n  " + "\n  ".join(lines))
+        msgs.append(f"{len(failing)} ill-conditioned cells listed")
     return msgs
 
 
@@ -215,7 +311,7 @@ def test_backward_full_image(name, variant):
     for v, cam in enumerate(cams):
         o = oracle.backward(sc, cam, g[v], mode=mode)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(c, None) for c in cams]))
     r.close()
 
 
@@ -240,7 +336,7 @@ def test_backward_large_sampled_pixels(name):
     for v, p in pix.items():
         o = oracle.backward(sc, cams[v], g[v, p[:, 1], p[:, 0]], mode=oracle.O3, pixels=p)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(cams[v], p) for v, p in pix.items()]))
     r.close()
 
 
@@ -353,7 +449,7 @@ def test_backward_record_overflow_fallback(monkeypatch):
     for v, cam in enumerate(cams):
         o = oracle.backward(sc, cam, g[v], mode=oracle.O3)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(c, None) for c in cams]))
     r.close()
 
 
@@ -423,7 +519,7 @@ def test_dipole_forward_and_backward_full_image(name, variant):
     for v, cam in enumerate(cams):
         o = oracle.backward(sc, cam, g[v], mode=mode)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(c, None) for c in cams]))
     r.close()
 
 
@@ -447,7 +543,7 @@ def test_dipole_large_sampled_pixels():
     for v, p in pix.items():
         o = oracle.backward(sc, cams[v], g[v, p[:, 1], p[:, 0]], mode=oracle.O3, pixels=p)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(cams[v], p) for v, p in pix.items()]))
     r.close()
 
 
@@ -580,7 +676,7 @@ def test_fisheye_forward_backward(name, variant):
     for v, cam in enumerate(cams):
         o = oracle.backward(sc, cam, g[v], mode=mode)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(c, None) for c in cams]))
     r.close()
 
 
@@ -599,7 +695,7 @@ def _full_parity(sc, cams, mode, seed):
     for v, cam in enumerate(cams):
         o = oracle.backward(sc, cam, g[v], mode=mode)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    msgs = grad_check(got, ref)
+    msgs = grad_check(got, ref, ctx=(sc, [(c, None) for c in cams]))
     r.close()
     return msgs
 
@@ -639,7 +735,7 @@ def test_detail_large_sampled_pixels():
     for v, p in pix.items():
         o = oracle.backward(sc, cams[v], g[v, p[:, 1], p[:, 0]], mode=oracle.O3, pixels=p)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(cams[v], p) for v, p in pix.items()]))
     r.close()
 
 
@@ -663,7 +759,7 @@ def test_detail_autograd_and_by_products():
     g = torch.from_numpy(pf_synth.make_grad_out(1, cams[0].height, cams[0].width, seed=3)).cuda()
     (out * g).sum().backward()
     ref = oracle.backward(sc, cams[0], g[0].cpu().numpy(), mode=oracle.O3)
-    grad_check(dict(zip(r2.param_names, [p.grad for p in params])), ref)
+    grad_check(dict(zip(r2.param_names, [p.grad for p in params])), ref, ctx=(sc, [(cams[0], None)]))
     N = sc.num_cells
     st = {"contrib": torch.zeros(N, device="cuda"), "normal": torch.zeros(N, device="cuda")}
     r.forward(cams[:1], stats=st)
@@ -708,7 +804,7 @@ def _parity_one(sc, cams, mode=oracle.O3, seed=29, flags=None):
     for v, cam in enumerate(cams):
         o = oracle.backward(sc, cam, g[v], mode=mode)
         ref = o if ref is None else {k: ref[k] + o[k] for k in ref}
-    grad_check(got, ref)
+    grad_check(got, ref, ctx=(sc, [(c, None) for c in cams]))
     r.close()
     return out
 
@@ -771,3 +867,82 @@ def test_edge_dense_single_tile_long_list():
     assert b["P"] > 0.8 * n      # (nearly) every cell lands in the one tile
     r_.close()
     _parity_one(sc, [cam])
+
+
+# --------------------------------------------------------------- bench configurations
+
+def test_static_inference_mip360_1m():
+    """The render-FPS handle of bench.py (PF_STATIC_SCENE | PF_INFERENCE: edge records
+    built once at creation, no backward state) on mip360_1m: bit-identical to the
+    training handle's image on every call, and the oracle on sampled pixels (3000 vs
+    O3 tile lists, 24 vs O1 all-pairs)."""
+    import paper_2604_24994_b200 as pf
+    sc, cams = case("mip360_1m")
+    rs = renderer(sc, flags=pf.PF_STATIC_SCENE | pf.PF_INFERENCE)
+    a = rs.forward(cams).cpu().numpy()
+    b = rs.forward(cams).cpu().numpy()          # second call: cached edge records
+    r0 = renderer(sc, flags=0)
+    c = r0.forward(cams).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    cam = cams[0]
+    rng = np.random.default_rng(7)
+    pix = np.stack([rng.integers(0, cam.width, 3000), rng.integers(0, cam.height, 3000)], 1)
+    ref = oracle.render(sc, cam, mode=oracle.O3, pixels=pix)["out"]
+    assert np.abs(a[0][pix[:, 1], pix[:, 0]] - ref).max() <= IMG_TOL
+    few = pix[:24]
+    ref1 = oracle.render(sc, cam, mode=oracle.O1, pixels=few)["out"]
+    assert np.abs(a[0][few[:, 1], few[:, 0]] - ref1).max() <= IMG_TOL
+    rs.close()
+    r0.close()
+
+
+def test_sweep64_3m_binning_and_sampled_pixels():
+    """sweep64_3m (3M cells, 64 views at 1080p) in the bench's launch configuration:
+    one 64-view call of the static inference handle (sorted in batches of 8 views).
+    Binning bit-exact on two views; views 0 and 63 against the oracle on 2000
+    sampled pixels each."""
+    import paper_2604_24994_b200 as pf
+    sc, cams = case("sweep64_3m")
+    assert len(cams) == 64 and sc.num_cells == 3_000_000
+    r = renderer(sc, flags=pf.PF_STATIC_SCENE | pf.PF_INFERENCE)
+    for cam in (cams[0], cams[63]):
+        g = r.debug_binning(cam)
+        o = oracle.binning(sc, cam)
+        assert g["P"] == o["P"]
+        assert np.array_equal(g["keys"].cpu().numpy().view(np.uint64), o["keys"])
+        assert np.array_equal(g["vals"].cpu().numpy().view(np.uint32), o["vals"])
+        assert np.array_equal(g["ranges"].cpu().numpy().view(np.uint32), o["ranges"])
+    out = r.forward(cams)
+    assert bool(torch.isfinite(out).all())
+    rng = np.random.default_rng(8)
+    for v in (0, 63):
+        cam = cams[v]
+        pix = np.stack([rng.integers(0, cam.width, 2000), rng.integers(0, cam.height, 2000)], 1)
+        got = out[v].cpu().numpy().astype(np.float64)[pix[:, 1], pix[:, 0]]
+        ref = oracle.render(sc, cam, mode=oracle.O3, pixels=pix)["out"]
+        assert np.abs(got - ref).max() <= IMG_TOL, v
+    # a view rendered alone equals its slot of the 64-view call, bit for bit
+    one = r.forward([cams[63]]).cpu().numpy()[0]
+    assert np.array_equal(one, out[63].cpu().numpy())
+    r.close()
+
+
+def test_train8_1m_full_frame_image_and_dense_gradients():
+    """One FULL 1080p frame of train8_1m (all 2,073,600 pixels) in the bench's launch
+    configuration (8 views in one call): image within 1e-4 of the oracle (O3) at every
+    pixel; dense dL/dimage on that view (zero on the others) and the C17 gradient bar,
+    every failing cell listed with its conditioning."""
+    sc, cams = case("train8_1m")
+    r = renderer(sc, flags=0)
+    out = r.forward(cams)
+    img = out[0].cpu().numpy().astype(np.float64)
+    ref = oracle.render(sc, cams[0], mode=oracle.O3)["out"]
+    err = np.abs(img - ref)
+    assert err.max() <= IMG_TOL, (err.max(), np.unravel_index(err.argmax(), err.shape))
+    H, W = cams[0].height, cams[0].width
+    g = np.zeros((len(cams), H, W, 4), np.float32)
+    g[0] = pf_synth.make_grad_out(1, H, W, seed=41)[0]
+    got = r.backward(cams, torch.from_numpy(g).cuda())
+    gref = oracle.backward(sc, cams[0], g[0], mode=oracle.O3)
+    print(grad_check(got, gref, ctx=(sc, [(cams[0], None)])))
+    r.close()
