@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--lists", default="cech", choices=["cech", "knn"],
                     help="neighbour lists: Čech-filtered (default) or unfiltered sym-16NN "
                          "(the paper's extraneous-edge comparison, P:236)")
+    ap.add_argument("--trace", action="store_true",
+                    help="render with the NEXT-4 adjacency-walk ray tracer (pf_trace_forward) "
+                         "instead of the tile rasterizer (forward only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -206,17 +209,18 @@ def load_peaks():
 def workload_tag(args):
     return (args.workload + ("+dipoles" if args.dipoles and not args.detail else "") +
             (f"+detail{args.detail}" if args.detail else "") +
-            ("+fisheye" if args.fisheye else "") +
+            ("+fisheye" if args.fisheye else "") + ("+trace" if args.trace else "") +
             ("+knn_lists" if args.lists == "knn" else ""))
 
 
-def is_train(workload):
-    return workload not in ("mip360_1m", "sweep64_3m")   # forward render-FPS workloads
+def is_train(args):
+    """fwd+bwd training step, or a forward render (render-FPS workloads, --trace)."""
+    return not args.trace and args.workload not in ("mip360_1m", "sweep64_3m")
 
 
 def make_config(args, sc, W, H, total_views, ws):
     """The JSON line's `config` -- built identically by both arms."""
-    train = is_train(args.workload)
+    train = is_train(args)
     return {"workload": workload_tag(args), "cells": sc.num_cells, "edges": sc.num_edges,
             "batch_views": total_views, "views_per_gpu": total_views / ws,
             "global_batch_views": total_views, "view_deal": "round-robin (rank r: r, r+N, ...)",
@@ -246,12 +250,15 @@ def run_reference(args):
     cams = orbit_cameras(wl, total)
     if args.fisheye:
         cams = [pf_synth.fisheye(c, 200.0) for c in cams]
-    train = is_train(wl)
+    train = is_train(args)
     H, W = cams[0].height, cams[0].width
     g = pf_synth.make_grad_out(1, H, W, seed=12)[0] if train else None
 
     def one_view(k):
         cam = cams[k % len(cams)]
+        if args.trace:
+            oracle.trace(sc, cam)
+            return
         oracle.render(sc, cam, mode=oracle.O3)
         if train:
             oracle.backward(sc, cam, g, mode=oracle.O3)
@@ -268,7 +275,8 @@ def run_reference(args):
     val = 1.0 / dt
     cores = oracle.num_threads()
     sample = (f"each step = one whole {W}x{H} view of the {total}-view batch (views cycled), "
-              f"oracle O3 {'forward+backward' if train else 'forward'} in double on "
+              f"oracle {'tracer' if args.trace else 'O3'} "
+              f"{'forward+backward' if train else 'forward'} in double on "
               f"{cores} host threads: {dt:.2f} s per view")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt,
@@ -282,7 +290,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(sc, cam, seconds, train=True, calib=None):
+def cpu_baseline(sc, cam, seconds, train=True, calib=None, trace=False):
     """Times the oracle (O3 tile-list mode, double, OpenMP over all host cores) on
     a bounded sample of pixel rows of one view and extrapolates to frames/s.
     Each oracle call rebuilds its own fp32 binning (a fixed per-frame cost A), so
@@ -298,6 +306,9 @@ def cpu_baseline(sc, cam, seconds, train=True, calib=None):
         y = y[y < H]
         pix = np.stack(np.meshgrid(np.arange(W), y), -1).reshape(-1, 2)
         t0 = time.perf_counter()
+        if trace:
+            oracle.trace(sc, cam, pixels=pix)
+            return time.perf_counter() - t0, pix.shape[0]
         oracle.render(sc, cam, mode=oracle.O3, pixels=pix)
         if train:
             oracle.backward(sc, cam, g[pix[:, 1], pix[:, 0]], mode=oracle.O3, pixels=pix)
@@ -316,7 +327,8 @@ def cpu_baseline(sc, cam, seconds, train=True, calib=None):
     B2 = max((t - A) / n, 1e-12)
     frame = A + B2 * W * H
     return {"value": 1.0 / frame, "calib": {"A": A, "B": B2}, "cores": oracle.num_threads(),
-            "sample": f"{n} pixels ({rows} rows) of one {W}x{H} view, oracle O3 "
+            "sample": f"{n} pixels ({rows} rows) of one {W}x{H} view, oracle "
+                      f"{'tracer' if trace else 'O3'} "
                       f"{'forward+backward' if train else 'forward'} in {t:.1f}s; "
                       f"per-frame fixed cost (own fp32 binning) {A:.2f}s + {B2 * 1e6:.2f}us/pixel "
                       f"-> {frame:.1f}s per frame"}
@@ -413,7 +425,7 @@ def main():
     nv = len(cams)
     t_gen = time.perf_counter() - t_gen
     H, W = cams[0].height, cams[0].width
-    train = is_train(wl)
+    train = is_train(args)
     # render-FPS workloads draw a fixed scene: its edge records (K0) are built once at
     # creation (PF_STATIC_SCENE); training workloads rebuild them every step
     r = pf.Renderer.from_scene(sc, dev, flags=0 if train else pf.PF_INFERENCE | pf.PF_STATIC_SCENE)
@@ -429,11 +441,14 @@ def main():
 
     from paper_2604_24994_b200 import dist as pfd
 
+    def render(rr, o):
+        return rr.trace(cams, out=o) if args.trace else rr.forward(cams, out=o)
+
     def step():
         if train:
             pfd.train_step(r, cams, grad_out, flat, out=out)   # fwd, bwd, NCCL all-reduce
         else:
-            r.forward(cams, out=out)
+            render(r, out)
 
     def barrier():
         if ws > 1:
@@ -466,12 +481,12 @@ def main():
 
     # ---------------- forward-only throughput (extra) ------------------------
     for _ in range(2):
-        r_inf.forward(cams, out=out)
+        render(r_inf, out)
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
-        r_inf.forward(cams, out=out)
+        render(r_inf, out)
     f1.record(stream)
     barrier()
     fwd_fps, _, fwd_ms = aggregate_fps(nv, f0.elapsed_time(f1) / args.steps, red_sum, red_max)
@@ -558,7 +573,7 @@ def main():
                     ev["d2h"][b].record(d2h)
             else:       # forward-only: the rendered images go back to the host
                 stream.wait_event(ev["d2h"][b])
-                r.forward(cams, out=outs[b])
+                render(r, outs[b])
                 ev["used"][b].record(stream)
                 with torch.cuda.stream(d2h):
                     d2h.wait_event(ev["used"][b])
@@ -584,6 +599,27 @@ def main():
                         "forward) + fwd + bwd (+ all-reduce) + D2H of the per-cell gradients "
                         "(overlapping the next forward), every step") if train
                else "fwd through the C-ABI (host cameras) + D2H of the rendered images, every step"}
+
+    trace = None
+    if args.trace:
+        # NEXT-4: one tracer launch per view, latency-bound pointer chasing; the
+        # algorithmic bytes of a walk step are the cell's records (A, B, E: 40 B) and
+        # its edge records (16 B x degree) plus the next cell's CSR index (4 B)
+        _, tst = r.trace(cams[:1], stats=True)
+        deg_mean = sc.num_edges / max(sc.num_cells, 1)
+        b_launch = tst["visited"] * (44 + 16 * deg_mean) + 16 * W * H
+        t_launch = fwd_ms / nv / 1e3
+        peaks_t, _ = load_peaks()
+        hbm_t = float(peaks_t.get("hbm_gbs", 6650.0))
+        trace = {"stats_view0": tst, "cells_per_ray": tst["visited"] / max(tst["rays"], 1),
+                 "locates_per_ray": tst["located"] / max(tst["rays"], 1),
+                 "segments_per_ray": tst["segments"] / max(tst["rays"], 1),
+                 "roofline": {"bound": "hbm", "kernel": "k9_trace",
+                              "achieved": b_launch / t_launch / 1e9, "peak": hbm_t,
+                              "unit": "GB/s", "frac": b_launch / t_launch / 1e9 / hbm_t,
+                              "algorithmic_bytes_per_launch": b_launch,
+                              "note": "walk-step records (cellA/B/E + edges + CSR index) "
+                                      "per launch / launch time (step time / views)"}}
 
     # ---------------- counters -> algorithmic flops, roofline ----------------
     cnt = np.zeros(4)
@@ -683,7 +719,7 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(sc, cams[0], args.cpu_seconds, train=train)
+            cpu = cpu_baseline(sc, cams[0], args.cpu_seconds, train=train, trace=args.trace)
             cpu = {"value": cpu["value"], "unit": UNIT, "cores": cpu["cores"], "kind": "oracle",
                    "sample": cpu["sample"]}
         except Exception as ex:  # noqa
@@ -700,7 +736,7 @@ def main():
             "config": make_config(args, sc, W, H, total, ws),
             "views_this_rank": nv, "allreduce": allreduce, "weak_scaling": weak,
             "clocks": clocks, "gpu_launches": int(launches),
-            "e2e": e2e, "roofline": roofline, "roofline_step": roofline_step, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": trace["roofline"] if trace else roofline, "roofline_step": roofline_step, "cpu_baseline": cpu,
             "fwd_fps": fwd_fps, "fwdbwd_fps": fps if train else None,
             "mpix_s": fps * W * H / 1e6, "fwd_mpix_s": fwd_fps * W * H / 1e6,
             "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
@@ -711,6 +747,7 @@ def main():
                      "passes": passes, "bytes_per_launch": sort_bytes, "achieved_gbs": sort_gbs,
                      "hbm_frac": (sort_gbs / hbm) if sort_gbs else None},
             "peaks_source": peaks_kind, "scene_gen_s": t_gen, "cech_graph": cech,
+            "trace": trace,
         }
         print(json.dumps(line), flush=True)
     r.close()

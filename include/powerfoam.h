@@ -191,6 +191,26 @@ typedef struct {
 PF_API int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t num_views,
                                  const float *grad_out, const pf_grads *grads, pf_stream_t stream);
 
+/*
+ * NEXT-4: the adjacency-walk ray tracer ("walk from one cell to the
+ * next by checking all faces", "the cell-to-cell traversal strategy ...
+ * still applies ... in addition to considering the sphere bounds", P:687-689;
+ * reading R7 of DESIGN.md).  Renders num_views >= 1 views (same width x height)
+ * into out (device f32[V,H,W,4], the layout of pf_render_forward) by walking
+ * every pixel ray from cell to cell: inside the union of balls the exit plane
+ * names the next cell (the Čech list), at a sphere exit the walk jumps the gap
+ * to the next ball on a BVH of the balls (built per call; once with
+ * PF_STATIC_SCENE).  The image equals pf_render_forward's up to fp32 rounding
+ * (the paper's "same" renderers, Fig. 1) for scenes with w = r^2 (P:184-189:
+ * the weight IS the squared radius); no backward state is saved.
+ * stats: host int64[5] or NULL (then no sync): rays traced, cells visited,
+ * locate (BVH) calls, composited segments, walks stopped by the step budget.
+ * Errors: PF_ERR_INVALID_ARGUMENT (NULL / bad camera), PF_ERR_CUDA,
+ * PF_ERR_OUT_OF_MEMORY.
+ */
+PF_API int pf_trace_forward(pf_scene *s, const pf_camera *cams, int32_t num_views, float *out,
+                            int64_t *stats, pf_stream_t stream);
+
 /* Frees everything the handle owns (not the caller's arrays).  NULL is a no-op. */
 PF_API int pf_destroy(pf_scene *s);
 

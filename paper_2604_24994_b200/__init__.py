@@ -28,7 +28,7 @@ _STATUS = {0: "PF_OK", 1: "PF_ERR_INVALID_ARGUMENT", 2: "PF_ERR_CUDA",
            3: "PF_ERR_OUT_OF_MEMORY", 4: "PF_ERR_STATE"}
 
 EXPORTS = ["pf_create_scene", "pf_render_forward", "pf_render_forward_ex", "pf_render_backward",
-           "pf_render_backward_ex", "pf_destroy",
+           "pf_render_backward_ex", "pf_trace_forward", "pf_destroy",
            "pf_last_error", "pf_debug_binning", "pf_debug_counters", "pf_launch_count",
            "pf_set_profiling", "pf_stage_times", "pf_last_pair_counts",
            "pf_cech_create", "pf_cech_destroy", "pf_cech_last_error", "pf_cech_build",
@@ -92,6 +92,7 @@ def load_library(build_if_missing: bool = True):
     L.pf_render_forward_ex.argtypes = [P, C.POINTER(_Camera), i32, P, P, P]
     L.pf_render_backward.argtypes = [P, C.POINTER(_Camera), i32, P, P, P, P, P, P, P]
     L.pf_render_backward_ex.argtypes = [P, C.POINTER(_Camera), i32, P, C.POINTER(_Grads), P]
+    L.pf_trace_forward.argtypes = [P, C.POINTER(_Camera), i32, P, P, P]
     L.pf_destroy.argtypes = [P]
     L.pf_last_error.restype = C.c_char_p
     L.pf_debug_binning.argtypes = [P, C.POINTER(_Camera), P, P, P, P, P, P, C.POINTER(i64), P]
@@ -298,6 +299,23 @@ class Renderer:
         _check(self._L.pf_render_forward_ex(self._h, arr, V, C.c_void_p(out.data_ptr()),
                                             ex, _stream(stream)))
         return out
+
+    def trace(self, cams, out=None, stream=None, stats=False):
+        """NEXT-4: renders the views with the adjacency-walk ray tracer into out
+        f32[V,H,W,4] (pf_trace_forward).  stats=True also returns a dict (rays,
+        visited, located, segments, diverged) -- one stream sync."""
+        arr, V = _cams(cams)
+        H, W = arr[0].height, arr[0].width
+        if out is None:
+            out = torch.empty((V, H, W, 4), device=self.device, dtype=torch.float32)
+        _dev_f32(out, (V, H, W, 4), self.device, "out")
+        st = (C.c_int64 * 5)() if stats else None
+        _check(self._L.pf_trace_forward(self._h, arr, V, C.c_void_p(out.data_ptr()), st,
+                                        _stream(stream)))
+        if not stats:
+            return out
+        keys = ("rays", "visited", "located", "segments", "diverged")
+        return out, {k: int(st[i]) for i, k in enumerate(keys)}
 
     def backward(self, cams, grad_out, grads=None, stream=None):
         """Accumulates dL/dparams into `grads` (dict or flat f32[grad_size] tensor;

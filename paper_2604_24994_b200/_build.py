@@ -10,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libpowerfoam.so")
-SOURCES = ["pf_api.cu", "pf_prep.cu", "pf_sort.cu", "pf_raster.cu", "pf_cech.cu"]
-HEADERS = ["pf_internal.cuh", os.path.join("..", "..", "include", "powerfoam.h")]
+SOURCES = ["pf_api.cu", "pf_prep.cu", "pf_sort.cu", "pf_raster.cu", "pf_cech.cu", "pf_trace.cu"]
+HEADERS = ["pf_internal.cuh", "pf_pixel.cuh", "pf_bvh.cuh", os.path.join("..", "..", "include", "powerfoam.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

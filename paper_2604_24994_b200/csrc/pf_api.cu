@@ -8,6 +8,7 @@
 #include <new>
 #include <string>
 
+#include "pf_bvh.cuh"
 #include "pf_internal.cuh"
 
 namespace {
@@ -403,6 +404,12 @@ int pf_destroy(pf_scene *s)
     if (!s) return PF_OK;
     DeviceGuard g(s->device);
     cudaDeviceSynchronize();
+    if (s->bvh) {
+        s->bvh->release();
+        delete s->bvh;
+        s->bvh = nullptr;
+    }
+    s->trace_stats.release();
     s->cellA.release();
     s->cellB.release();
     s->cellE.release();
@@ -598,6 +605,49 @@ int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const f
     if (brc != PF_OK) return brc;
     PF_CUDA(pf::launch_unpack(s, g->sites, g->weights, g->radii, g->density, g->rgb,
                               s->ds.cellN ? g->normals : nullptr, st));
+    return PF_OK;
+}
+
+int pf_trace_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out, int64_t *stats,
+                     pf_stream_t stream)
+{
+    if (!s) return fail(PF_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    if (!cams || V < 1) return fail(PF_ERR_INVALID_ARGUMENT, "need >= 1 camera");
+    if (!out) return fail(PF_ERR_INVALID_ARGUMENT, "out is NULL");
+    for (int v = 0; v < V; ++v) {
+        int rc = check_camera(cams[v]);
+        if (rc) return rc;
+        if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+            return fail(PF_ERR_INVALID_ARGUMENT, "all views of one call must share width/height");
+    }
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool stat = (s->flags & PF_STATIC_SCENE) != 0;
+    if (!stat || !s->edges_built) {
+        PF_CUDA(pf::launch_edge_records(s, st));
+        s->edges_built = true;
+    }
+    if (!s->bvh) {
+        s->bvh = new (std::nothrow) pf::BallBVH();
+        if (!s->bvh) return fail(PF_ERR_OUT_OF_MEMORY, "host allocation failed");
+    }
+    if (!stat || !s->bvh_built) {
+        PF_CUDA(pf::build_ball_bvh(s, *s->bvh, s->ds.N, s->ds.sites, s->ds.radii, st));
+        s->bvh_built = true;
+    }
+    PF_CUDA(s->trace_stats.reserve(8 * 8));
+    unsigned long long *dst = s->trace_stats.as<unsigned long long>();
+    if (stats) PF_CUDA(cudaMemsetAsync(dst, 0, 8 * 5, st));
+    const size_t npix = (size_t)cams[0].width * cams[0].height;
+    for (int v = 0; v < V; ++v)
+        PF_CUDA(pf::launch_trace(s, *s->bvh, cam_params(cams[v]), out + 4 * npix * (size_t)v,
+                                 stats ? dst : nullptr, st));
+    if (stats) {
+        unsigned long long h[5];
+        PF_CUDA(cudaMemcpyAsync(h, dst, sizeof(h), cudaMemcpyDeviceToHost, st));
+        PF_CUDA(cudaStreamSynchronize(st));
+        for (int k = 0; k < 5; ++k) stats[k] = (int64_t)h[k];
+    }
     return PF_OK;
 }
 

@@ -16,6 +16,7 @@
 
 #include <string>
 
+#include "pf_bvh.cuh"
 #include "pf_internal.cuh"
 
 namespace pf {
@@ -129,10 +130,6 @@ __global__ void c2_radix_tree(const unsigned long long *__restrict__ codes, int6
     if (rleaf) parent_leaf[gamma + 1] = (uint32_t)i;
     else parent_int[gamma + 1] = (uint32_t)i;
 }
-
-struct Box {
-    float lo[3], hi[3];
-};
 
 __device__ __forceinline__ Box sphere_box(const float *__restrict__ sites,
                                           const float *__restrict__ radii, uint32_t i)
@@ -320,10 +317,60 @@ __global__ void c7_connect(const float *__restrict__ sites, const float *__restr
 }  // namespace
 }  // namespace pf
 
+namespace pf {
+
+cudaError_t build_ball_bvh(pf_scene *scratch, BallBVH &B, int64_t N, const float *sites,
+                           const float *radii, cudaStream_t st)
+{
+    const size_t n = (size_t)N;
+    cudaError_t e;
+#define PF_BV(x)                    \
+    if ((e = (x)) != cudaSuccess)   \
+        return e;
+    PF_BV(B.keys.reserve(8 * n));
+    PF_BV(B.keys_alt.reserve(8 * n));
+    PF_BV(B.vals.reserve(4 * n));
+    PF_BV(B.vals_alt.reserve(4 * n));
+    PF_BV(B.bb.reserve(64));
+    PF_BV(B.left.reserve(4 * n));
+    PF_BV(B.right.reserve(4 * n));
+    PF_BV(B.pint.reserve(4 * n));
+    PF_BV(B.pleaf.reserve(4 * n));
+    PF_BV(B.bint.reserve(sizeof(Box) * n));
+    PF_BV(B.bleaf.reserve(sizeof(Box) * n));
+    PF_BV(B.arrive.reserve(4 * n));
+    // bounds (init min = +inf bits, max = -inf bits)
+    static const float init[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    PF_BV(cudaMemcpyAsync(B.bb.ptr, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    c0_bounds<<<min(ceil_div(N, 256), 1184), 256, 0, st>>>(sites, N, B.bb.as<float>());
+    c1_morton<<<ceil_div(N, 256), 256, 0, st>>>(sites, N, B.bb.as<float>(),
+                                                 B.keys.as<unsigned long long>(), B.vals.as<uint32_t>());
+    bool alt = false;
+    PF_BV(radix_sort_pairs(scratch, B.keys.as<uint64_t>(), B.vals.as<uint32_t>(),
+                           B.keys_alt.as<uint64_t>(), B.vals_alt.as<uint32_t>(), N, 30, &alt, st));
+    const unsigned long long *codes = (alt ? B.keys_alt : B.keys).as<unsigned long long>();
+    B.order = (alt ? B.vals_alt : B.vals).as<uint32_t>();
+    B.n = N;
+    if (N > 1)
+        c2_radix_tree<<<ceil_div(N - 1, 256), 256, 0, st>>>(codes, N, B.left.as<uint32_t>(),
+                                                             B.right.as<uint32_t>(), B.pint.as<uint32_t>(),
+                                                             B.pleaf.as<uint32_t>());
+    PF_BV(cudaMemsetAsync(B.arrive.ptr, 0, 4 * n, st));
+    c3_refit<<<ceil_div(N, 256), 256, 0, st>>>(sites, radii, B.order, N, B.left.as<uint32_t>(),
+                                                B.right.as<uint32_t>(), B.pint.as<uint32_t>(),
+                                                B.pleaf.as<uint32_t>(), B.bint.as<Box>(),
+                                                B.bleaf.as<Box>(), B.arrive.as<int>());
+    scratch->launches += 4;
+#undef PF_BV
+    return cudaGetLastError();
+}
+
+}  // namespace pf
+
 struct pf_cech {
     pf_scene scratch;   // sort / scan workspaces and launch counter (reused machinery)
-    pf::DevBuf keys, keys_alt, vals, vals_alt, bb, left, right, pint, pleaf, bint, bleaf,
-        arrive, counts, offs32, flag;
+    pf::BallBVH bvh;
+    pf::DevBuf counts, offs32, flag;
 };
 
 namespace {
@@ -359,9 +406,8 @@ int pf_cech_destroy(pf_cech *h)
 {
     if (!h) return PF_OK;
     cudaDeviceSynchronize();
-    pf::DevBuf *bufs[] = {&h->keys, &h->keys_alt, &h->vals, &h->vals_alt, &h->bb, &h->left,
-                          &h->right, &h->pint, &h->pleaf, &h->bint, &h->bleaf, &h->arrive,
-                          &h->counts, &h->offs32, &h->flag, &h->scratch.sort_hist,
+    h->bvh.release();
+    pf::DevBuf *bufs[] = {&h->counts, &h->offs32, &h->flag, &h->scratch.sort_hist,
                           &h->scratch.scan_tmp};
     for (auto *b : bufs) b->release();
     delete h;
@@ -378,45 +424,15 @@ int pf_cech_build(pf_cech *h, int64_t N, const float *sites, const float *radii,
     if (N < 1 || N >= ((int64_t)1 << 30)) return cfail(PF_ERR_INVALID_ARGUMENT, "N must be in [1, 2^30)");
     cudaStream_t st = (cudaStream_t)stream;
     const size_t n = (size_t)N;
-    PF_CC(h->keys.reserve(8 * n));
-    PF_CC(h->keys_alt.reserve(8 * n));
-    PF_CC(h->vals.reserve(4 * n));
-    PF_CC(h->vals_alt.reserve(4 * n));
-    PF_CC(h->bb.reserve(64));
-    PF_CC(h->left.reserve(4 * n));
-    PF_CC(h->right.reserve(4 * n));
-    PF_CC(h->pint.reserve(4 * n));
-    PF_CC(h->pleaf.reserve(4 * n));
-    PF_CC(h->bint.reserve(sizeof(Box) * n));
-    PF_CC(h->bleaf.reserve(sizeof(Box) * n));
-    PF_CC(h->arrive.reserve(4 * n));
     PF_CC(h->counts.reserve(4 * n));
     PF_CC(h->offs32.reserve(4 * n + 16));
     PF_CC(h->flag.reserve(16));
-    // bounds (init min = +inf bits, max = -inf bits)
-    const float init[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    PF_CC(cudaMemcpyAsync(h->bb.ptr, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    c0_bounds<<<min(ceil_div(N, 256), 1184), 256, 0, st>>>(sites, N, h->bb.as<float>());
-    c1_morton<<<ceil_div(N, 256), 256, 0, st>>>(sites, N, h->bb.as<float>(),
-                                                 h->keys.as<unsigned long long>(), h->vals.as<uint32_t>());
-    bool alt = false;
-    PF_CC(radix_sort_pairs(&h->scratch, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
-                           h->keys_alt.as<uint64_t>(), h->vals_alt.as<uint32_t>(), N, 30, &alt, st));
-    const unsigned long long *codes = (alt ? h->keys_alt : h->keys).as<unsigned long long>();
-    const uint32_t *order = (alt ? h->vals_alt : h->vals).as<uint32_t>();
-    if (N > 1)
-        c2_radix_tree<<<ceil_div(N - 1, 256), 256, 0, st>>>(codes, N, h->left.as<uint32_t>(),
-                                                             h->right.as<uint32_t>(), h->pint.as<uint32_t>(),
-                                                             h->pleaf.as<uint32_t>());
-    PF_CC(cudaMemsetAsync(h->arrive.ptr, 0, 4 * n, st));
+    PF_CC(build_ball_bvh(&h->scratch, h->bvh, N, sites, radii, st));
+    const uint32_t *order = h->bvh.order;
     PF_CC(cudaMemsetAsync(h->flag.ptr, 0, 4, st));
-    c3_refit<<<ceil_div(N, 256), 256, 0, st>>>(sites, radii, order, N, h->left.as<uint32_t>(),
-                                                h->right.as<uint32_t>(), h->pint.as<uint32_t>(),
-                                                h->pleaf.as<uint32_t>(), h->bint.as<Box>(),
-                                                h->bleaf.as<Box>(), h->arrive.as<int>());
     c4_query<false><<<ceil_div(N, 128), 128, 0, st>>>(
-        sites, radii, order, N, h->left.as<uint32_t>(), h->right.as<uint32_t>(), h->bint.as<Box>(),
-        h->bleaf.as<Box>(), h->counts.as<int>(), nullptr, nullptr, h->flag.as<int>());
+        sites, radii, order, N, h->bvh.left.as<uint32_t>(), h->bvh.right.as<uint32_t>(), h->bvh.bint.as<Box>(),
+        h->bvh.bleaf.as<Box>(), h->counts.as<int>(), nullptr, nullptr, h->flag.as<int>());
     long long *d_tot = reinterpret_cast<long long *>(h->offs32.as<uint32_t>() + ((n + 3) & ~3ull));
     PF_CC(exclusive_scan_counts(&h->scratch, h->counts.as<int>(), N, h->offs32.as<uint32_t>(), d_tot, st));
     c5_offsets<<<ceil_div(N, 256), 256, 0, st>>>(h->offs32.as<uint32_t>(), h->counts.as<int>(), N,
@@ -429,11 +445,11 @@ int pf_cech_build(pf_cech *h, int64_t N, const float *sites, const float *radii,
     if (ovf) return cfail(PF_ERR_CUDA, "BVH traversal stack overflow");
     if (E >= ((long long)1 << 32)) return cfail(PF_ERR_OUT_OF_MEMORY, "edge count exceeds 2^32");
     *num_edges = E;
-    h->scratch.launches += 7;
+    h->scratch.launches += 3;
     if (!nbr_indices || capacity < E) return PF_OK;   // caller sizes the index array
     c4_query<true><<<ceil_div(N, 128), 128, 0, st>>>(
-        sites, radii, order, N, h->left.as<uint32_t>(), h->right.as<uint32_t>(), h->bint.as<Box>(),
-        h->bleaf.as<Box>(), nullptr, nbr_offsets, nbr_indices, h->flag.as<int>());
+        sites, radii, order, N, h->bvh.left.as<uint32_t>(), h->bvh.right.as<uint32_t>(), h->bvh.bint.as<Box>(),
+        h->bvh.bleaf.as<Box>(), nullptr, nbr_offsets, nbr_indices, h->flag.as<int>());
     c6_sort_rows<<<ceil_div(N, 256), 256, 0, st>>>(nbr_offsets, N, nbr_indices);
     h->scratch.launches += 2;
     PF_CC(cudaGetLastError());

@@ -81,6 +81,8 @@ struct ViewState {
     DevBuf saved;                            // float4[H*W] final (C + T bg, T)
 };
 
+struct BallBVH;   // pf_bvh.cuh
+
 struct StageEvent {
     int stage;
     cudaEvent_t a, b;
@@ -117,6 +119,10 @@ struct pf_scene {
     cudaEvent_t side_fork = nullptr, side_join = nullptr;
     std::vector<pf::StageEvent> events;
     std::vector<cudaEvent_t> event_pool;
+    // NEXT-4 tracer: the ball BVH (built per call; once for PF_STATIC_SCENE) and stats
+    pf::BallBVH *bvh = nullptr;
+    bool bvh_built = false;
+    pf::DevBuf trace_stats;
 };
 
 namespace pf {
@@ -139,6 +145,8 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
                            uint32_t *rec_used, float *st_contrib, float *st_normal,
                            cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
+cudaError_t launch_trace(pf_scene *s, const BallBVH &bvh, const CamParams &cam, float *out,
+                         unsigned long long *stats, cudaStream_t st);
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
                           float *gn, cudaStream_t st);
 
