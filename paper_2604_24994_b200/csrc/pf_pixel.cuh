@@ -304,7 +304,8 @@ __device__ __forceinline__ int cull_planes(const WarpStage &S, int j, const Warp
     if (__any_sync(0xffffffffu, kill)) return -1;
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     const int n = __popc(m);
-    if (keep) {
+    __syncwarp();   // every lane's reads of the previous cell's kept planes happen before
+    if (keep) {     // this cell's planes overwrite them (racecheck: WAR across lanes)
         const int p = __popc(m & ((1u << lane) - 1u));
         B.E[p] = E;
         B.q[p] = (uint8_t)lane;

@@ -27,6 +27,8 @@ def run(sc, cams, tag):
     ri = r.sibling(pf.PF_INFERENCE | pf.PF_STATIC_SCENE)
     ri.forward(cams)
     ri.forward(cams)
+    img, st = ri.trace(cams, stats=True)     # NEXT-4 tracer (static scene: cached BVH)
+    ri.trace(cams)
     torch.cuda.synchronize()
     print(tag, "ok", float(out.sum()), float(grads["sites"].abs().sum()), flush=True)
     ri.close()
@@ -54,6 +56,9 @@ def main():
         torch.cuda.synchronize()
         print(name, "cech ok", int(idx.numel()), float(loss.sum()), flush=True)
         cb.close()
+    # release PyTorch's cached blocks so the leak check sees only the library's memory
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
