@@ -52,7 +52,7 @@ def test_trace_equals_oracle_and_raster(name, fish):
         vis += int(o["stats"][..., 0].sum())
     assert st["diverged"] == 0
     npx = sum(c.width * c.height for c in cams)
-    assert (st["rays"] == npx) if not fish else (0 < st["rays"] < npx)
+    assert (st["rays"] == npx) if not fish else (0 < st["rays"] <= npx)
     # the walk visits the cells the oracle's walk visits (fp32 slivers aside)
     assert abs(st["visited"] - vis) <= 0.01 * vis + 8
     r.close()
