@@ -659,24 +659,32 @@ def main():
             "ncu_issue_pct": prof.get("issue_pct_of_peak"),
             "note": "instruction count of one launch from the committed ncu capture "
                     "(same kernel, same workload); the FP32 fraction is below this because "
-                    "the path is not FMA-shaped (a plane test is ~17 instructions for 16 "
-                    "flops) and the per-(warp, cell) lockstep work serves ~3.4 hit pixels "
-                    "of 32 on average (DESIGN 9); the algorithmic flops count every list "
-                    "plane, the warp plane cull executes ~1 per hit cell"}
+                    "the path is not FMA-shaped (a plane clip is ~17 SASS instructions for "
+                    "16 algorithmic flops) and the per-(warp, cell) lockstep work (sphere "
+                    "test, warp plane cull, compositing, K6->K7 record) is overhead; the "
+                    "algorithmic flops count every list plane (~11 per hit), the warp plane "
+                    "cull leaves ~5.8 per (warp, hit cell) (profiles/r02_k6_experiments.md)"}
     sort_ms, sort_n = stages["K4_sort"]
     pairs = r.pair_counts(nv)
     P = float(np.mean(pairs))
-    # one radix sort per call over all views' pairs: key bits = 32 + tile + view bits;
-    # algorithmic bytes per pass = 8 (histogram key read) + 12 read + 12 write per pair
-    vbits = math.ceil(math.log2(nv)) if nv > 1 else 0
-    passes = math.ceil((32 + math.ceil(math.log2((W + 15) // 16 * ((H + 15) // 16))) + vbits) / 8)
-    sort_bytes = 32.0 * P * nv * passes
-    sort_gbs = sort_bytes / (sort_ms / max(sort_n, 1) / 1e3) / 1e9 if sort_ms > 0 else None
+    bcount = r.debug_binning(cams[0])["count"]
+    n_vis = float((bcount > 0).sum().item())
+    # depth-first binning (DESIGN 6, K4): per sort batch of <= 8 views, the visible
+    # cells are radix-sorted by (view, depth key) over 32 + view bits, then the pairs by
+    # (view, tile) over tile + view bits with 32-bit keys; algorithmic bytes per item
+    # and pass: cells 8 (histogram key read) + 12 read + 12 write, pairs 4 + 8 + 8
+    vbits = math.ceil(math.log2(min(nv, 8))) if nv > 1 else 0
+    tbits = math.ceil(math.log2((W + 15) // 16 * ((H + 15) // 16)))
+    passes_cells = math.ceil((32 + vbits) / 8)
+    passes_pairs = math.ceil((tbits + vbits) / 8)
+    sort_bytes = 32.0 * n_vis * nv * passes_cells + 20.0 * P * nv * passes_pairs
+    sort_ms_step = sort_ms / args.steps
+    sort_gbs = sort_bytes / (sort_ms_step / 1e3) / 1e9 if sort_ms > 0 else None
+    # the 48-bit pair sort this replaces: 6 passes over every pair
+    legacy_bytes = 32.0 * P * nv * math.ceil((32 + tbits + vbits) / 8)
     hbm = float(peaks.get("hbm_gbs", 6650.0))
 
     # ---------------- whole-step rooflines (SURVEY §8(d) byte and flop models) -------
-    bcount = r.debug_binning(cams[0])["count"]
-    n_vis = float((bcount > 0).sum().item())
     deg_mean = sc.num_edges / max(N, 1)
     T_tiles = ((W + 15) // 16) * ((H + 15) // 16)
     pix = W * H
@@ -743,9 +751,16 @@ def main():
             "stage_launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
             "pairs_per_view": P, "counters_per_view": {"X_s": cnt[0], "X_h": cnt[1],
                                                        "X_p": cnt[2], "X_c": cnt[3]},
-            "sort": {"ms_per_launch": sort_ms / max(sort_n, 1), "pairs_per_launch": P * nv,
-                     "passes": passes, "bytes_per_launch": sort_bytes, "achieved_gbs": sort_gbs,
-                     "hbm_frac": (sort_gbs / hbm) if sort_gbs else None},
+            "sort": {"ms_per_step": sort_ms_step, "launches_per_step": sort_n / args.steps,
+                     "pairs_per_step": P * nv, "visible_cells_per_step": n_vis * nv,
+                     "passes_cells": passes_cells, "passes_pairs": passes_pairs,
+                     "bytes_per_step": sort_bytes, "achieved_gbs": sort_gbs,
+                     "hbm_frac": (sort_gbs / hbm) if sort_gbs else None,
+                     "legacy_pair_sort_bytes": legacy_bytes,
+                     "legacy_equivalent_gbs": legacy_bytes / (sort_ms_step / 1e3) / 1e9
+                     if sort_ms > 0 else None,
+                     "model": "depth-first binning: visible cells sorted by (view, depth), "
+                              "pairs by (view, tile); legacy = one 48-bit sort of all pairs"},
             "peaks_source": peaks_kind, "scene_gen_s": t_gen, "cech_graph": cech,
             "trace": trace,
         }

@@ -99,29 +99,48 @@ int reserve_view_bins(pf_scene *s, pf::ViewState &v)
     PF_CUDA(v.rect.reserve(16 * N));
     PF_CUDA(v.count.reserve(4 * N));
     PF_CUDA(v.keybits.reserve(4 * N));
-    PF_CUDA(v.offsets.reserve(4 * N));
     if (v.cam.model == PF_FISHEYE)
         PF_CUDA(v.tdir.reserve(sizeof(double) * (3 * (size_t)v.cam.tiles_x * v.cam.tiles_y + 2)));
     return PF_OK;
 }
 
-// K3..K5 for views [0, V) of this call (K1/K2 ran, every v.P is known): the pairs
-// of all views are emitted into one array with the view id above the tile bits,
-// sorted once, and split into per-view tile ranges.  Leaves the sorted keys in
-// *keys_out (scratch) and the sorted cell ids in s->vals_all.
-int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
-                     uint64_t **keys_out)
+// The views of one sort batch as a kernel parameter.
+pf::BatchViews batch_views(pf::ViewState *views, int b0, int b1)
 {
-    // Views are sorted in batches of up to kSortViews: the view id takes the bits
-    // above the tile id, and more than 8 views would add a radix pass for every
-    // pair (51 bits = 7 passes for 64 views at 1080p instead of 48 = 6).
-    constexpr int kSortViews = 8;
+    pf::BatchViews bv;
+    memset(&bv, 0, sizeof(bv));
+    bv.n = b1 - b0;
+    bv.first = b0;
+    for (int v = b0; v < b1; ++v) {
+        bv.count[v - b0] = views[v].count.as<int>();
+        bv.keybits[v - b0] = views[v].keybits.as<uint32_t>();
+        bv.rect[v - b0] = views[v].rect.as<int4>();
+        bv.tdir[v - b0] = views[v].tdir.as<double>();
+        bv.cam[v - b0] = views[v].cam;
+    }
+    return bv;
+}
+
+// Sorting and ranges for views [0, V) of this call (K1 and the visible-cell
+// counts ran, every v.P is known), in batches of up to kBatchViews views:
+//   K2: compact the visible cells of the batch (view-major, cell order);
+//   K4a: radix-sort them by (view, depth key) -- 32 + view bits, ~N_vis items;
+//   K3: emit their tile pairs in that order, key = view << tile_bits | tile;
+//   K4b: stable radix sort of the pairs by (view, tile) (tile_bits + view bits);
+//   K5: per-tile ranges, LPT tile order.
+// Inside a tile the pairs are then ordered by (depth key, cell): the order of the
+// stable (tile << 32 | key) sort of cell-major pairs.  Leaves the
+// sorted (view, tile) keys in *keys_out (scratch) and the cell ids in s->vals_all.
+int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
+                     uint32_t **keys_out)
+{
+    constexpr int kSortViews = pf::kBatchViews;
     const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     const int tb = tile_bits(T);
     const int Vb = V < kSortViews ? V : kSortViews;
     int vb = 0;
     while ((1 << vb) < Vb) ++vb;
-    if (32 + tb + vb > 64) return fail(PF_ERR_INVALID_ARGUMENT, "too many tiles for 64-bit keys");
+    if (tb + vb > 32) return fail(PF_ERR_INVALID_ARGUMENT, "too many tiles for the sort keys");
     int64_t Ptot = 0;
     for (int v = 0; v < V; ++v) {
         views[v].pair_off = Ptot;
@@ -130,31 +149,50 @@ int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
     if (Ptot >= (int64_t)0xFFFFFFFFll)
         return fail(PF_ERR_OUT_OF_MEMORY, "pair count of one call exceeds 2^32");
     const size_t p = (size_t)(Ptot > 0 ? Ptot : 1);
-    PF_CUDA(s->keys0.reserve(8 * p));
-    PF_CUDA(s->keys1.reserve(8 * p));
+    const size_t N = (size_t)s->ds.N;
+    const size_t nv = N * (size_t)Vb + 1;   // visible cells of one batch, at most
+    PF_CUDA(s->keys0.reserve(4 * p));
+    PF_CUDA(s->keys1.reserve(4 * p));
     PF_CUDA(s->vals1.reserve(4 * p));
     PF_CUDA(s->vals_all.reserve(4 * p));
     PF_CUDA(s->ranges_all.reserve(sizeof(uint2) * (size_t)T * V));
-    uint64_t *k0 = s->keys0.as<uint64_t>(), *k1 = s->keys1.as<uint64_t>();
+    PF_CUDA(s->ckeys0.reserve(8 * nv));
+    PF_CUDA(s->ckeys1.reserve(8 * nv));
+    PF_CUDA(s->cvals0.reserve(4 * nv));
+    PF_CUDA(s->cvals1.reserve(4 * nv));
+    PF_CUDA(s->ccnt.reserve(4 * nv));
+    PF_CUDA(s->coffs.reserve(4 * nv + 16));
+    const int nbx = pf::vis_blocks((int64_t)N);
+    PF_CUDA(s->bvis_off.reserve(4 * ((size_t)nbx * Vb + 16)));
+    uint32_t *k0 = s->keys0.as<uint32_t>(), *k1 = s->keys1.as<uint32_t>();
     uint32_t *v0 = s->vals_all.as<uint32_t>(), *v1 = s->vals1.as<uint32_t>();
     uint2 *rall = s->ranges_all.as<uint2>();
-    uint64_t *ks = k0;
+    long long *d_tmp = s->scan_totals.as<long long>() + V;   // two scratch totals (bin_views)
     for (int b0 = 0; b0 < V; b0 += kSortViews) {
         const int b1 = (b0 + kSortViews < V) ? b0 + kSortViews : V;
         const int64_t off = views[b0].pair_off;
         const int64_t Pb = views[b1 - 1].pair_off + views[b1 - 1].P - off;
-        for (int v = b0; v < b1; ++v) {
-            if (views[v].P == 0) continue;
-            PF_CUDA(pf::launch_emit(s, views[v], k0 + views[v].pair_off, v0 + views[v].pair_off,
-                                    (uint64_t)(v - b0) << (32 + tb), st));
-        }
-        bool alt = false;
+        const pf::BatchViews bv = batch_views(views, b0, b1);
+        int64_t nvis = 0;
+        for (int v = b0; v < b1; ++v) nvis += views[v].nvis;
         if (Pb > 0) {
-            PF_CUDA(pf::radix_sort_pairs(s, k0 + off, v0 + off, k1 + off, v1 + off, Pb, 32 + tb + vb,
-                                         &alt, st));
+            PF_CUDA(pf::launch_compact_visible(s, bv, nbx, s->bvis.as<int>(), s->bvis_off.as<uint32_t>(),
+                                               d_tmp, s->ckeys0.as<unsigned long long>(),
+                                               s->cvals0.as<uint32_t>(), st));
+            bool alt = false;   // (radix_sort_pairs times itself as stage 4)
+            PF_CUDA(pf::radix_sort_pairs(s, s->ckeys0.as<uint64_t>(), s->cvals0.as<uint32_t>(),
+                                         s->ckeys1.as<uint64_t>(), s->cvals1.as<uint32_t>(), nvis,
+                                         32 + vb, &alt, st));
+            const unsigned long long *sk = (alt ? s->ckeys1 : s->ckeys0).as<unsigned long long>();
+            const uint32_t *sv = (alt ? s->cvals1 : s->cvals0).as<uint32_t>();
+            PF_CUDA(pf::launch_emit_sorted(s, bv, tb, sk, sv, nvis, s->ccnt.as<int>(),
+                                           s->coffs.as<uint32_t>(), d_tmp + 1,
+                                           k0 + off, v0 + off, st));
+            PF_CUDA(pf::radix_sort_pairs32(s, k0 + off, v0 + off, k1 + off, v1 + off, Pb, tb + vb,
+                                           &alt, st));
             if (alt) {
                 PF_CUDA(cudaMemcpyAsync(v0 + off, v1 + off, 4 * (size_t)Pb, cudaMemcpyDeviceToDevice, st));
-                PF_CUDA(cudaMemcpyAsync(k0 + off, k1 + off, 8 * (size_t)Pb, cudaMemcpyDeviceToDevice, st));
+                PF_CUDA(cudaMemcpyAsync(k0 + off, k1 + off, 4 * (size_t)Pb, cudaMemcpyDeviceToDevice, st));
             }
         }
         // ranges of this batch's views, relative to the batch's first pair
@@ -172,39 +210,59 @@ int emit_sort_ranges(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st,
     }
     PF_CUDA(pf::launch_tile_order(s, rall, T, V, s->order_all.as<uint32_t>(),
                                   s->chunk_off_all.as<uint32_t>(), st));
-    *keys_out = ks;
+    *keys_out = k0;
     return PF_OK;
 }
 
-// K1 + K2 for views [0, V) then one readback of all pair totals.
-int bin_views(pf_scene *s, int V, cudaStream_t st)
+// K1 for views [0, V), the visible-cell and pair counts of every view (one
+// kernel per sort batch), then one readback of all pair totals and visible
+// counts (the call's only host sync before K6).
+int bin_views_of(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st)
 {
-    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t) * (size_t)V));
-    int64_t *d_tot = s->scan_totals.as<int64_t>();
+    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t) * (size_t)(V + 4)));
+    PF_CUDA(s->ptot.reserve(sizeof(long long) * (size_t)V));
+    long long *ptot = s->ptot.as<long long>();
+    PF_CUDA(cudaMemsetAsync(ptot, 0, sizeof(long long) * (size_t)V, st));
+    const int nbx = pf::vis_blocks(s->ds.N);
+    PF_CUDA(s->bvis.reserve(sizeof(int) * ((size_t)nbx * V + 16)));
     for (int v = 0; v < V; ++v) {
-        pf::ViewState &vs = s->views[v];
+        pf::ViewState &vs = views[v];
         int rc = reserve_view_bins(s, vs);
         if (rc) return rc;
         PF_CUDA(pf::launch_preprocess(s, vs, st));
-        PF_CUDA(pf::launch_scan_counts(s, vs, d_tot + v, st));
     }
-    if ((int)s->pinned_n < V) {
+    for (int b0 = 0; b0 < V; b0 += pf::kBatchViews) {
+        const int b1 = (b0 + pf::kBatchViews < V) ? b0 + pf::kBatchViews : V;
+        PF_CUDA(pf::launch_count_visible(s, batch_views(views, b0, b1), nbx, s->bvis.as<int>(),
+                                         ptot, st));
+    }
+    if ((int)s->pinned_n < 2 * V) {
         if (s->pinned) cudaFreeHost(s->pinned);
         s->pinned = nullptr;
         s->pinned_n = 0;
-        PF_CUDA(cudaMallocHost(&s->pinned, sizeof(int64_t) * (size_t)(V + 16)));
-        s->pinned_n = V + 16;
+        PF_CUDA(cudaMallocHost(&s->pinned, sizeof(int64_t) * (size_t)(2 * V + 16)));
+        s->pinned_n = 2 * V + 16;
     }
-    PF_CUDA(cudaMemcpyAsync(s->pinned, d_tot, sizeof(int64_t) * (size_t)V,
-                            cudaMemcpyDeviceToHost, st));
+    // per view: the pair total, and the visible cells (a sum over its blocks)
+    PF_CUDA(cudaMemcpyAsync(s->pinned, ptot, sizeof(int64_t) * (size_t)V, cudaMemcpyDeviceToHost, st));
+    std::vector<int> hb((size_t)nbx * V);
+    PF_CUDA(cudaMemcpyAsync(hb.data(), s->bvis.ptr, sizeof(int) * hb.size(), cudaMemcpyDeviceToHost, st));
     PF_CUDA(cudaStreamSynchronize(st));
     for (int v = 0; v < V; ++v) {
-        int64_t P = s->pinned[v];
+        const int64_t P = s->pinned[v];
         if (P < 0 || P >= (int64_t)0xFFFFFFFFll)
             return fail(PF_ERR_OUT_OF_MEMORY, "tile/cell pair count exceeds 2^32");
-        s->views[v].P = P;
+        views[v].P = P;
+        int64_t c = 0;
+        for (int b = 0; b < nbx; ++b) c += hb[(size_t)v * nbx + b];
+        views[v].nvis = c;
     }
     return PF_OK;
+}
+
+int bin_views(pf_scene *s, int V, cudaStream_t st)
+{
+    return bin_views_of(s, s->views.data(), V, st);
 }
 
 }  // namespace
@@ -427,7 +485,6 @@ int pf_destroy(pf_scene *s)
         v.rect.release();
         v.count.release();
         v.keybits.release();
-        v.offsets.release();
         v.tdir.release();
         v.saved.release();
         v.desc.release();
@@ -437,9 +494,11 @@ int pf_destroy(pf_scene *s)
     s->debug_view.rect.release();
     s->debug_view.count.release();
     s->debug_view.keybits.release();
-    s->debug_view.offsets.release();
     s->debug_view.tdir.release();
     s->vals_all.release();
+    pf::DevBuf *cbufs[] = {&s->bvis, &s->bvis_off, &s->ptot, &s->ckeys0, &s->ckeys1,
+                           &s->cvals0, &s->cvals1, &s->ccnt, &s->coffs};
+    for (auto *b : cbufs) b->release();
     s->ranges_all.release();
     s->order_all.release();
     s->chunk_off_all.release();
@@ -523,7 +582,7 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
         PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * (size_t)V));
         PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * (size_t)V, st));
     }
-    uint64_t *ks_all = nullptr;
+    uint32_t *ks_all = nullptr;
     rc = emit_sort_ranges(s, s->views.data(), V, st, &ks_all);
     if (rc) return rc;
     if (k0_side) PF_CUDA(cudaStreamWaitEvent(st, s->side_join, 0));
@@ -663,28 +722,22 @@ int pf_debug_binning(pf_scene *s, const pf_camera *cam, int32_t *rect, int32_t *
     pf::ViewState &vs = s->debug_view;
     s->fwd_views = 0;   // the debug pass reuses the call's sorted-pair arrays
     vs.cam = cam_params(*cam);
-    int64_t *d_tot;
-    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t)));
-    d_tot = s->scan_totals.as<int64_t>();
-    rc = reserve_view_bins(s, vs);
+    rc = bin_views_of(s, &vs, 1, st);
     if (rc) return rc;
-    PF_CUDA(pf::launch_preprocess(s, vs, st));
-    PF_CUDA(pf::launch_scan_counts(s, vs, d_tot, st));
-    int64_t P = 0;
-    PF_CUDA(cudaMemcpyAsync(&P, d_tot, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    PF_CUDA(cudaStreamSynchronize(st));
-    vs.P = P;
+    const int64_t P = vs.P;
     *num_pairs = P;
     const size_t N = (size_t)s->ds.N;
     if (rect) PF_CUDA(cudaMemcpyAsync(rect, vs.rect.ptr, 16 * N, cudaMemcpyDeviceToDevice, st));
     if (count) PF_CUDA(cudaMemcpyAsync(count, vs.count.ptr, 4 * N, cudaMemcpyDeviceToDevice, st));
     if (keybits) PF_CUDA(cudaMemcpyAsync(keybits, vs.keybits.ptr, 4 * N, cudaMemcpyDeviceToDevice, st));
     if (keys) {
-        uint64_t *ks = nullptr;
+        uint32_t *ks = nullptr;
         rc = emit_sort_ranges(s, &vs, 1, st, &ks);
         if (rc) return rc;
         if (P > 0) {
-            PF_CUDA(cudaMemcpyAsync(keys, ks, 8 * (size_t)P, cudaMemcpyDeviceToDevice, st));
+            // the sort's keys hold the tile only: export the full (tile << 32 | keybits)
+            PF_CUDA(pf::launch_full_keys(s, ks, vs.vals_p, vs.keybits.as<uint32_t>(), P,
+                                         tile_bits(vs.cam.tiles_x * vs.cam.tiles_y), keys, st));
             if (vals) PF_CUDA(cudaMemcpyAsync(vals, vs.vals_p, 4 * (size_t)P, cudaMemcpyDeviceToDevice, st));
         }
         if (ranges)
@@ -710,17 +763,9 @@ int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_s
     pf::ViewState &vs = s->debug_view;
     s->fwd_views = 0;   // the debug pass reuses the call's sorted-pair arrays
     vs.cam = cam_params(*cam);
-    PF_CUDA(s->scan_totals.reserve(sizeof(int64_t)));
-    int64_t *d_tot = s->scan_totals.as<int64_t>();
-    rc = reserve_view_bins(s, vs);
+    rc = bin_views_of(s, &vs, 1, st);
     if (rc) return rc;
-    PF_CUDA(pf::launch_preprocess(s, vs, st));
-    PF_CUDA(pf::launch_scan_counts(s, vs, d_tot, st));
-    int64_t P = 0;
-    PF_CUDA(cudaMemcpyAsync(&P, d_tot, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    PF_CUDA(cudaStreamSynchronize(st));
-    vs.P = P;
-    uint64_t *ks;
+    uint32_t *ks;
     rc = emit_sort_ranges(s, &vs, 1, st, &ks);
     if (rc) return rc;
     PF_CUDA(cudaMemsetAsync(counters, 0, 32 * (size_t)cam->width * cam->height, st));

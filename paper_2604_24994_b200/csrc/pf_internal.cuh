@@ -66,8 +66,9 @@ struct DevBuf {
 
 struct ViewState {
     CamParams cam{};
-    int64_t P = 0;
-    DevBuf rect, count, keybits, offsets;   // binning of this view (N-sized)
+    int64_t P = 0;                           // tile/cell pairs of this view
+    int64_t nvis = 0;                        // visible cells (count > 0)
+    DevBuf rect, count, keybits;             // binning of this view (N-sized)
     DevBuf tdir;                             // fisheye: tile-centre rays (3T doubles) + cos/sin(th)
     uint32_t *vals_p = nullptr;              // sorted cell ids (the call's shared array)
     uint2 *ranges_p = nullptr;               // this view's per-tile [start,end) into vals_p
@@ -82,6 +83,18 @@ struct ViewState {
 };
 
 struct BallBVH;   // pf_bvh.cuh
+
+// one sort batch of up to kBatchViews views (kernel parameter of the binning)
+constexpr int kBatchViews = 8;
+struct BatchViews {
+    const int *count[kBatchViews];
+    const uint32_t *keybits[kBatchViews];
+    const int4 *rect[kBatchViews];
+    const double *tdir[kBatchViews];
+    CamParams cam[kBatchViews];
+    int n;       // views in the batch
+    int first;   // index of the batch's first view in the call
+};
 
 struct StageEvent {
     int stage;
@@ -99,6 +112,8 @@ struct pf_scene {
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
     pf::DevBuf vals_all, ranges_all;   // sorted pairs of all views of the last call
+    pf::DevBuf bvis, bvis_off, ptot;   // visible-cell counts per (view, block), pair totals
+    pf::DevBuf ckeys0, ckeys1, cvals0, cvals1, ccnt, coffs;   // visible cells sorted by depth
     pf::DevBuf order_all, chunk_off_all;  // per-view tile orders / chunk offsets (V x T)
     pf::DevBuf acc;                 // backward packed accumulators
     pf::DevBuf rec_used;            // u32[V] records used per view (K6 atomics)
@@ -131,13 +146,26 @@ namespace pf {
 cudaError_t launch_edge_records(pf_scene *s, cudaStream_t st);
 cudaError_t launch_validate(pf_scene *s, int *d_flag, cudaStream_t st);
 cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st);
-cudaError_t launch_scan_counts(pf_scene *s, ViewState &v, int64_t *d_total, cudaStream_t st);
-cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
-                        uint64_t view_key, cudaStream_t st);
 cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                              uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
                              cudaStream_t st);
-cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, int tile_bits,
+cudaError_t radix_sort_pairs32(pf_scene *s, uint32_t *keys, uint32_t *vals, uint32_t *keys_alt,
+                               uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
+                               cudaStream_t st);
+int vis_blocks(int64_t N);
+cudaError_t launch_count_visible(pf_scene *s, const BatchViews &bv, int nbx, int *bvis,
+                                 long long *ptot, cudaStream_t st);
+cudaError_t launch_compact_visible(pf_scene *s, const BatchViews &bv, int nbx, const int *bvis,
+                                   uint32_t *boff, long long *d_nvis, unsigned long long *keys,
+                                   uint32_t *vals, cudaStream_t st);
+cudaError_t launch_emit_sorted(pf_scene *s, const BatchViews &bv, int tile_bits,
+                               const unsigned long long *skeys, const uint32_t *svals, int64_t n,
+                               int *cnt_sorted, uint32_t *offs, long long *d_tot,
+                               uint32_t *keys, uint32_t *vals, cudaStream_t st);
+cudaError_t launch_full_keys(pf_scene *s, const uint32_t *tkeys, const uint32_t *vals,
+                             const uint32_t *keybits, int64_t P, int tile_bits, uint64_t *out,
+                             cudaStream_t st);
+cudaError_t launch_ranges(pf_scene *s, const uint32_t *keys, int64_t P, int T, int tile_bits,
                           uint2 *ranges_all, int V, cudaStream_t st);
 cudaError_t launch_tile_order(pf_scene *s, const uint2 *ranges_all, int T, int V,
                               uint32_t *order_all, uint32_t *chunk_off_all, cudaStream_t st);

@@ -536,45 +536,115 @@ cudaError_t exclusive_scan_counts(pf_scene *s, const int *cnt, int64_t n, uint32
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan_counts(pf_scene *s, ViewState &v, int64_t *d_total, cudaStream_t st)
-{
-    cudaEvent_t ev;
-    stage_begin(s, 2, st, &ev);
-    cudaError_t err = exclusive_scan_counts(s, v.count.as<int>(), s->ds.N,
-                                            v.offsets.as<uint32_t>(), (long long *)d_total, st);
-    stage_end(s, 2, st, ev);
-    return err;
-}
 
 // ------------------------------------------------------------------------
-// K3: emit (tile << 32 | keybits, cell) pairs -- one warp per 32 cells, the
-// warp writes each cell's pairs cooperatively (coalesced, big rects balanced)
+// Depth-first binning of a batch of up to kBatchViews views (replaces the
+// 48-bit pair sort): every view's VISIBLE cells (count > 0) are compacted in
+// cell order, sorted ONCE by (view, depth key) -- ~N_vis items instead of P
+// pairs --, their tile pairs are emitted in that order with a 16-bit
+// (view, tile) key, and a stable 2-pass radix sort by (view, tile) finishes:
+// inside a tile the pairs keep the (depth key, cell) order of the emission,
+// which is exactly the order of the stable (tile << 32 | key) sort of
+// cell-major pairs (ties by cell index).
 // ------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__restrict__ count,
-        const uint32_t *__restrict__ keybits, const uint32_t *__restrict__ offs,
-        unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
-        unsigned long long view_key)
+constexpr int kVisThreads = 256, kVisItems = 8, kVisChunk = kVisThreads * kVisItems;
+
+// KV1: per (view, block of kVisChunk cells): number of visible cells -> bvis,
+// and the view's pair total (sum of counts) -> ptot[view] (atomics; integers)
+__global__ void __launch_bounds__(kVisThreads)
+kv1_count(BatchViews bv, int64_t N, int nbx, int *__restrict__ bvis, long long *__restrict__ ptot)
 {
-    // A warp owns 32 consecutive cells, whose pairs occupy one contiguous output
-    // range [off[i0], off[i0] + total).  It writes that range 32 positions at a
-    // time (coalesced); position p finds its source lane by a 5-step binary
-    // search over the lanes' offsets (shuffles), so big rectangles are balanced.
+    __shared__ long long sw[33];
+    __shared__ int swi[33];
+    const int v = blockIdx.y;
+    const int *cnt = bv.count[v];
+    const int64_t base = (int64_t)blockIdx.x * kVisChunk;
+    int nv = 0;
+    long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+        const int64_t i = base + (int64_t)k * kVisThreads + threadIdx.x;
+        if (i < N) {
+            const int c = cnt[i];
+            nv += c > 0;
+            sum += c;
+        }
+    }
+    long long tot;
+    block_excl_scan<long long>(sum, sw, &tot);
+    int ntot;
+    block_excl_scan<int>(nv, swi, &ntot);
+    if (threadIdx.x == 0) {
+        bvis[(size_t)(bv.first + v) * nbx + blockIdx.x] = ntot;
+        if (tot) atomicAdd(reinterpret_cast<unsigned long long *>(ptot + bv.first + v),
+                           (unsigned long long)tot);
+    }
+}
+
+// KV2: compaction of the visible cells (view-major, ascending cell index) into
+// (view << 32 | keybits, cell) at the scanned block offsets
+__global__ void __launch_bounds__(kVisThreads)
+kv2_compact(BatchViews bv, int64_t N, int nbx, const uint32_t *__restrict__ boff,
+            unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals)
+{
+    __shared__ int swi[33];
+    const int v = blockIdx.y;
+    const int *cnt = bv.count[v];
+    const uint32_t *kb = bv.keybits[v];
+    const int64_t base = (int64_t)blockIdx.x * kVisChunk + (int64_t)threadIdx.x * kVisItems;
+    int f[kVisItems];
+    int nv = 0;
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+        const int64_t i = base + k;
+        f[k] = (i < N) && cnt[i] > 0;
+        nv += f[k];
+    }
+    int tot;
+    int o = block_excl_scan<int>(nv, swi, &tot) + (int)boff[(size_t)v * nbx + blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+        if (f[k]) {
+            const int64_t i = base + k;
+            keys[o] = ((unsigned long long)v << 32) | kb[i];
+            vals[o] = (uint32_t)i;
+            ++o;
+        }
+    }
+}
+
+// KV3: counts of the sorted visible cells (the emission sizes, in depth order)
+__global__ void __launch_bounds__(256)
+kv3_gather(BatchViews bv, const unsigned long long *__restrict__ keys,
+           const uint32_t *__restrict__ vals, int64_t n, int *__restrict__ cnt_sorted)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    cnt_sorted[q] = bv.count[(int)(keys[q] >> 32)][vals[q]];
+}
+
+// KV4: emission in depth order, pinhole views (a warp writes its 32
+// items' contiguous output range 32 pairs at a time), key = view << tb | tile
+__global__ void __launch_bounds__(256)
+kv4_emit(BatchViews bv, int tile_bits, const unsigned long long *__restrict__ skeys,
+         const uint32_t *__restrict__ svals, const int *__restrict__ cnt_sorted,
+         const uint32_t *__restrict__ offs, int64_t n, uint32_t *__restrict__ keys,
+         uint32_t *__restrict__ vals)
+{
     const int lane = threadIdx.x & 31;
     const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
     const int64_t i = i0 + lane;
-    int cnt = 0;
+    int cnt = 0, view = 0, tx = 1;
+    uint32_t cell = 0, off = 0;
     int4 rc = make_int4(0, 0, 1, 0);
-    uint32_t kb = 0, off = 0;
-    if (i < N) {
-        cnt = count[i];
+    if (i < n) {
+        cnt = cnt_sorted[i];
         off = offs[i];
-        if (cnt) {
-            rc = rect[i];
-            kb = keybits[i];
-        }
+        view = (int)(skeys[i] >> 32);
+        cell = svals[i];
+        rc = bv.rect[view][cell];
+        tx = bv.cam[view].tiles_x;
     }
-    // exclusive prefix of the counts inside the warp (offs is the global one)
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -583,8 +653,9 @@ k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__rest
     }
     const int excl = incl - cnt;
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t base = __shfl_sync(0xffffffffu, off, 0) ;
+    const uint32_t base = __shfl_sync(0xffffffffu, off, 0);
     const int w = rc.z - rc.x;
+    const uint32_t vkey = (uint32_t)view << tile_bits;
     for (int p0 = 0; p0 < total; p0 += 32) {
         const int p = p0 + lane;
         int src = 0;
@@ -598,105 +669,158 @@ k3_emit(int64_t N, int tiles_x, const int4 *__restrict__ rect, const int *__rest
         const int x0 = __shfl_sync(0xffffffffu, rc.x, src);
         const int y0 = __shfl_sync(0xffffffffu, rc.y, src);
         const int ww = __shfl_sync(0xffffffffu, w, src);
-        const uint32_t k = __shfl_sync(0xffffffffu, kb, src);
+        const int tw = __shfl_sync(0xffffffffu, tx, src);
+        const uint32_t vk = __shfl_sync(0xffffffffu, vkey, src);
+        const uint32_t c = __shfl_sync(0xffffffffu, cell, src);
         if (p < total) {
             const int q = p - ex;
             const int dy = q / ww, dx = q - dy * ww;
-            const unsigned long long tile = (unsigned long long)((y0 + dy) * tiles_x + (x0 + dx));
-            keys[base + p] = view_key | (tile << 32) | k;
-            vals[base + p] = (uint32_t)(i0 + src);
+            keys[base + p] = vk | (uint32_t)((y0 + dy) * tw + (x0 + dx));
+            vals[base + p] = c;
         }
     }
 }
 
-// fisheye emission: the warp's 32 cells one after another, the lanes over the
-// cell's candidate tiles (re-tested; the count from K1 is the number that pass),
-// passing tiles compacted by ballot so the key/value stores are contiguous
+// KV4 for batches with fisheye views: the warp's items one after another, the
+// lanes over the item's candidate tiles (fisheye tiles re-tested as in
+// K1 counted them; pinhole rects taken whole), ballot-compacted stores
 __global__ void __launch_bounds__(256)
-k3_emit_fisheye(int64_t N, CamParams cam, const float *__restrict__ sites,
-                const float *__restrict__ radii, const int4 *__restrict__ rect,
-                const int *__restrict__ count, const uint32_t *__restrict__ keybits,
-                const uint32_t *__restrict__ offs, unsigned long long *__restrict__ keys,
-                uint32_t *__restrict__ vals, unsigned long long view_key,
-                const double *__restrict__ tdir)
+kv4_emit_items(BatchViews bv, int tile_bits, const float *__restrict__ sites,
+               const float *__restrict__ radii, const unsigned long long *__restrict__ skeys,
+               const uint32_t *__restrict__ svals, const uint32_t *__restrict__ offs, int64_t n,
+               uint32_t *__restrict__ keys, uint32_t *__restrict__ vals)
 {
     const int lane = threadIdx.x & 31;
     const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
-    if (i0 >= N) return;
-    const int64_t i = i0 + lane;
-    int cnt = 0;
-    if (i < N) cnt = count[i];
-    unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);
-    const int T = cam.tiles_x * cam.tiles_y;
-    const double cth = __ldg(tdir + 3 * T), sth = __ldg(tdir + 3 * T + 1);
-    while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int64_t cell = i0 + src;
-        const int4 rc = rect[cell];
-        double c[3];
-        camera_coords(cam, sites + 3 * cell, c);
-        const double r = radii[cell];
-        const uint32_t k = keybits[cell];
-        uint32_t o = offs[cell];
-        const int w = rc.z - rc.x, n = w * (rc.w - rc.y);
-        for (int b = 0; b < n; b += 32) {
+    if (i0 >= n) return;
+    const int m = (int)min((int64_t)32, n - i0);
+    for (int src = 0; src < m; ++src) {
+        const int64_t it = i0 + src;
+        const int view = (int)(skeys[it] >> 32);
+        const uint32_t cell = svals[it];
+        const CamParams &cam = bv.cam[view];
+        const int4 rc = bv.rect[view][cell];
+        uint32_t o = offs[it];
+        const uint32_t vkey = (uint32_t)view << tile_bits;
+        const int w = rc.z - rc.x, cntt = w * (rc.w - rc.y);
+        double c[3] = {0.0, 0.0, 0.0};
+        double r = 0.0, cth = 0.0, sth = 0.0;
+        const double *tdir = bv.tdir[view];
+        const bool fish = cam.model == PF_FISHEYE;
+        if (fish) {
+            camera_coords(cam, sites + 3 * (size_t)cell, c);
+            r = radii[cell];
+            const int T = cam.tiles_x * cam.tiles_y;
+            cth = __ldg(tdir + 3 * T);
+            sth = __ldg(tdir + 3 * T + 1);
+        }
+        for (int b = 0; b < cntt; b += 32) {
             const int t = b + lane;
             const int tx = rc.x + (w ? t % w : 0), ty = rc.y + (w ? t / w : 0);
-            const bool pass = t < n && fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir);
-            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            const bool pass = t < cntt && (!fish || fisheye_tile_pass(cam, c, r, cth, sth, tx, ty, tdir));
+            const unsigned msk = __ballot_sync(0xffffffffu, pass);
             if (pass) {
-                const uint32_t q = o + __popc(m & ((1u << lane) - 1u));
-                const unsigned long long tile = (unsigned long long)(ty * cam.tiles_x + tx);
-                keys[q] = view_key | (tile << 32) | k;
-                vals[q] = (uint32_t)cell;
+                const uint32_t q = o + __popc(msk & ((1u << lane) - 1u));
+                keys[q] = vkey | (uint32_t)(ty * cam.tiles_x + tx);
+                vals[q] = cell;
             }
-            o += __popc(m);
+            o += __popc(msk);
         }
     }
 }
 
-cudaError_t launch_emit(pf_scene *s, ViewState &v, uint64_t *keys, uint32_t *vals,
-                        uint64_t view_key, cudaStream_t st)
+// debug export: full (tile << 32 | keybits) keys of a single-view call
+__global__ void __launch_bounds__(256)
+kv5_full_keys(const uint32_t *__restrict__ tkeys, const uint32_t *__restrict__ vals,
+              const uint32_t *__restrict__ keybits, int64_t P, int tile_bits,
+              unsigned long long *__restrict__ out)
 {
-    if (v.cam.model == PF_FISHEYE) {
-        cudaEvent_t ev;
-        stage_begin(s, 3, st, &ev);
-        k3_emit_fisheye<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
-            s->ds.N, v.cam, s->ds.sites, s->ds.radii, v.rect.as<int4>(), v.count.as<int>(),
-            v.keybits.as<uint32_t>(), v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals,
-            (unsigned long long)view_key, v.tdir.as<double>());
-        ++s->launches;
-        stage_end(s, 3, st, ev);
-        return cudaGetLastError();
-    }
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P) return;
+    const unsigned long long tile = tkeys[q] & ((1u << tile_bits) - 1u);
+    out[q] = (tile << 32) | keybits[vals[q]];
+}
+
+cudaError_t launch_count_visible(pf_scene *s, const BatchViews &bv, int nbx, int *bvis,
+                                 long long *ptot, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 2, st, &ev);
+    kv1_count<<<dim3(nbx, bv.n), kVisThreads, 0, st>>>(bv, s->ds.N, nbx, bvis, ptot);
+    ++s->launches;
+    stage_end(s, 2, st, ev);
+    return cudaGetLastError();
+}
+
+int vis_blocks(int64_t N) { return ceil_div(N, kVisChunk); }
+
+cudaError_t launch_compact_visible(pf_scene *s, const BatchViews &bv, int nbx, const int *bvis,
+                                   uint32_t *boff, long long *d_nvis, unsigned long long *keys,
+                                   uint32_t *vals, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 2, st, &ev);
+    cudaError_t err = exclusive_scan_counts(s, bvis + (size_t)bv.first * nbx, (int64_t)bv.n * nbx,
+                                            boff, d_nvis, st);
+    if (err != cudaSuccess) return err;
+    kv2_compact<<<dim3(nbx, bv.n), kVisThreads, 0, st>>>(bv, s->ds.N, nbx, boff, keys, vals);
+    ++s->launches;
+    stage_end(s, 2, st, ev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_emit_sorted(pf_scene *s, const BatchViews &bv, int tile_bits,
+                               const unsigned long long *skeys, const uint32_t *svals, int64_t n,
+                               int *cnt_sorted, uint32_t *offs, long long *d_tot,
+                               uint32_t *keys, uint32_t *vals, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
     cudaEvent_t ev;
     stage_begin(s, 3, st, &ev);
-    k3_emit<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(
-        s->ds.N, v.cam.tiles_x, v.rect.as<int4>(), v.count.as<int>(), v.keybits.as<uint32_t>(),
-        v.offsets.as<uint32_t>(), (unsigned long long *)keys, vals,
-        (unsigned long long)view_key);
+    kv3_gather<<<ceil_div(n, 256), 256, 0, st>>>(bv, skeys, svals, n, cnt_sorted);
+    ++s->launches;
+    cudaError_t err = exclusive_scan_counts(s, cnt_sorted, n, offs, d_tot, st);
+    if (err != cudaSuccess) return err;
+    bool fish = false;
+    for (int v = 0; v < bv.n; ++v) fish = fish || bv.cam[v].model == PF_FISHEYE;
+    if (fish)
+        kv4_emit_items<<<ceil_div(n, 256), 256, 0, st>>>(bv, tile_bits, s->ds.sites, s->ds.radii,
+                                                          skeys, svals, offs, n, keys, vals);
+    else
+        kv4_emit<<<ceil_div(n, 256), 256, 0, st>>>(bv, tile_bits, skeys, svals, cnt_sorted, offs,
+                                                    n, keys, vals);
     ++s->launches;
     stage_end(s, 3, st, ev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_full_keys(pf_scene *s, const uint32_t *tkeys, const uint32_t *vals,
+                             const uint32_t *keybits, int64_t P, int tile_bits, uint64_t *out,
+                             cudaStream_t st)
+{
+    if (P == 0) return cudaSuccess;
+    kv5_full_keys<<<ceil_div(P, 256), 256, 0, st>>>(tkeys, vals,
+                                                    keybits, P, tile_bits,
+                                                    (unsigned long long *)out);
+    ++s->launches;
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------
 // K5: per-tile ranges [start, end) of the sorted pairs ((0,0) for empty tiles)
 // ------------------------------------------------------------------------
-// keys of all views of a call: (view << (32 + tile_bits)) | (tile << 32) | keybits;
-// ranges[view * T + tile] = [start, end) in the call's sorted arrays.
-__global__ void __launch_bounds__(256) k5_ranges(const unsigned long long *__restrict__ keys,
+// keys of all views of a sort batch: (view << tile_bits) | tile (kv4_emit);
+// ranges[view * T + tile] = [start, end) in the batch's sorted arrays.
+__global__ void __launch_bounds__(256) k5_ranges(const uint32_t *__restrict__ keys,
                                                  int64_t P, int T, int tile_bits,
                                                  uint2 *__restrict__ ranges)
 {
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= P) return;
-    const unsigned long long vt = keys[q] >> 32;   // (view << tile_bits) | tile
-    const uint32_t idx = (uint32_t)(vt >> tile_bits) * (uint32_t)T +
-                         (uint32_t)(vt & ((1ull << tile_bits) - 1ull));
-    if (q == 0 || (keys[q - 1] >> 32) != vt) ranges[idx].x = (uint32_t)q;
-    if (q == P - 1 || (keys[q + 1] >> 32) != vt) ranges[idx].y = (uint32_t)(q + 1);
+    const uint32_t vt = keys[q];   // (view << tile_bits) | tile
+    const uint32_t idx = (vt >> tile_bits) * (uint32_t)T + (vt & ((1u << tile_bits) - 1u));
+    if (q == 0 || keys[q - 1] != vt) ranges[idx].x = (uint32_t)q;
+    if (q == P - 1 || keys[q + 1] != vt) ranges[idx].y = (uint32_t)(q + 1);
 }
 
 // Grid order for K6/K7: tiles by decreasing list length (longest-processing-time
@@ -749,7 +873,7 @@ __global__ void __launch_bounds__(1024) k5_tile_order(const uint2 *__restrict__ 
     }
 }
 
-cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, int tile_bits,
+cudaError_t launch_ranges(pf_scene *s, const uint32_t *keys, int64_t P, int T, int tile_bits,
                           uint2 *ranges_all, int V, cudaStream_t st)
 {
     cudaError_t err = cudaMemsetAsync(ranges_all, 0, sizeof(uint2) * (size_t)T * V, st);
@@ -757,7 +881,7 @@ cudaError_t launch_ranges(pf_scene *s, const uint64_t *keys, int64_t P, int T, i
     if (P == 0) return cudaSuccess;
     cudaEvent_t ev;
     stage_begin(s, 5, st, &ev);
-    k5_ranges<<<ceil_div(P, 256), 256, 0, st>>>((const unsigned long long *)keys, P, T, tile_bits,
+    k5_ranges<<<ceil_div(P, 256), 256, 0, st>>>(keys, P, T, tile_bits,
                                                  ranges_all);
     ++s->launches;
     stage_end(s, 5, st, ev);

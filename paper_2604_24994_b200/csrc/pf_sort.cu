@@ -29,9 +29,9 @@ constexpr int kSortThreads = PF_SORT_THREADS, kSortItems = PF_SORT_TILE / PF_SOR
               kSortTile = kSortThreads * kSortItems, kSortWarps = kSortThreads / 32;
 constexpr int kRadixBits = 8, kRadix = 1 << kRadixBits;
 
+template <class KeyT>
 __global__ void __launch_bounds__(kSortThreads)
-k4_histogram(const unsigned long long *__restrict__ keys, int64_t n, int shift, int nb,
-             int *__restrict__ hist)
+k4_histogram(const KeyT *__restrict__ keys, int64_t n, int shift, int nb, int *__restrict__ hist)
 {
     __shared__ int h[kSortWarps][kRadix];
     const int warp = threadIdx.x >> 5;
@@ -60,17 +60,21 @@ k4_histogram(const unsigned long long *__restrict__ keys, int64_t n, int shift, 
 // staged in shared memory, and the threads then write it out in tile order, so
 // each digit's run (about 16 keys per block) goes to consecutive addresses:
 // coalesced stores instead of one scattered 8-byte store per key.
-constexpr size_t kScatterSmem = (size_t)kSortTile * (sizeof(unsigned long long) + sizeof(uint32_t)) +
-                                (size_t)kSortWarps * kRadix * sizeof(uint32_t) +
-                                2 * kRadix * sizeof(uint32_t);
+template <class KeyT>
+constexpr size_t scatter_smem()
+{
+    return (size_t)kSortTile * (sizeof(KeyT) + sizeof(uint32_t)) +
+           (size_t)kSortWarps * kRadix * sizeof(uint32_t) + 2 * kRadix * sizeof(uint32_t);
+}
 
+template <class KeyT>
 __global__ void __launch_bounds__(kSortThreads)
-k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restrict__ vin,
-           unsigned long long *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
-           int shift, int nb, const uint32_t *__restrict__ digit_offs)
+k4_scatter(const KeyT *__restrict__ kin, const uint32_t *__restrict__ vin, KeyT *__restrict__ kout,
+           uint32_t *__restrict__ vout, int64_t n, int shift, int nb,
+           const uint32_t *__restrict__ digit_offs)
 {
     extern __shared__ __align__(16) unsigned char sort_smem[];
-    unsigned long long *sk = reinterpret_cast<unsigned long long *>(sort_smem);
+    KeyT *sk = reinterpret_cast<KeyT *>(sort_smem);
     uint32_t *sv = reinterpret_cast<uint32_t *>(sk + kSortTile);
     uint32_t(*wh)[kRadix] = reinterpret_cast<uint32_t(*)[kRadix]>(sv + kSortTile);
     uint32_t *dstart = reinterpret_cast<uint32_t *>(wh + kSortWarps);
@@ -81,14 +85,14 @@ k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restric
     const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t bbase = (int64_t)blockIdx.x * kSortTile;
     const int64_t wbase = bbase + (int64_t)warp * (32 * kSortItems);
-    unsigned long long key[kSortItems];
+    KeyT key[kSortItems];
     uint32_t val[kSortItems], rank[kSortItems];
     int dig[kSortItems];
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         int64_t idx = wbase + r * 32 + lane;
         bool valid = idx < n;
-        key[r] = valid ? kin[idx] : 0ull;
+        key[r] = valid ? kin[idx] : KeyT(0);
         val[r] = valid ? vin[idx] : 0u;
     }
 #pragma unroll
@@ -150,7 +154,7 @@ k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restric
     __syncthreads();
     const int nvalid = (int)min((int64_t)kSortTile, n - bbase);
     for (int q = threadIdx.x; q < nvalid; q += kSortThreads) {
-        const unsigned long long k = sk[q];
+        const KeyT k = sk[q];
         const int d = (int)((k >> shift) & (kRadix - 1));
         const uint32_t pos = gbase[d] + ((uint32_t)q - dstart[d]);
         kout[pos] = k;
@@ -158,9 +162,10 @@ k4_scatter(const unsigned long long *__restrict__ kin, const uint32_t *__restric
     }
 }
 
-cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
-                             uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
-                             cudaStream_t st)
+template <class KeyT>
+static cudaError_t radix_sort_t(pf_scene *s, KeyT *keys, uint32_t *vals, KeyT *keys_alt,
+                                uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
+                                cudaStream_t st)
 {
     *result_in_alt = false;
     if (n <= 1) return cudaSuccess;
@@ -172,28 +177,45 @@ cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64
     uint32_t *offs = reinterpret_cast<uint32_t *>(hist + hist_n);
     long long *dummy_total = reinterpret_cast<long long *>(
         (reinterpret_cast<uintptr_t>(offs + hist_n) + 15) & ~uintptr_t(15));
-    unsigned long long *ka = (unsigned long long *)keys, *kb = (unsigned long long *)keys_alt;
+    KeyT *ka = keys, *kb = keys_alt;
     uint32_t *va = vals, *vb = vals_alt;
     bool alt = false;
     cudaEvent_t ev;
-    cudaFuncSetAttribute(k4_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem);
+    constexpr size_t smem = scatter_smem<KeyT>();
+    cudaFuncSetAttribute(k4_scatter<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     stage_begin(s, 4, st, &ev);
     for (int shift = 0; shift < end_bit; shift += kRadixBits) {
-        k4_histogram<<<nb, kSortThreads, 0, st>>>(ka, n, shift, nb, hist);
+        k4_histogram<KeyT><<<nb, kSortThreads, 0, st>>>(ka, n, shift, nb, hist);
         ++s->launches;
         err = exclusive_scan_counts(s, hist, (int64_t)hist_n, offs, dummy_total, st);
         if (err != cudaSuccess) return err;
-        k4_scatter<<<nb, kSortThreads, kScatterSmem, st>>>(ka, va, kb, vb, n, shift, nb, offs);
+        k4_scatter<KeyT><<<nb, kSortThreads, smem, st>>>(ka, va, kb, vb, n, shift, nb, offs);
         ++s->launches;
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
-        unsigned long long *tk = ka; ka = kb; kb = tk;
+        KeyT *tk = ka; ka = kb; kb = tk;
         uint32_t *tv = va; va = vb; vb = tv;
         alt = !alt;
     }
     stage_end(s, 4, st, ev);
     *result_in_alt = alt;
     return cudaGetLastError();
+}
+
+cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+                             uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
+                             cudaStream_t st)
+{
+    return radix_sort_t<unsigned long long>(s, (unsigned long long *)keys, vals,
+                                            (unsigned long long *)keys_alt, vals_alt, n, end_bit,
+                                            result_in_alt, st);
+}
+
+cudaError_t radix_sort_pairs32(pf_scene *s, uint32_t *keys, uint32_t *vals, uint32_t *keys_alt,
+                               uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
+                               cudaStream_t st)
+{
+    return radix_sort_t<uint32_t>(s, keys, vals, keys_alt, vals_alt, n, end_bit, result_in_alt, st);
 }
 
 }  // namespace pf
