@@ -28,12 +28,15 @@ namespace {
 
 constexpr int kStack = 64;
 
-__device__ __forceinline__ uint32_t expand_bits(uint32_t v)
+// spread the low 21 bits of v to every third bit of a 63-bit word
+__device__ __forceinline__ unsigned long long expand_bits21(unsigned long long v)
 {
-    v = (v * 0x00010001u) & 0xFF0000FFu;
-    v = (v * 0x00000101u) & 0x0F00F00Fu;
-    v = (v * 0x00000011u) & 0xC30C30C3u;
-    v = (v * 0x00000005u) & 0x49249249u;
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x001f00000000ffffull;
+    v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
     return v;
 }
 
@@ -79,24 +82,28 @@ __global__ void c1_morton(const float *__restrict__ sites, int64_t N, const floa
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    uint32_t q[3];
+    // 63-bit codes (21 bits per axis): scenes with a dense object inside a wide
+    // shell (mip360: |p| up to 80, cells of ~0.01 near the centre) would otherwise
+    // put thousands of centre cells on one 30-bit code, split by index order only
+    unsigned long long q[3];
     for (int m = 0; m < 3; ++m) {
-        const float ext = fmaxf(bb[3 + m] - bb[m], 1e-30f);
-        const float u = fminf(fmaxf((sites[3 * i + m] - bb[m]) / ext, 0.0f), 1.0f);
-        q[m] = min((uint32_t)(u * 1024.0f), 1023u);
+        const double ext = fmax((double)bb[3 + m] - (double)bb[m], 1e-30);
+        const double u = fmin(fmax(((double)sites[3 * i + m] - (double)bb[m]) / ext, 0.0), 1.0);
+        q[m] = (unsigned long long)fmin(u * 2097152.0, 2097151.0);
     }
-    keys[i] = (expand_bits(q[0]) << 2) | (expand_bits(q[1]) << 1) | expand_bits(q[2]);
+    keys[i] = (expand_bits21(q[0]) << 2) | (expand_bits21(q[1]) << 1) | expand_bits21(q[2]);
     vals[i] = (uint32_t)i;
 }
 
-// common-prefix length of the unique 64-bit keys (morton << 32 | sorted position)
+// common-prefix length of the unique 96-bit keys (63-bit morton code, then the
+// 32-bit sorted position)
 __device__ __forceinline__ int delta(const unsigned long long *__restrict__ codes, int64_t n,
                                      int64_t i, int64_t j)
 {
     if (j < 0 || j >= n) return -1;
-    const unsigned long long a = (codes[i] << 32) | (unsigned long long)i;
-    const unsigned long long b = (codes[j] << 32) | (unsigned long long)j;
-    return __clzll(a ^ b);
+    const unsigned long long a = codes[i], b = codes[j];
+    if (a != b) return __clzll(a ^ b);
+    return 64 + __clz((uint32_t)i ^ (uint32_t)j);
 }
 
 // Karras (2012): internal node i of n-1, children encoded as (idx << 1) | is_leaf
@@ -347,7 +354,7 @@ cudaError_t build_ball_bvh(pf_scene *scratch, BallBVH &B, int64_t N, const float
                                                  B.keys.as<unsigned long long>(), B.vals.as<uint32_t>());
     bool alt = false;
     PF_BV(radix_sort_pairs(scratch, B.keys.as<uint64_t>(), B.vals.as<uint32_t>(),
-                           B.keys_alt.as<uint64_t>(), B.vals_alt.as<uint32_t>(), N, 30, &alt, st));
+                           B.keys_alt.as<uint64_t>(), B.vals_alt.as<uint32_t>(), N, 63, &alt, st));
     const unsigned long long *codes = (alt ? B.keys_alt : B.keys).as<unsigned long long>();
     B.order = (alt ? B.vals_alt : B.vals).as<uint32_t>();
     B.n = N;

@@ -41,13 +41,9 @@ namespace pf {
 #ifndef PF_K7_DIRECT_MAX   // up to this many segment lanes: per-lane atomics, no warp reduction
 #define PF_K7_DIRECT_MAX 10
 #endif
-#ifndef PF_K7_SMEMACC   // K7: own-cell gradient terms summed per CTA in shared memory
-#define PF_K7_SMEMACC 0
-#endif
 #ifndef PF_K7_GROUP   // K7: up to this many consecutive disjoint-mask records per pass
 #define PF_K7_GROUP 4
 #endif
-constexpr int kAccSlots = 512;   // tile-list slots with a shared own-cell accumulator
 #ifndef PF_K7D_MINB
 #define PF_K7D_MINB 1
 #endif
@@ -744,8 +740,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
                                                  const DeviceScene &ds, float *acc, int lane,
                                                  float cr, float cg, float cb, const float4 &dnrm,
                                                  const DetailCtx *X, const float *om,
-                                                 float (*buf)[33], bool grouped = false,
-                                                 float *accS = nullptr, int slot = -1)
+                                                 float (*buf)[33], bool grouped = false)
 {
     if (kDetail) {
         // (an fp32 instantiation for non-grazing warps measured slower on B200: the
@@ -784,32 +779,9 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
         }
     }
     // own-cell terms: one lane alone issues its atomics, else a transposing warp
-    // reduction then one 9-lane atomic instruction.  With PF_K7_SMEMACC the target is
-    // the CTA's shared accumulator of the cell's tile-list slot (flushed once per
-    // CTA), for the slots below kAccSlots.
+    // reduction then one 9-lane atomic instruction
     float *accc = acc + 12 * (size_t)S.cell[j];
     const unsigned sm = __ballot_sync(0xffffffffu, seg);
-    if (PF_K7_SMEMACC && slot >= 0 && (grouped || __popc(sm) <= PF_K7_DIRECT_MAX)) {
-        if (seg) {
-            float *a = accS + 12 * slot;
-            atomicAdd(a + 0, o.px);
-            atomicAdd(a + 1, o.py);
-            atomicAdd(a + 2, o.pz);
-            atomicAdd(a + 3, o.w);
-            atomicAdd(a + 4, o.r);
-            atomicAdd(a + 5, gs);
-            atomicAdd(a + 6, gR);
-            atomicAdd(a + 7, gG);
-            atomicAdd(a + 8, gB);
-            if (dipole) {
-                atomicAdd(a + 9, o.nx);
-                atomicAdd(a + 10, o.ny);
-                atomicAdd(a + 11, o.nz);
-            }
-        }
-        return;
-    }
-    if (PF_K7_SMEMACC && slot >= 0) accc = accS + 12 * slot;   // single record: uniform slot
     if (grouped || __popc(sm) <= PF_K7_DIRECT_MAX) {   // (a group spans several cells)
         if (seg) {
             atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
@@ -844,18 +816,11 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     __shared__ WarpCtx WC[kWarps];
     __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
     extern __shared__ float dyn_smem[];   // detail variant: [kWarps][32][33] reduction tiles
-    constexpr bool kSmem = PF_K7_SMEMACC && !kDetail;
-    float *accS = dyn_smem;   // kSmem: [kAccSlots][12] own-cell terms per tile-list slot
-    __shared__ uint16_t LS[kSmem ? kWarps : 1][32];      // list slot of each staged record
     const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
     float (*buf)[33] = reinterpret_cast<float (*)[33]>(dyn_smem + (kDetail ? warp * 32 * 33 : 0));
-    if (kSmem) {
-        for (int q = threadIdx.x; q < kAccSlots * 12; q += blockDim.x) accS[q] = 0.0f;
-        __syncthreads();
-    }
     PixelSetup P;
     setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
@@ -929,10 +894,8 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 }
                 const bool seg = g.dt > 0.0f;
                 if (!__any_sync(0xffffffffu, seg)) continue;
-                const int ls = 32 * (int)c + j;
                 segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb,
-                                                   dpl, &X, om, buf, false, accS,
-                                                   (kSmem && ls < kAccSlots) ? ls : -1);
+                                                   dpl, &X, om, buf);
                 if (seg && px.T < kTStop) done = true;
             }
             __syncwarp();
@@ -946,7 +909,6 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
             const uint2 mp = __ldg(reinterpret_cast<const uint2 *>(R0 + (size_t)lane * kRecWords));
             my_mask = mp.x;
             const uint32_t pos = mp.y;
-            if (kSmem) LS[warp][lane] = (uint16_t)min(32u * c + pos, 65535u);
             const uint32_t cell = __ldg(vals + base + pos);
             const float4 A = __ldg(ds.cellA + cell);
             double x0, x1, x2;
@@ -1000,30 +962,11 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
                 }
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
-            const int ls = kSmem ? (int)LS[warp][j] : 0;
             segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb, dpl,
-                                               &X, om, buf, grouped, accS,
-                                               (kSmem && ls < kAccSlots) ? ls : -1);
+                                               &X, om, buf, grouped);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();
-    }
-    if (kSmem) {   // flush the CTA's own-cell sums: one float4 RED per slot quarter
-        __syncthreads();
-        const uint32_t len = rg.y - rg.x;
-        for (uint32_t q = threadIdx.x; q < min(len, (uint32_t)kAccSlots); q += blockDim.x) {
-            const float4 *a = reinterpret_cast<const float4 *>(accS + 12 * q);
-            const float4 a0 = a[0], a1 = a[1], a2 = a[2];
-            const bool n0 = a0.x != 0.0f || a0.y != 0.0f || a0.z != 0.0f || a0.w != 0.0f;
-            const bool n1 = a1.x != 0.0f || a1.y != 0.0f || a1.z != 0.0f || a1.w != 0.0f;
-            const bool n2 = a2.x != 0.0f || a2.y != 0.0f || a2.z != 0.0f || a2.w != 0.0f;
-            if (n0 || n1 || n2) {
-                float4 *dst = reinterpret_cast<float4 *>(acc + 12 * (size_t)__ldg(vals + rg.x + q));
-                if (n0) atomicAdd(dst, a0);
-                if (n1) atomicAdd(dst + 1, a1);
-                if (n2) atomicAdd(dst + 2, a2);
-            }
-        }
     }
 }
 
@@ -1031,8 +974,7 @@ template <bool kDipole, int kDetail>
 static void launch_backward_t(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
-    constexpr int smem = kDetail ? kWarps * 32 * 33 * (int)sizeof(float)
-                                 : (PF_K7_SMEMACC ? kAccSlots * 12 * (int)sizeof(float) : 0);
+    constexpr int smem = kDetail ? kWarps * 32 * 33 * (int)sizeof(float) : 0;
     if (smem)
         cudaFuncSetAttribute(k7_backward<kDipole, kDetail>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
