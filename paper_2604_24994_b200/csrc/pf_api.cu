@@ -468,6 +468,7 @@ int pf_destroy(pf_scene *s)
         s->bvh = nullptr;
     }
     s->trace_stats.release();
+    s->trace_nodes.release();
     s->cellA.release();
     s->cellB.release();
     s->cellE.release();
@@ -692,6 +693,7 @@ int pf_trace_forward(pf_scene *s, const pf_camera *cams, int32_t V, float *out, 
     }
     if (!stat || !s->bvh_built) {
         PF_CUDA(pf::build_ball_bvh(s, *s->bvh, s->ds.N, s->ds.sites, s->ds.radii, st));
+        PF_CUDA(pf::pack_trace_nodes(s, *s->bvh, s->trace_nodes, st));
         s->bvh_built = true;
     }
     PF_CUDA(s->trace_stats.reserve(8 * 8));

@@ -137,7 +137,7 @@ struct pf_scene {
     // NEXT-4 tracer: the ball BVH (built per call; once for PF_STATIC_SCENE) and stats
     pf::BallBVH *bvh = nullptr;
     bool bvh_built = false;
-    pf::DevBuf trace_stats;
+    pf::DevBuf trace_stats, trace_nodes;   // stats; BVH nodes in the tracer's layout
 };
 
 namespace pf {
@@ -173,6 +173,7 @@ cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *count
                            uint32_t *rec_used, float *st_contrib, float *st_normal,
                            cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
+cudaError_t pack_trace_nodes(pf_scene *s, BallBVH &bvh, DevBuf &nodes, cudaStream_t st);
 cudaError_t launch_trace(pf_scene *s, const BallBVH &bvh, const CamParams &cam, float *out,
                          unsigned long long *stats, cudaStream_t st);
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,

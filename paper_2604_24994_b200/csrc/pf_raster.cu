@@ -466,6 +466,21 @@ __device__ __forceinline__ void sv_units(const float2 s[kMaxDetail], int K, doub
     }
 }
 
+// one unit vector (q - s)/|q - s| (as sv_units for one site)
+template <typename T>
+__device__ __forceinline__ void sv_unit(const float2 sk, double q0, double q1, T &ux, T &uy)
+{
+    ux = uy = (T)0;
+    const T dx = (T)(q0 - (double)sk.x), dy = (T)(q1 - (double)sk.y);
+    const T r2 = dx * dx + dy * dy;
+    if (r2 > (T)0) {
+        T ri = (T)rsqrtf((float)r2);
+        if (sizeof(T) == 8) ri = ri * ((T)1.5 - (T)0.5 * r2 * ri * ri);
+        ux = dx * ri;
+        uy = dy * ri;
+    }
+}
+
 struct BwdPixel {
     float T, Cr, Cg, Cb;
     float4 fin, G;
@@ -481,16 +496,18 @@ template <typename T, int KT>
 __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg,
                                             const WarpStage &S, int j, BwdPixel &px,
                                             const DeviceScene &ds, float *acc, int lane,
-                                            const DetailCtx &X, const float *om, float (*buf)[33])
+                                            const DetailCtx &X, const float *om, float (*buf)[33],
+                                            float (*gbuf)[25])
 {
     const int K = KT == 8 ? 8 : ds.K;   // K == 8 (the paper's setting) known at compile time
     const uint32_t cell = S.cell[j];
     const float tau = ds.sv_tau;
     OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
     float gs = 0.0f;
-    float guv[2 * kMaxDetail], gdisp[kMaxDetail];
-#pragma unroll
-    for (int k = 0; k < kMaxDetail; ++k) guv[2 * k] = guv[2 * k + 1] = gdisp[k] = 0.0f;
+    // dL/ds_k (2K) and dL/dd_k (K) of this lane's segment go straight to its row of the
+    // warp's gbuf tile (column sums below): no per-lane register arrays for them, and
+    // the per-site unit vectors, weights and displacements are recomputed / re-read per
+    // k instead of held in fp64 arrays (register pressure: 2 CTAs/SM)
     if (seg) {
         const double *F = ds.cellF + (size_t)kCellF * cell;
         const double m0 = __ldg(F), m1 = __ldg(F + 1), m2 = __ldg(F + 2);
@@ -569,28 +586,31 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
         const T tm0 = (T)m0, tm1 = (T)m1, tm2 = (T)m2, tu0 = (T)u0, tu1 = (T)u1, tu2 = (T)u2;
         const T tv0 = (T)v0, tv1 = (T)v1, tv2 = (T)v2, td0 = (T)d0, td1 = (T)d1, td2 = (T)d2;
         const T tA = (T)X.G.A, ttau = (T)tau;
-        T w[kMaxDetail], ux[kMaxDetail], uy[kMaxDetail];
         T wsum = 0, sw = 0;
 #pragma unroll
         for (int k = 0; k < kMaxDetail; ++k) {
-            w[k] = (T)ws[k];
-            wsum += w[k];
-            sw += w[k] * (T)dG[k];
+            wsum += (T)ws[k];
+            sw += (T)ws[k] * (T)dG[k];
         }
         const T iwsum = (T)1 / wsum;
         sw *= iwsum;   // renormalised: sum_k w_k (dG_k - sw) = 0 to working-precision rounding
-        sv_units<T>(st, K, qs0, qs1, ux, uy);
         T gq0 = 0, gq1 = 0;
         const T cq = -ttau * (T)wa * iwsum;
 #pragma unroll
         for (int k = 0; k < kMaxDetail; ++k) {
+            float gx = 0.0f, gy = 0.0f;
             if (k < K) {
-                const T grho = cq * w[k] * ((T)dG[k] - sw);
-                gq0 += grho * ux[k];
-                gq1 += grho * uy[k];
-                guv[2 * k] -= (float)(grho * ux[k]);
-                guv[2 * k + 1] -= (float)(grho * uy[k]);
+                T ux, uy;
+                sv_unit<T>(__ldg(uv + k), qs0, qs1, ux, uy);
+                const T grho = cq * (T)ws[k] * ((T)dG[k] - sw);
+                gq0 += grho * ux;
+                gq1 += grho * uy;
+                gx = -(float)(grho * ux);
+                gy = -(float)(grho * uy);
             }
+            gbuf[lane][2 * k] = gx;
+            gbuf[lane][2 * k + 1] = gy;
+            gbuf[lane][16 + k] = 0.0f;
         }
         T gm0 = 0, gm1 = 0, gm2 = 0, gc0 = 0, gc1 = 0, gc2 = 0;
         T gu0 = 0, gu1 = 0, gu2 = 0, gv0 = 0, gv1 = 0, gv2 = 0;
@@ -624,15 +644,12 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             const double qb0 = __fma_rn(y0, u0, __fma_rn(y1, u1, __dmul_rn(y2, u2)));
             const double qb1 = __fma_rn(y0, v0, __fma_rn(y1, v1, __dmul_rn(y2, v2)));
             const float *wb = X.G.w;   // detail_plane's weights at x_bar
-            sv_units<T>(st, K, qb0, qb1, ux, uy);
             const float *dk = ds.ddisp + (size_t)K * cell;
-            T dr = 0, bsum = 0, dv[kMaxDetail];
+            T dr = 0, bsum = 0;
 #pragma unroll
             for (int k = 0; k < kMaxDetail; ++k) {
-                w[k] = (T)wb[k];
-                bsum += w[k];
-                dv[k] = k < K ? (T)__ldg(dk + k) : (T)0;
-                dr += w[k] * dv[k];
+                bsum += (T)wb[k];
+                if (k < K) dr += (T)wb[k] * (T)__ldg(dk + k);
             }
             const T ibsum = (T)1 / bsum;
             dr *= ibsum;
@@ -640,13 +657,15 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
 #pragma unroll
             for (int k = 0; k < kMaxDetail; ++k) {
                 if (k < K) {
-                    const T wk = w[k] * ibsum;
-                    gdisp[k] = (float)(wk * gdr);
-                    const T grho = -ttau * wk * gdr * (dv[k] - dr);
-                    gb0 += grho * ux[k];
-                    gb1 += grho * uy[k];
-                    guv[2 * k] -= (float)(grho * ux[k]);
-                    guv[2 * k + 1] -= (float)(grho * uy[k]);
+                    T ux, uy;
+                    sv_unit<T>(__ldg(uv + k), qb0, qb1, ux, uy);
+                    const T wk = (T)wb[k] * ibsum;
+                    gbuf[lane][16 + k] = (float)(wk * gdr);
+                    const T grho = -ttau * wk * gdr * ((T)__ldg(dk + k) - dr);
+                    gb0 += grho * ux;
+                    gb1 += grho * uy;
+                    gbuf[lane][2 * k] -= (float)(grho * ux);
+                    gbuf[lane][2 * k + 1] -= (float)(grho * uy);
                 }
             }
             const T b0 = (T)y0, b1 = (T)y1, b2 = (T)y2;
@@ -701,17 +720,9 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             atomicAdd(dst + 2, make_float2(accv[4], accv[5]));
         }
     }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kMaxDetail; ++k) {
-        buf[lane][2 * k] = guv[2 * k];
-        buf[lane][2 * k + 1] = guv[2 * k + 1];
-        buf[lane][16 + k] = gdisp[k];
-    }
-    __syncwarp();
     if (lane < 24) {
         float t = 0.0f;
-        for (unsigned mm = segm; mm; mm &= mm - 1) t += buf[__ffs(mm) - 1][lane];
+        for (unsigned mm = segm; mm; mm &= mm - 1) t += gbuf[__ffs(mm) - 1][lane];
         if (lane < 16) {
             if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cell + lane, t);
         } else if (lane - 16 < K && ds.g_disp) {
@@ -745,7 +756,8 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
     if (kDetail) {
         // (an fp32 instantiation for non-grazing warps measured slower on B200: the
         // fp64 -> fp32 conversions cost more than the fp64 arithmetic they save)
-        detail_segment<double, kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, buf);
+        detail_segment<double, kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, buf,
+                                        reinterpret_cast<float (*)[25]>(&buf[32][0]));
         return;
     }
     constexpr bool dipole = kDipole;
@@ -820,7 +832,9 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
-    float (*buf)[33] = reinterpret_cast<float (*)[33]>(dyn_smem + (kDetail ? warp * 32 * 33 : 0));
+    // detail: per warp a [32][33] outer-product tile followed by a [32][25] tile of
+    // the per-lane site / displacement gradients
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(dyn_smem + (kDetail ? warp * 32 * 58 : 0));
     PixelSetup P;
     setup_pixel(cam, tile, P, PR, W);
     const uint2 rg = ranges[tile];
@@ -974,7 +988,7 @@ template <bool kDipole, int kDetail>
 static void launch_backward_t(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
 {
     const int T = v.cam.tiles_x * v.cam.tiles_y;
-    constexpr int smem = kDetail ? kWarps * 32 * 33 * (int)sizeof(float) : 0;
+    constexpr int smem = kDetail ? kWarps * 32 * 58 * (int)sizeof(float) : 0;
     if (smem)
         cudaFuncSetAttribute(k7_backward<kDipole, kDetail>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
