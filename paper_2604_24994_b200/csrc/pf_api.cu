@@ -121,6 +121,48 @@ pf::BatchViews batch_views(pf::ViewState *views, int b0, int b1)
     return bv;
 }
 
+pf::ViewArgs view_args(pf::ViewState &vs, float *out, const float *grad_out, bool record)
+{
+    pf::ViewArgs a;
+    memset(&a, 0, sizeof(a));
+    a.cam = vs.cam;
+    a.ranges = vs.ranges_p;
+    a.order = vs.order;
+    a.vals = vs.vals_p;
+    a.chunk_off = vs.chunk_off;
+    a.out = (float4 *)out;
+    a.saved = record ? vs.saved.as<float4>() : nullptr;
+    a.grad_out = (const float4 *)grad_out;
+    a.desc = record ? vs.desc.as<uint2>() : nullptr;
+    a.wdone = record ? vs.wdone.as<uint32_t>() : nullptr;
+    a.rec = record ? vs.rec.as<uint32_t>() : nullptr;
+    a.rec_cap = (uint32_t)vs.rec_cap;
+    return a;
+}
+
+// The ViewArgs of a fused K6 / K7 launch: staged in pinned memory (slot 0 forward,
+// slot 1 backward; every reuse of a slot follows a host sync of the call that used
+// it) and copied to the handle's device array on the call's stream.
+int upload_view_args(pf_scene *s, const pf::ViewArgs *a, int V, int slot, cudaStream_t st,
+                     const pf::ViewArgs **dev)
+{
+    const int per = V + 8;
+    if (s->pinned_args_n < per) {
+        if (s->pinned_args) cudaFreeHost(s->pinned_args);
+        s->pinned_args = nullptr;
+        s->pinned_args_n = 0;
+        PF_CUDA(cudaMallocHost(&s->pinned_args, sizeof(pf::ViewArgs) * 2 * (size_t)per));
+        s->pinned_args_n = per;
+    }
+    PF_CUDA(s->vargs.reserve(sizeof(pf::ViewArgs) * 2 * (size_t)s->pinned_args_n));
+    pf::ViewArgs *h = s->pinned_args + (size_t)slot * s->pinned_args_n;
+    memcpy(h, a, sizeof(pf::ViewArgs) * (size_t)V);
+    pf::ViewArgs *d = s->vargs.as<pf::ViewArgs>() + (size_t)slot * s->pinned_args_n;
+    PF_CUDA(cudaMemcpyAsync(d, h, sizeof(pf::ViewArgs) * (size_t)V, cudaMemcpyHostToDevice, st));
+    *dev = d;
+    return PF_OK;
+}
+
 // Sorting and ranges for views [0, V) of this call (K1 and the visible-cell
 // counts ran, every v.P is known), in batches of up to kBatchViews views:
 //   K2: compact the visible cells of the batch (view-major, cell order);
@@ -506,6 +548,8 @@ int pf_destroy(pf_scene *s)
     s->rec_used.release();
     if (s->pinned) cudaFreeHost(s->pinned);
     if (s->pinned_rec) cudaFreeHost(s->pinned_rec);
+    if (s->pinned_args) cudaFreeHost(s->pinned_args);
+    s->vargs.release();
     for (auto &e : s->events) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -587,6 +631,7 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
     rc = emit_sort_ranges(s, s->views.data(), V, st, &ks_all);
     if (rc) return rc;
     if (k0_side) PF_CUDA(cudaStreamWaitEvent(st, s->side_join, 0));
+    s->host_args.resize(V);
     for (int v = 0; v < V; ++v) {
         pf::ViewState &vs = s->views[v];
         uint32_t *used = nullptr;
@@ -601,7 +646,15 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
             PF_CUDA(vs.rec.reserve(72 * (size_t)vs.rec_cap));
             used = s->rec_used.as<uint32_t>() + v;
         }
-        PF_CUDA(pf::launch_forward(s, vs, out + 4 * npix * (size_t)v, nullptr, used,
+        pf::ViewArgs a = view_args(vs, out + 4 * npix * (size_t)v, nullptr, record);
+        a.rec_used = used;
+        s->host_args[v] = a;
+    }
+    {   // K6 of every view in one launch
+        const pf::ViewArgs *dargs = nullptr;
+        rc = upload_view_args(s, s->host_args.data(), V, 0, st, &dargs);
+        if (rc) return rc;
+        PF_CUDA(pf::launch_forward(s, s->views.data(), V, dargs, nullptr, record,
                                    ex ? ex->contrib : nullptr, ex ? ex->normal_term : nullptr, st));
     }
     if (record) {
@@ -655,10 +708,13 @@ int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const f
     s->ds.g_disp = g->detail_disp;
     s->ds.g_sv = g->detail_sv;
     int brc = PF_OK;
-    for (int v = 0; v < V && brc == PF_OK; ++v) {
-        pf::ViewState &vs = s->views[v];
-        if (vs.P == 0) continue;
-        cudaError_t e = pf::launch_backward(s, vs, grad_out + 4 * npix * (size_t)v, st);
+    s->host_args.resize(V);
+    for (int v = 0; v < V; ++v)
+        s->host_args[v] = view_args(s->views[v], nullptr, grad_out + 4 * npix * (size_t)v, true);
+    const pf::ViewArgs *dargs = nullptr;
+    brc = upload_view_args(s, s->host_args.data(), V, 1, st, &dargs);
+    if (brc == PF_OK) {   // K7 of every view in one launch
+        cudaError_t e = pf::launch_backward(s, s->views.data(), V, dargs, st);
         if (e != cudaSuccess) brc = cuda_fail(e, "K7");
     }
     s->ds.g_uv = s->ds.g_disp = s->ds.g_sv = nullptr;
@@ -771,7 +827,11 @@ int pf_debug_counters(pf_scene *s, const pf_camera *cam, int64_t *counters, pf_s
     rc = emit_sort_ranges(s, &vs, 1, st, &ks);
     if (rc) return rc;
     PF_CUDA(cudaMemsetAsync(counters, 0, 32 * (size_t)cam->width * cam->height, st));
-    PF_CUDA(pf::launch_forward(s, vs, nullptr, counters, nullptr, nullptr, nullptr, st));
+    s->host_args.assign(1, view_args(vs, nullptr, nullptr, false));
+    const pf::ViewArgs *dargs = nullptr;
+    rc = upload_view_args(s, s->host_args.data(), 1, 0, st, &dargs);
+    if (rc) return rc;
+    PF_CUDA(pf::launch_forward(s, &vs, 1, dargs, counters, false, nullptr, nullptr, st));
     PF_CUDA(cudaStreamSynchronize(st));
     return PF_OK;
 }

@@ -84,6 +84,19 @@ struct ViewState {
 
 struct BallBVH;   // pf_bvh.cuh
 
+// Per-view arguments of the fused multi-view K6 / K7 launches (a device array,
+// one entry per view; CTA b works on view b / T, tile order[b % T]).
+struct ViewArgs {
+    CamParams cam;
+    const uint2 *ranges;
+    const uint32_t *order, *vals, *chunk_off;
+    float4 *out, *saved;
+    const float4 *grad_out;
+    uint2 *desc;
+    uint32_t *wdone, *rec, *rec_used;
+    uint32_t rec_cap, pad_;
+};
+
 // one sort batch of up to kBatchViews views (kernel parameter of the binning)
 constexpr int kBatchViews = 8;
 struct BatchViews {
@@ -138,6 +151,13 @@ struct pf_scene {
     pf::BallBVH *bvh = nullptr;
     bool bvh_built = false;
     pf::DevBuf trace_stats, trace_nodes;   // stats; BVH nodes in the tracer's layout
+    pf::DevBuf vargs;               // ViewArgs of the fused K6 / K7 launches
+    pf::ViewArgs *pinned_args = nullptr;
+    std::vector<pf::ViewArgs> host_args;
+    int pinned_args_n = 0;
+    int cull_on = -1;               // PF_PLANE_CULL (debug knob), read once per handle
+    bool attrs_k6 = false, attrs_k7 = false;   // dynamic shared-memory attributes set
+    int k6_per_view = -1;           // PF_K6_PER_VIEW (A/B knob): one K6 launch per view
 };
 
 namespace pf {
@@ -169,10 +189,13 @@ cudaError_t launch_ranges(pf_scene *s, const uint32_t *keys, int64_t P, int T, i
                           uint2 *ranges_all, int V, cudaStream_t st);
 cudaError_t launch_tile_order(pf_scene *s, const uint2 *ranges_all, int T, int V,
                               uint32_t *order_all, uint32_t *chunk_off_all, cudaStream_t st);
-cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           uint32_t *rec_used, float *st_contrib, float *st_normal,
+// K6 over views [0, V) in ONE launch (args: the views' ViewArgs, device); counters
+// (debug counting build) only with V == 1
+cudaError_t launch_forward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                           int64_t *counters, bool record, float *st_contrib, float *st_normal,
                            cudaStream_t st);
-cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st);
+cudaError_t launch_backward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                            cudaStream_t st);
 cudaError_t pack_trace_nodes(pf_scene *s, BallBVH &bvh, DevBuf &nodes, cudaStream_t st);
 cudaError_t launch_trace(pf_scene *s, const BallBVH &bvh, const CamParams &cam, float *out,
                          unsigned long long *stats, cudaStream_t st);

@@ -357,6 +357,16 @@ __device__ __forceinline__ void composite_step(float sig, float dt, float cr, fl
     T = __fmul_rn(T, ex);
 }
 
+// the ViewArgs of this CTA's view into shared memory (fused multi-view launches)
+__device__ __forceinline__ void load_view_args(const ViewArgs *__restrict__ va, int T, ViewArgs &VA)
+{
+    static_assert(sizeof(ViewArgs) % 4 == 0 && sizeof(ViewArgs) <= 4 * 256, "ViewArgs");
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(va + blockIdx.x / (unsigned)T);
+    if (threadIdx.x < sizeof(ViewArgs) / 4)
+        reinterpret_cast<uint32_t *>(&VA)[threadIdx.x] = __ldg(src + threadIdx.x);
+    __syncthreads();
+}
+
 struct PixelSetup {
     int x, y;
     bool in_image;   // inside the W x H image (gets an output)

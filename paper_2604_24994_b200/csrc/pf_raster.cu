@@ -44,25 +44,41 @@ namespace pf {
 #ifndef PF_K7_GROUP   // K7: up to this many consecutive disjoint-mask records per pass
 #define PF_K7_GROUP 4
 #endif
+constexpr int kFuseTiles = 4096;   // views with fewer tiles: one fused K6 / K7 launch
 #ifndef PF_K7D_MINB
-#define PF_K7D_MINB 1
+#define PF_K7D_MINB 2
 #endif
 #ifndef PF_K6D_MINB
 #define PF_K6D_MINB 3
 #endif
 // kWide: the non-recording launch for wide-cone (fisheye) views, at 4 CTAs/SM
 // (measured: 5 CTAs/SM is faster for pinhole views, slower for fisheye ones)
-template <bool kCount, bool kRecord, bool kDipole, int kDetail, bool kWide = false>
+// kFused: all views of the call in one launch, this CTA's ViewArgs read from the
+// device array into shared memory (small views: no per-view launch tails); else
+// one launch per view with its ViewArgs by value (constant-bank operands; measured
+// faster for 1080p views, whose launches are ~14 waves long)
+template <bool kCount, bool kRecord, bool kDipole, int kDetail, bool kWide = false,
+          bool kFused = false>
 __global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB
                                                : (kRecord || kWide ? PF_K6_MINB : PF_K6I_MINB))
-k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
-           const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
-           float4 *__restrict__ out, float4 *__restrict__ saved, long long *__restrict__ counters,
-           const uint32_t *__restrict__ chunk_off, uint2 *__restrict__ desc,
-           uint32_t *__restrict__ wdone, uint32_t *__restrict__ rec, uint32_t *__restrict__ rec_used,
-           uint32_t rec_cap, float *__restrict__ st_contrib, float *__restrict__ st_normal,
-           int cull_on)
+k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, int ntiles,
+           long long *__restrict__ counters, float *__restrict__ st_contrib,
+           float *__restrict__ st_normal, int cull_on)
 {
+    __shared__ ViewArgs VAs[kFused ? 1 : 1];
+    if (kFused) load_view_args(va, ntiles, VAs[0]);
+    const ViewArgs &VA = kFused ? VAs[0] : one;
+    const CamParams &cam = VA.cam;
+    const uint2 *__restrict__ ranges = VA.ranges;
+    const uint32_t *__restrict__ vals = VA.vals;
+    float4 *__restrict__ out = VA.out;
+    float4 *__restrict__ saved = VA.saved;
+    const uint32_t *__restrict__ chunk_off = VA.chunk_off;
+    uint2 *__restrict__ desc = VA.desc;
+    uint32_t *__restrict__ wdone = VA.wdone;
+    uint32_t *__restrict__ rec = VA.rec;
+    uint32_t *__restrict__ rec_used = VA.rec_used;
+    const uint32_t rec_cap = VA.rec_cap;
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
@@ -72,7 +88,8 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
     // so its X_p stays the SURVEY 8(d) work count
     constexpr bool kCull = PF_K6_PCULL && !kCount;
     extern __shared__ PlaneBuf PB[];   // kWarps entries when kCull (dynamic: static smem is full)
-    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = (int)VA.order[kFused ? blockIdx.x % ntiles : blockIdx.x], lane = threadIdx.x & 31,
+              warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
@@ -223,56 +240,90 @@ k6_forward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
 }
 
 template <bool kDipole, int kDetail>
-static void launch_forward_t(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                             uint32_t *rec_used, float *stc, float *stn, cudaStream_t st)
+static void launch_forward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                             int64_t *counters, bool record, float *stc, float *stn,
+                             cudaStream_t st)
 {
-    const int T = v.cam.tiles_x * v.cam.tiles_y;
+    const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     // the plane-cull buffers are dynamic shared memory (static + dynamic may pass 48 KB)
     const size_t dyn = PF_K6_PCULL ? kWarps * sizeof(PlaneBuf) : 0;
-    const char *e = getenv("PF_PLANE_CULL");   // debug knob: 0 clips by every list plane
-    const bool wide = v.cam.model == PF_FISHEYE;
-    const int cull = (e && e[0] == '0') ? 0 : 1;
-    if (dyn) {   // per call: the attribute is per device
+    if (s->cull_on < 0) {   // debug knob, read once per handle: 0 clips by every list plane
+        const char *e = getenv("PF_PLANE_CULL");
+        s->cull_on = (e && e[0] == '0') ? 0 : 1;
+    }
+    bool wide = false;
+    for (int v = 0; v < V; ++v) wide = wide || views[v].cam.model == PF_FISHEYE;
+    if (dyn && !s->attrs_k6) {   // once per handle (the attribute is per device)
         cudaFuncSetAttribute(k6_forward<false, true, kDipole, kDetail>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         cudaFuncSetAttribute(k6_forward<false, false, kDipole, kDetail>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k6_forward<false, true, kDipole, kDetail, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k6_forward<false, false, kDipole, kDetail, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if constexpr (!kDetail) {
+            cudaFuncSetAttribute(k6_forward<false, false, kDipole, kDetail, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            cudaFuncSetAttribute(k6_forward<false, false, kDipole, kDetail, true, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        }
     }
-    if (counters)
-        k6_forward<true, false, kDipole, kDetail><<<T, 256, 0, st>>>(
-            s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
-            (float4 *)out, nullptr, (long long *)counters, nullptr, nullptr, nullptr, nullptr,
-            nullptr, 0u, nullptr, nullptr, 0);
-    else if (rec_used)
-        k6_forward<false, true, kDipole, kDetail><<<T, 256, dyn, st>>>(
-            s->ds, v.cam, v.ranges_p, v.order, v.vals_p,
-            (float4 *)out, v.saved.as<float4>(), nullptr, v.chunk_off,
-            v.desc.as<uint2>(), v.wdone.as<uint32_t>(), v.rec.as<uint32_t>(), rec_used,
-            (uint32_t)v.rec_cap, stc, stn, cull);
-    else {
-        auto kern = k6_forward<false, false, kDipole, kDetail>;
-        if constexpr (!kDetail)
-            if (wide) kern = k6_forward<false, false, kDipole, kDetail, true>;
-        kern<<<T, 256, dyn, st>>>(s->ds, v.cam, v.ranges_p, v.order, v.vals_p, (float4 *)out,
-                                  nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                  0u, stc, stn, cull);
+    s->attrs_k6 = true;
+    // fused for small views (few waves per launch), per view otherwise (PF_K6_PER_VIEW=1
+    // forces per-view launches, =0 the fused one; A/B knob)
+    if (s->k6_per_view < 0) {
+        const char *e = getenv("PF_K6_PER_VIEW");
+        s->k6_per_view = e ? (e[0] == '1' ? 1 : 0) : 2;
+    }
+    const bool fused = s->k6_per_view == 0 || (s->k6_per_view == 2 && T < kFuseTiles);
+    const ViewArgs *h = s->host_args.data();
+    if (fused) {
+        const unsigned grid = (unsigned)(T * V);
+        if (counters)
+            k6_forward<true, false, kDipole, kDetail, false, true><<<grid, 256, 0, st>>>(
+                s->ds, h[0], args, T, (long long *)counters, nullptr, nullptr, 0);
+        else if (record)
+            k6_forward<false, true, kDipole, kDetail, false, true><<<grid, 256, dyn, st>>>(
+                s->ds, h[0], args, T, nullptr, stc, stn, s->cull_on);
+        else {
+            auto kern = k6_forward<false, false, kDipole, kDetail, false, true>;
+            if constexpr (!kDetail)
+                if (wide) kern = k6_forward<false, false, kDipole, kDetail, true, true>;
+            kern<<<grid, 256, dyn, st>>>(s->ds, h[0], args, T, nullptr, stc, stn, s->cull_on);
+        }
+        return;
+    }
+    for (int v = 0; v < V; ++v) {
+        if (counters)
+            k6_forward<true, false, kDipole, kDetail><<<T, 256, 0, st>>>(
+                s->ds, h[v], nullptr, T, (long long *)counters, nullptr, nullptr, 0);
+        else if (record)
+            k6_forward<false, true, kDipole, kDetail><<<T, 256, dyn, st>>>(
+                s->ds, h[v], nullptr, T, nullptr, stc, stn, s->cull_on);
+        else {
+            auto kern = k6_forward<false, false, kDipole, kDetail>;
+            if constexpr (!kDetail)
+                if (wide) kern = k6_forward<false, false, kDipole, kDetail, true>;
+            kern<<<T, 256, dyn, st>>>(s->ds, h[v], nullptr, T, nullptr, stc, stn, s->cull_on);
+        }
     }
 }
 
-cudaError_t launch_forward(pf_scene *s, ViewState &v, float *out, int64_t *counters,
-                           uint32_t *rec_used, float *st_contrib, float *st_normal,
+cudaError_t launch_forward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                           int64_t *counters, bool record, float *st_contrib, float *st_normal,
                            cudaStream_t st)
 {
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
     if (s->ds.K == 8)
-        launch_forward_t<true, 8>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<true, 8>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     else if (s->ds.K)
-        launch_forward_t<true, 1>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<true, 1>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     else if (s->ds.cellN)
-        launch_forward_t<true, 0>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<true, 0>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     else
-        launch_forward_t<false, 0>(s, v, out, counters, rec_used, st_contrib, st_normal, st);
+        launch_forward_t<false, 0>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     ++s->launches;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();
@@ -814,21 +865,30 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
 
 }  // namespace
 
-template <bool kDipole, int kDetail>
+template <bool kDipole, int kDetail, bool kFused = false>
 __global__ void __launch_bounds__(256, kDetail ? PF_K7D_MINB : PF_K7_MINB)
-k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
-            const uint32_t *__restrict__ order, const uint32_t *__restrict__ vals,
-            const float4 *__restrict__ saved, const float4 *__restrict__ grad_out,
-            float *__restrict__ acc, const uint32_t *__restrict__ chunk_off,
-            const uint2 *__restrict__ desc, const uint32_t *__restrict__ wdone,
-            const uint32_t *__restrict__ rec)
+k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, int ntiles,
+            float *__restrict__ acc)
 {
+    __shared__ ViewArgs VAs[1];
+    if (kFused) load_view_args(va, ntiles, VAs[0]);
+    const ViewArgs &VA = kFused ? VAs[0] : one;
+    const CamParams &cam = VA.cam;
+    const uint2 *__restrict__ ranges = VA.ranges;
+    const uint32_t *__restrict__ vals = VA.vals;
+    const float4 *__restrict__ saved = VA.saved;
+    const float4 *__restrict__ grad_out = VA.grad_out;
+    const uint32_t *__restrict__ chunk_off = VA.chunk_off;
+    const uint2 *__restrict__ desc = VA.desc;
+    const uint32_t *__restrict__ wdone = VA.wdone;
+    const uint32_t *__restrict__ rec = VA.rec;
     __shared__ WarpStage WS[kWarps];
     __shared__ PixelRays PR;
     __shared__ WarpCtx WC[kWarps];
     __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
     extern __shared__ float dyn_smem[];   // detail variant: [kWarps][32][33] reduction tiles
-    const int tile = (int)order[blockIdx.x], lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = (int)VA.order[kFused ? blockIdx.x % ntiles : blockIdx.x], lane = threadIdx.x & 31,
+              warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
     WarpCtx &W = WC[warp];
@@ -985,31 +1045,45 @@ k7_backward(DeviceScene ds, CamParams cam, const uint2 *__restrict__ ranges,
 }
 
 template <bool kDipole, int kDetail>
-static void launch_backward_t(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
+static void launch_backward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                              cudaStream_t st)
 {
-    const int T = v.cam.tiles_x * v.cam.tiles_y;
+    const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     constexpr int smem = kDetail ? kWarps * 32 * 58 * (int)sizeof(float) : 0;
-    if (smem)
+    if (smem && !s->attrs_k7) {
         cudaFuncSetAttribute(k7_backward<kDipole, kDetail>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k7_backward<kDipole, kDetail><<<T, 256, smem, st>>>(
-        s->ds, v.cam, v.ranges_p, v.order, v.vals_p, v.saved.as<float4>(),
-        (const float4 *)grad_out, s->acc.as<float>(), v.chunk_off, v.desc.as<uint2>(),
-        v.wdone.as<uint32_t>(), v.rec.as<uint32_t>());
+        cudaFuncSetAttribute(k7_backward<kDipole, kDetail, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
+    s->attrs_k7 = true;
+    const ViewArgs *h = s->host_args.data();
+    const bool fused = s->k6_per_view == 0 || (s->k6_per_view != 1 && T < kFuseTiles);
+    if (fused) {
+        k7_backward<kDipole, kDetail, true><<<(unsigned)(T * V), 256, smem, st>>>(
+            s->ds, h[0], args, T, s->acc.as<float>());
+        return;
+    }
+    for (int v = 0; v < V; ++v) {
+        if (views[v].P == 0) continue;
+        k7_backward<kDipole, kDetail><<<T, 256, smem, st>>>(s->ds, h[v], nullptr, T,
+                                                            s->acc.as<float>());
+    }
 }
 
-cudaError_t launch_backward(pf_scene *s, ViewState &v, const float *grad_out, cudaStream_t st)
+cudaError_t launch_backward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                            cudaStream_t st)
 {
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
     if (s->ds.K == 8)
-        launch_backward_t<true, 8>(s, v, grad_out, st);
+        launch_backward_t<true, 8>(s, views, V, args, st);
     else if (s->ds.K)
-        launch_backward_t<true, 1>(s, v, grad_out, st);
+        launch_backward_t<true, 1>(s, views, V, args, st);
     else if (s->ds.cellN)
-        launch_backward_t<true, 0>(s, v, grad_out, st);
+        launch_backward_t<true, 0>(s, views, V, args, st);
     else
-        launch_backward_t<false, 0>(s, v, grad_out, st);
+        launch_backward_t<false, 0>(s, views, V, args, st);
     ++s->launches;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();

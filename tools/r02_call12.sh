@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+VARIANTS="build/base.so default" bash tools/ab.sh
+cp gpurun_out/ab.log gpurun_out/ab_fused.log
+VARIANTS="default" BENCH_ARGS="--workload nerfsynth200k" bash tools/ab.sh
+cp gpurun_out/ab.log gpurun_out/ab_nerf.log
