@@ -41,6 +41,9 @@ namespace pf {
 #ifndef PF_K7_DIRECT_MAX   // up to this many segment lanes: per-lane atomics, no warp reduction
 #define PF_K7_DIRECT_MAX 10
 #endif
+#ifndef PF_K7_PREFETCH   // K7: L2 prefetch of the next chunk's K6 records
+#define PF_K7_PREFETCH 1
+#endif
 #ifndef PF_K7_GROUP   // K7: up to this many consecutive disjoint-mask records per pass
 #define PF_K7_GROUP 4
 #endif
@@ -937,8 +940,22 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
     constexpr bool kGroup = !kDetail && PF_K7_GROUP > 1;   // detail: warp-level per-cell reductions
     const uint32_t nchunks = wdone[(size_t)tile * kWarps + warp];
     const uint32_t c0 = chunk_off[tile];
+    uint2 dnext = nchunks ? desc[(size_t)c0 * kWarps + warp] : make_uint2(0u, 0u);
     for (uint32_t c = 0; c < nchunks; ++c) {
-        const uint2 d = desc[(size_t)(c0 + c) * kWarps + warp];
+        const uint2 d = dnext;
+        if (PF_K7_PREFETCH && c + 1 < nchunks) {
+            // the next chunk's descriptor now, and its record block pulled into L2 while
+            // this chunk is replayed (records were written by K6 long before: DRAM)
+            dnext = desc[(size_t)(c0 + c + 1) * kWarps + warp];
+            if (dnext.y != 0u && dnext.y != kOverflow) {
+                const char *rb = reinterpret_cast<const char *>(rec + (size_t)dnext.x * kRecWords);
+                const uint32_t bytes = dnext.y * (uint32_t)(4 * kRecWords);
+                for (uint32_t o = (uint32_t)lane * 128u; o < bytes; o += 32u * 128u)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + o));
+            }
+        } else if (c + 1 < nchunks) {
+            dnext = desc[(size_t)(c0 + c + 1) * kWarps + warp];
+        }
         if (d.y == 0u) continue;
         const uint32_t base = rg.x + 32u * c;
         if (d.y == kOverflow) {
