@@ -361,6 +361,13 @@ def _free_port():
     return port
 
 
+def share_gpu():
+    """Test-only knob (PF_BENCH_SHARE_GPU=1): every rank on cuda:0 with the gloo
+    backend, so the N-rank path of this script (self-launch, view deal, all-reduce
+    timing, whole-job FPS) can be exercised on a one-GPU box.  Never a bench number."""
+    return os.environ.get("PF_BENCH_SHARE_GPU") == "1"
+
+
 def self_launch(args):
     """`--gpus N` outside torchrun: re-exec under torch.distributed.run with N ranks
     (one per GPU, rendezvous on 127.0.0.1).  Fails loudly if fewer than N GPUs are
@@ -374,7 +381,7 @@ def self_launch(args):
         return
     import torch
     n = torch.cuda.device_count()
-    if n < args.gpus:
+    if n < args.gpus and not share_gpu():
         raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
                          f"found {n}")
     env = dict(os.environ)
@@ -400,12 +407,17 @@ def main():
     import pf_synth
 
     ws, rank, local = dist_env()
+    if share_gpu():
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if share_gpu():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def red(x, op):
         if ws == 1:
@@ -743,6 +755,8 @@ def main():
             "dtype": "f32", "data": "synthetic (pf_synth seeded generator, random-init foam)",
             "config": make_config(args, sc, W, H, total, ws),
             "views_this_rank": nv, "allreduce": allreduce, "weak_scaling": weak,
+            **({"shared_gpu_test": "PF_BENCH_SHARE_GPU=1: all ranks on cuda:0 over gloo "
+                                   "(path test, not a measurement)"} if share_gpu() else {}),
             "clocks": clocks, "gpu_launches": int(launches),
             "e2e": e2e, "roofline": trace["roofline"] if trace else roofline, "roofline_step": roofline_step, "cpu_baseline": cpu,
             "fwd_fps": fwd_fps, "fwdbwd_fps": fps if train else None,

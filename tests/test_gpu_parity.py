@@ -946,3 +946,26 @@ def test_train8_1m_full_frame_image_and_dense_gradients():
     gref = oracle.backward(sc, cams[0], g[0], mode=oracle.O3)
     print(grad_check(got, gref, ctx=(sc, [(cams[0], None)])))
     r.close()
+
+
+def test_fused_and_per_view_launches_agree(monkeypatch):
+    """K6 / K7 of all views in one fused launch (small views, arguments in shared
+    memory) vs one launch per view (arguments by value): bit-identical images and the
+    same gradients up to atomic summation order (PF_K6_PER_VIEW=0 / 1)."""
+    sc, cams = case("small360")
+    cams = cams[:4]
+    H, W = cams[0].height, cams[0].width
+    g = torch.from_numpy(pf_synth.make_grad_out(len(cams), H, W, seed=37)).cuda()
+    res = {}
+    for knob in ("0", "1"):
+        monkeypatch.setenv("PF_K6_PER_VIEW", knob)
+        r = renderer(sc, flags=0)
+        out = r.forward(cams).cpu().numpy()
+        grads = {k: v.detach().cpu().numpy().astype(np.float64)
+                 for k, v in r.backward(cams, g).items()}
+        res[knob] = (out, grads)
+        r.close()
+    assert np.array_equal(res["0"][0], res["1"][0])
+    for k, a in res["0"][1].items():
+        b = res["1"][1][k]
+        assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
