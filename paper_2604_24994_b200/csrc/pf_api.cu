@@ -8,6 +8,8 @@
 #include <new>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pf_bvh.cuh"
 #include "pf_internal.cuh"
 
@@ -339,11 +341,16 @@ void DevBuf::release()
     bytes = 0;
 }
 
+// NVTX range names of the stages (SURVEY §5 tracing): visible in nsys / ncu --nvtx
+static const char *const kStageNames[PF_NUM_STAGES] = {
+    "pf K0 edge records", "pf K1 preprocess", "pf K2 visible/compact", "pf K3 emit",
+    "pf K4 sort", "pf K5 ranges", "pf K6 forward", "pf K7 backward", "pf K8 unpack"};
+
 void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev)
 {
     *ev = nullptr;
+    nvtxRangePushA(kStageNames[stage]);   // host-side range around the stage's launches
     if (!s->profiling) return;
-    (void)stage;
     if (s->event_pool.empty()) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return;
@@ -356,6 +363,7 @@ void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev)
 
 void stage_end(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t ev)
 {
+    nvtxRangePop();
     if (!ev) return;
     cudaEvent_t e2;
     if (s->event_pool.empty()) {

@@ -41,6 +41,9 @@ namespace pf {
 #ifndef PF_K7_DIRECT_MAX   // up to this many segment lanes: per-lane atomics, no warp reduction
 #define PF_K7_DIRECT_MAX 10
 #endif
+#ifndef PF_K7_NBR_PREFETCH   // K7: L1 prefetch of a binding plane's neighbour id
+#define PF_K7_NBR_PREFETCH 1
+#endif
 #ifndef PF_K7_PREFETCH   // K7: L2 prefetch of the next chunk's K6 records
 #define PF_K7_PREFETCH 1
 #endif
@@ -452,8 +455,9 @@ __device__ __forceinline__ void warp_reduce16_atomic(float v[16], float *acc_cel
 // value of one interval end from its recorded constraint code (see end_code)
 template <bool kDipole>
 __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restrict__ edges,
-                                           uint32_t eb, uint32_t code, bool lo, const Seg &g,
-                                           int &q, const float4 &dplane)
+                                           const int32_t *__restrict__ nbr, uint32_t eb,
+                                           uint32_t code, bool lo, const Seg &g, int &q,
+                                           const float4 &dplane)
 {
     if (code == 0u) {
         q = kEndSphere;
@@ -470,6 +474,9 @@ __device__ __forceinline__ float coded_end(const Ray &R, const float4 *__restric
     } else {
         q = (int)code;                      // 2 + local plane index
         E = __ldg(edges + eb + code - 2u);
+#if PF_K7_NBR_PREFETCH   // end_grad reads the neighbour id after the replay math
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(nbr + eb + code - 2u));
+#endif
     }
     const float a = fmaf(R.dx, E.x, fmaf(R.dy, E.y, __fmul_rn(R.dz, E.z)));
     const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
@@ -1039,8 +1046,10 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
             prepare(j, seg, dpl, cr, cg, cb);
             if (seg) {
                 const uint32_t eb = S.eb[j];
-                g.lo = coded_end<kDipole>(P.R, ds.edges, eb, code & 0xffu, true, g, g.lo_q, dpl);
-                g.hi = coded_end<kDipole>(P.R, ds.edges, eb, code >> 8, false, g, g.hi_q, dpl);
+                g.lo = coded_end<kDipole>(P.R, ds.edges, ds.nbr_idx, eb, code & 0xffu, true, g,
+                                          g.lo_q, dpl);
+                g.hi = coded_end<kDipole>(P.R, ds.edges, ds.nbr_idx, eb, code >> 8, false, g,
+                                          g.hi_q, dpl);
             }
             const bool full = seg && (((code & 0xffu) == 255u) || ((code >> 8) == 255u));
             if (__any_sync(0xffffffffu, full)) {
