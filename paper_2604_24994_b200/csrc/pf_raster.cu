@@ -32,6 +32,9 @@ namespace pf {
 #ifndef PF_K6I_MINB   // K6 without records (inference, counting): 5 CTAs/SM measured faster
 #define PF_K6I_MINB 5
 #endif
+#ifndef PF_K6_CULL_MIN_REC   // recording K6: cells with fewer list planes are clipped by
+#define PF_K6_CULL_MIN_REC 6u  // all of them (the cull costs more than it saves there;
+#endif                         // measured: 6 best of {0, 6, 9, 12}; inference K6: always cull)
 #ifndef PF_K6_PCULL   // warp-level plane cull in K6 (cull_planes)
 #define PF_K6_PCULL 1
 #endif
@@ -125,7 +128,8 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                 xp += S.deg[j];
             }
             int kept = 0;
-            const bool culled = kCull && cull_on && S.deg[j] <= 32u;
+            const bool culled = kCull && cull_on && S.deg[j] <= 32u &&
+                                S.deg[j] >= (kRecord ? PF_K6_CULL_MIN_REC : 0u);
             if (culled) {
                 kept = cull_planes(S, j, W, ds.edges, PB[warp], lane);
                 if (kept < 0) continue;   // the warp's beam misses cell i: every interval is empty
