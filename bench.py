@@ -334,9 +334,10 @@ def cpu_baseline(sc, cam, seconds, train=True, calib=None, trace=False):
                       f"-> {frame:.1f}s per frame"}
 
 
-def load_traffic(kernel_tag, full=False):
-    """DRAM bytes per launch of a kernel from the newest committed ncu export
-    (full=True: the whole record, incl. the warp-instruction count)."""
+def load_traffic(kernel_tag, workload, full=False):
+    """DRAM bytes per launch of a kernel from the newest committed ncu export of the
+    SAME workload (full=True: the whole record, incl. the warp-instruction count).
+    A capture of another workload is not this launch's traffic: None then."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
     for f in reversed(files):
@@ -344,7 +345,7 @@ def load_traffic(kernel_tag, full=False):
             d = json.load(open(f))
         except Exception:
             continue
-        if kernel_tag in d:
+        if kernel_tag in d and d[kernel_tag].get("workload") == workload:
             if full:
                 return d[kernel_tag]
             return d[kernel_tag]["traffic_bytes"], d[kernel_tag]["source"]
@@ -647,18 +648,24 @@ def main():
     dom = "K7_backward" if (train and k7_ms >= k6_ms) else "K6_forward"
     d_ms, d_n = stages[dom]
     d_avg = d_ms / max(d_n, 1)
-    d_flops = f_bwd if dom == "K7_backward" else f_fwd
+    # views per launch: one per launch for 1080p views, all views of the call for a
+    # fused small-view launch (DESIGN 6, launch shape)
+    views_per_launch = nv * args.steps / max(d_n, 1)
+    d_flops = (f_bwd if dom == "K7_backward" else f_fwd) * views_per_launch
     achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
     ktag = ("k7_backward" if dom == "K7_backward" else "k6_forward") + ("_detail" if args.detail else "")
-    traffic, traffic_src = load_traffic(ktag)
-    prof = load_traffic(ktag, full=True) or {}
+    if not train and not args.detail:
+        ktag = "k6_forward_inference"                    # render workloads run the inference K6
+    traffic, traffic_src = load_traffic(ktag, workload_tag(args))
+    prof = load_traffic(ktag, workload_tag(args), full=True) or {}
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write)",
-                "traffic_source": traffic_src,
+                "traffic_source": traffic_src or ("no committed ncu capture of this kernel "
+                                                  "on this workload"),
                 "peak_note": f"FP32 = {SM_COUNT} SM x {FP32_LANES_PER_SM} lanes x 2 x "
                              f"{sm_max:.0f} MHz (guide unit counts; no tensor-core path)",
-                "avg_launch_ms": d_avg,
+                "avg_launch_ms": d_avg, "views_per_launch": views_per_launch,
                 "algorithmic_flops_per_launch": d_flops}
     if prof.get("warp_inst") and d_avg > 0:
         # the SM issue roofline: 4 schedulers x 148 SMs x clock warp-instructions/s

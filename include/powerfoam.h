@@ -246,8 +246,9 @@ PF_API int64_t pf_launch_count(const pf_scene *s);
 
 /*
  * Stage timing.  While enabled, CUDA events are recorded (on the call's
- * stream) around every launch of the named stages; pf_stage_times synchronizes,
- * writes per-stage totals in milliseconds and launch counts, and clears them.
+ * stream) around each stage's launches of a call; pf_stage_times synchronizes,
+ * writes per-stage totals in milliseconds and the number of kernels launched
+ * inside them, and clears them.
  * Stages: 0 edge records (K0), 1 preprocess (K1), 2 scan (K2), 3 emit (K3),
  * 4 sort (K4), 5 ranges (K5), 6 forward blend (K6), 7 backward (K7), 8 unpack (K8).
  */

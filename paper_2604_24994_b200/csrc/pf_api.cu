@@ -350,6 +350,7 @@ void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev)
 {
     *ev = nullptr;
     nvtxRangePushA(kStageNames[stage]);   // host-side range around the stage's launches
+    s->stage_l0 = s->launches;
     if (!s->profiling) return;
     if (s->event_pool.empty()) {
         cudaEvent_t e;
@@ -373,7 +374,7 @@ void stage_end(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t ev)
         s->event_pool.pop_back();
     }
     cudaEventRecord(e2, st);
-    s->events.push_back(StageEvent{stage, ev, e2});
+    s->events.push_back(StageEvent{stage, ev, e2, (int)(s->launches - s->stage_l0)});
 }
 
 }  // namespace pf
@@ -867,7 +868,7 @@ int pf_stage_times(pf_scene *s, double *ms, int64_t *launches)
         PF_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
         if (e.stage >= 0 && e.stage < PF_NUM_STAGES) {
             ms[e.stage] += t;
-            if (launches) launches[e.stage] += 1;
+            if (launches) launches[e.stage] += e.launches;
         }
         s->event_pool.push_back(e.a);
         s->event_pool.push_back(e.b);

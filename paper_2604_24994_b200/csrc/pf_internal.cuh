@@ -112,6 +112,7 @@ struct BatchViews {
 struct StageEvent {
     int stage;
     cudaEvent_t a, b;
+    int launches;   // kernels launched between a and b
 };
 
 }  // namespace pf
@@ -146,6 +147,7 @@ struct pf_scene {
     cudaStream_t side = nullptr;    // K0 of a training forward runs here, beside K1-K5
     cudaEvent_t side_fork = nullptr, side_join = nullptr;
     std::vector<pf::StageEvent> events;
+    int64_t stage_l0 = 0;   // s->launches at the open stage's begin
     std::vector<cudaEvent_t> event_pool;
     // NEXT-4 tracer: the ball BVH (built per call; once for PF_STATIC_SCENE) and stats
     pf::BallBVH *bvh = nullptr;

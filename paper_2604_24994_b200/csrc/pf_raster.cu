@@ -50,6 +50,10 @@ namespace pf {
 #ifndef PF_K7_PREFETCH   // K7: L2 prefetch of the next chunk's K6 records
 #define PF_K7_PREFETCH 1
 #endif
+#ifndef PF_K7_AGG   // K7: neighbour REDs aggregated over lanes with the same j (match_any);
+                    // measured 9.32 -> 14.09 ms per 8 views (train8_1m): off
+#define PF_K7_AGG 0
+#endif
 #ifndef PF_K7_GROUP   // K7: up to this many consecutive disjoint-mask records per pass
 #define PF_K7_GROUP 4
 #endif
@@ -250,9 +254,9 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
 }
 
 template <bool kDipole, int kDetail>
-static void launch_forward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
-                             int64_t *counters, bool record, float *stc, float *stn,
-                             cudaStream_t st)
+static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                            int64_t *counters, bool record, float *stc, float *stn,
+                            cudaStream_t st)
 {
     const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     // the plane-cull buffers are dynamic shared memory (static + dynamic may pass 48 KB)
@@ -302,7 +306,7 @@ static void launch_forward_t(pf_scene *s, const ViewState *views, int V, const V
                 if (wide) kern = k6_forward<false, false, kDipole, kDetail, true, true>;
             kern<<<grid, 256, dyn, st>>>(s->ds, h[0], args, T, nullptr, stc, stn, s->cull_on);
         }
-        return;
+        return 1;
     }
     for (int v = 0; v < V; ++v) {
         if (counters)
@@ -318,6 +322,7 @@ static void launch_forward_t(pf_scene *s, const ViewState *views, int V, const V
             kern<<<T, 256, dyn, st>>>(s->ds, h[v], nullptr, T, nullptr, stc, stn, s->cull_on);
         }
     }
+    return V;
 }
 
 cudaError_t launch_forward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
@@ -326,15 +331,16 @@ cudaError_t launch_forward(pf_scene *s, const ViewState *views, int V, const Vie
 {
     cudaEvent_t ev;
     stage_begin(s, 6, st, &ev);
+    int n;
     if (s->ds.K == 8)
-        launch_forward_t<true, 8>(s, views, V, args, counters, record, st_contrib, st_normal, st);
+        n = launch_forward_t<true, 8>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     else if (s->ds.K)
-        launch_forward_t<true, 1>(s, views, V, args, counters, record, st_contrib, st_normal, st);
+        n = launch_forward_t<true, 1>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     else if (s->ds.cellN)
-        launch_forward_t<true, 0>(s, views, V, args, counters, record, st_contrib, st_normal, st);
+        n = launch_forward_t<true, 0>(s, views, V, args, counters, record, st_contrib, st_normal, st);
     else
-        launch_forward_t<false, 0>(s, views, V, args, counters, record, st_contrib, st_normal, st);
-    ++s->launches;
+        n = launch_forward_t<false, 0>(s, views, V, args, counters, record, st_contrib, st_normal, st);
+    s->launches += n;
     stage_end(s, 6, st, ev);
     return cudaGetLastError();
 }
@@ -355,11 +361,14 @@ struct OwnGrad {
 
 // Accumulator layout: 12 floats per cell, acc[12 i + k]:
 //   k = 0..3 (p.x, p.y, p.z, w)  4..7 (r, sigma, R, G)  8 (B)  9..11 dipole normal.
+// With nj != nullptr the neighbour term is returned in (*nj, *nv) for a warp-aggregated
+// scatter (red_nbr_agg) instead of being issued here.
 template <bool kDipole, bool kDetail>
 __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, float tprime,
                                          float wgt, float rad, const float4 *__restrict__ edges,
                                          const int32_t *__restrict__ nbr, float *acc, OwnGrad &o,
-                                         const float4 &dnrm, uint32_t eb, float &g_ts)
+                                         const float4 &dnrm, uint32_t eb, float &g_ts,
+                                         int *nj = nullptr, float4 *nv = nullptr)
 {
     if (q == kEndNear) return;
     if (kDetail && q == kEndDipole) {   // the displaced face: through the detail chain
@@ -398,8 +407,49 @@ __device__ __forceinline__ void end_grad(const Ray &R, const Seg &g, int q, floa
     o.pz = fmaf(f, xpz, o.pz);
     o.w = fmaf(0.5f, f, o.w);
     const int j = __ldg(nbr + qe);
-    atomicAdd(reinterpret_cast<float4 *>(acc + 12 * (size_t)j),
-              make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f));
+    const float4 t = make_float4(f * (E.x - xpx), f * (E.y - xpy), f * (E.z - xpz), -0.5f * f);
+    if (nj) {
+        *nj = j;
+        *nv = t;
+        return;
+    }
+    atomicAdd(reinterpret_cast<float4 *>(acc + 12 * (size_t)j), t);
+}
+
+// Warp-aggregated neighbour scatter (every lane calls it; j < 0: nothing to add).
+// Lanes with the same neighbour j (neighbouring pixels leaving cell i through the
+// same face) are found by __match_any_sync; their float4 terms are summed by a
+// log-step tree over each group's lanes (uniform shuffles) and the group's lowest
+// lane issues ONE REDG.F32x4.  If no two lanes share a j the REDs go out directly.
+__device__ __forceinline__ void red_nbr_agg(float *acc, int j, float4 v, int lane)
+{
+    const int key = j >= 0 ? j : -1 - lane;   // idle lanes: singleton groups
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const bool multi = __any_sync(0xffffffffu, __popc(peers) > 1);
+    if (multi) {
+        const unsigned below = peers & ((1u << lane) - 1u);
+        unsigned up = peers & ~(below | (1u << lane));
+        int rel = __popc(below);
+        while (__any_sync(0xffffffffu, up != 0u)) {
+            const int nxt = up ? __ffs(up) - 1 : lane;
+            const float tx = __shfl_sync(0xffffffffu, v.x, nxt),
+                        ty = __shfl_sync(0xffffffffu, v.y, nxt),
+                        tz = __shfl_sync(0xffffffffu, v.z, nxt),
+                        tw = __shfl_sync(0xffffffffu, v.w, nxt);
+            const bool even = !(rel & 1);
+            if (even && up) {
+                v.x += tx;
+                v.y += ty;
+                v.z += tz;
+                v.w += tw;
+            }
+            up &= __ballot_sync(0xffffffffu, even);
+            rel >>= 1;
+        }
+        if (j >= 0 && below == 0u) atomicAdd(reinterpret_cast<float4 *>(acc + 12 * (size_t)j), v);
+    } else if (j >= 0) {
+        atomicAdd(reinterpret_cast<float4 *>(acc + 12 * (size_t)j), v);
+    }
 }
 
 // Sum of 9 per-lane values over the warp by a transposing reduction (12 shuffles
@@ -828,6 +878,8 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
     constexpr bool dipole = kDipole;
     OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
     float gs = 0.0f, gR = 0.0f, gG = 0.0f, gB = 0.0f, g_ts = 0.0f;
+    int nj_hi = -1, nj_lo = -1;   // neighbour terms for the aggregated scatter
+    float4 nv_hi = make_float4(0.0f, 0.0f, 0.0f, 0.0f), nv_lo = nv_hi;
     if (seg) {
         const float sig = S.sig[j];
         const float Tk = px.T;
@@ -850,10 +902,14 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
             const float rad = S.r[j];
             const uint32_t eb = S.eb[j];
             end_grad<kDipole, false>(R, g, g.hi_q, g.hi, gdt, rad, ds.edges, ds.nbr_idx, acc, o,
-                                     dnrm, eb, g_ts);
+                                     dnrm, eb, g_ts, PF_K7_AGG ? &nj_hi : nullptr, &nv_hi);
             end_grad<kDipole, false>(R, g, g.lo_q, g.lo, -gdt, rad, ds.edges, ds.nbr_idx, acc, o,
-                                     dnrm, eb, g_ts);
+                                     dnrm, eb, g_ts, PF_K7_AGG ? &nj_lo : nullptr, &nv_lo);
         }
+    }
+    if (PF_K7_AGG) {
+        red_nbr_agg(acc, nj_hi, nv_hi, lane);
+        red_nbr_agg(acc, nj_lo, nv_lo, lane);
     }
     // own-cell terms: one lane alone issues its atomics, else a transposing warp
     // reduction then one 9-lane atomic instruction
@@ -1075,8 +1131,8 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
 }
 
 template <bool kDipole, int kDetail>
-static void launch_backward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
-                              cudaStream_t st)
+static int launch_backward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
+                             cudaStream_t st)
 {
     const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     constexpr int smem = kDetail ? kWarps * 32 * 58 * (int)sizeof(float) : 0;
@@ -1092,13 +1148,16 @@ static void launch_backward_t(pf_scene *s, const ViewState *views, int V, const 
     if (fused) {
         k7_backward<kDipole, kDetail, true><<<(unsigned)(T * V), 256, smem, st>>>(
             s->ds, h[0], args, T, s->acc.as<float>());
-        return;
+        return 1;
     }
+    int n = 0;
     for (int v = 0; v < V; ++v) {
         if (views[v].P == 0) continue;
         k7_backward<kDipole, kDetail><<<T, 256, smem, st>>>(s->ds, h[v], nullptr, T,
                                                             s->acc.as<float>());
+        ++n;
     }
+    return n;
 }
 
 cudaError_t launch_backward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
@@ -1106,15 +1165,16 @@ cudaError_t launch_backward(pf_scene *s, const ViewState *views, int V, const Vi
 {
     cudaEvent_t ev;
     stage_begin(s, 7, st, &ev);
+    int n;
     if (s->ds.K == 8)
-        launch_backward_t<true, 8>(s, views, V, args, st);
+        n = launch_backward_t<true, 8>(s, views, V, args, st);
     else if (s->ds.K)
-        launch_backward_t<true, 1>(s, views, V, args, st);
+        n = launch_backward_t<true, 1>(s, views, V, args, st);
     else if (s->ds.cellN)
-        launch_backward_t<true, 0>(s, views, V, args, st);
+        n = launch_backward_t<true, 0>(s, views, V, args, st);
     else
-        launch_backward_t<false, 0>(s, views, V, args, st);
-    ++s->launches;
+        n = launch_backward_t<false, 0>(s, views, V, args, st);
+    s->launches += n;
     stage_end(s, 7, st, ev);
     return cudaGetLastError();
 }

@@ -78,9 +78,13 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum"]
 traffic = OrderedDict()
+workloads = {}
 for rep in sorted(f for f in os.listdir(src) if f.startswith("prof_") and f.endswith(".ncu-rep")):
     path = os.path.join(src, rep)
     name = rep[5:-8]
+    if "@" in name:                     # prof_<kernel>@<workload>.ncu-rep
+        name, wl = name.split("@", 1)
+        workloads[name] = wl
     det = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
@@ -122,7 +126,10 @@ for rep in sorted(f for f in os.listdir(src) if f.startswith("prof_") and f.ends
     if "dram__bytes_read.sum" in vals:
         traffic[name] = {"dram_read_bytes": tobytes(vals["dram__bytes_read.sum"]),
                          "dram_write_bytes": tobytes(vals["dram__bytes_write.sum"]),
-                         "source": f"profiles/{tag}_{name}_full.txt (ncu --set full, 1 launch)"}
+                         "source": f"profiles/{tag}_{name}_full.txt (ncu --set full, 1 launch)",
+                         # the bench workload tag of the capture (bench.py matches on it);
+                         # prof_<kernel>[@<workload>].ncu-rep, default the bench default
+                         "workload": workloads.get(name, "train8_1m")}
         traffic[name]["traffic_bytes"] = (traffic[name]["dram_read_bytes"]
                                           + traffic[name]["dram_write_bytes"])
         if "smsp__inst_executed.sum" in vals:
