@@ -58,6 +58,9 @@ namespace pf {
 #define PF_K7_GROUP 4
 #endif
 constexpr int kFuseTiles = 4096;   // views with fewer tiles: one fused K6 / K7 launch
+#ifndef PF_K7D_GROUP   // detail K7: records per pass (per-record column reductions inside)
+#define PF_K7D_GROUP 4
+#endif
 #ifndef PF_K7D_MINB
 #define PF_K7D_MINB 2
 #endif
@@ -612,7 +615,7 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
                                             const WarpStage &S, int j, BwdPixel &px,
                                             const DeviceScene &ds, float *acc, int lane,
                                             const DetailCtx &X, const float *om, float (*buf)[33],
-                                            float (*gbuf)[25])
+                                            float (*gbuf)[25], bool grouped)
 {
     const int K = KT == 8 ? 8 : ds.K;   // K == 8 (the paper's setting) known at compile time
     const uint32_t cell = S.cell[j];
@@ -816,10 +819,16 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
         o.py += (float)gc1;
         o.pz += (float)gc2;
     }
-    const unsigned segm = __ballot_sync(0xffffffffu, seg);   // rows of buf that were written
+    const unsigned segall = __ballot_sync(0xffffffffu, seg);   // rows of buf that were written
     __syncwarp();
-    // dL/dv: lane -> site k = lane / 4 and 6 consecutive (a, c) entries
-    {
+    // one column reduction per record of the pass (a group of records with disjoint lane
+    // masks holds several cells; lanes without a segment never match)
+    for (unsigned rem = segall; rem;) {
+        const int jr = __shfl_sync(0xffffffffu, j, __ffs(rem) - 1);
+        const unsigned segm = __ballot_sync(0xffffffffu, seg && j == jr);
+        rem &= ~segm;
+        const uint32_t cr = S.cell[jr];
+        // dL/dv: lane -> site k = lane / 4 and 6 consecutive (a, c) entries
         const int k = lane >> 2, ac0 = (lane & 3) * 6;
         float accv[6] = {0, 0, 0, 0, 0, 0};
         for (unsigned mm = segm; mm; mm &= mm - 1) {
@@ -829,25 +838,25 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             for (int q = 0; q < 6; ++q) accv[q] = fmaf(wk, buf[l][8 + ac0 + q], accv[q]);
         }
         if (k < K && ds.g_sv) {
-            float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cell + k) * 24 + ac0);
+            float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cr + k) * 24 + ac0);
             atomicAdd(dst, make_float2(accv[0], accv[1]));
             atomicAdd(dst + 1, make_float2(accv[2], accv[3]));
             atomicAdd(dst + 2, make_float2(accv[4], accv[5]));
         }
-    }
-    if (lane < 24) {
-        float t = 0.0f;
-        for (unsigned mm = segm; mm; mm &= mm - 1) t += gbuf[__ffs(mm) - 1][lane];
-        if (lane < 16) {
-            if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cell + lane, t);
-        } else if (lane - 16 < K && ds.g_disp) {
-            atomicAdd(ds.g_disp + (size_t)K * cell + (lane - 16), t);
+        if (lane < 24) {
+            float t = 0.0f;
+            for (unsigned mm = segm; mm; mm &= mm - 1) t += gbuf[__ffs(mm) - 1][lane];
+            if (lane < 16) {
+                if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cr + lane, t);
+            } else if (lane - 16 < K && ds.g_disp) {
+                atomicAdd(ds.g_disp + (size_t)K * cr + (lane - 16), t);
+            }
         }
     }
     __syncwarp();
     // own-cell terms (rgb_i is unused by detail cells: no colour gradient)
     float *accc = acc + 12 * (size_t)cell;
-    if (__popc(segm) <= PF_K7_DIRECT_MAX) {
+    if (grouped || __popc(segall) <= PF_K7_DIRECT_MAX) {
         if (seg) {
             atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
             atomicAdd(reinterpret_cast<float4 *>(accc) + 2, make_float4(0.0f, o.nx, o.ny, o.nz));
@@ -872,7 +881,7 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
         // (an fp32 instantiation for non-grazing warps measured slower on B200: the
         // fp64 -> fp32 conversions cost more than the fp64 arithmetic they save)
         detail_segment<double, kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, buf,
-                                        reinterpret_cast<float (*)[25]>(&buf[32][0]));
+                                        reinterpret_cast<float (*)[25]>(&buf[32][0]), grouped);
         return;
     }
     constexpr bool dipole = kDipole;
@@ -1004,7 +1013,8 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
             dpl = S.nrm[j];
         }
     };
-    constexpr bool kGroup = !kDetail && PF_K7_GROUP > 1;   // detail: warp-level per-cell reductions
+    constexpr bool kGroup = (kDetail ? PF_K7D_GROUP : PF_K7_GROUP) > 1;
+    constexpr uint32_t kGroupMax = kDetail ? PF_K7D_GROUP : PF_K7_GROUP;
     const uint32_t nchunks = wdone[(size_t)tile * kWarps + warp];
     const uint32_t c0 = chunk_off[tile];
     uint2 dnext = nchunks ? desc[(size_t)c0 * kWarps + warp] : make_uint2(0u, 0u);
@@ -1082,7 +1092,7 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
             int jl = ((uni >> lane) & 1u) ? (int)k : -1;
             uint32_t k1 = k + 1;
             if (kGroup) {
-                while (k1 < nrec && k1 - k < (uint32_t)PF_K7_GROUP) {
+                while (k1 < nrec && k1 - k < kGroupMax) {
                     const uint32_t m2 = __shfl_sync(0xffffffffu, my_mask, (int)k1);
                     if (m2 & uni) break;
                     uni |= m2;
