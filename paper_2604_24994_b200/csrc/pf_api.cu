@@ -555,6 +555,10 @@ int pf_destroy(pf_scene *s)
     s->order_all.release();
     s->chunk_off_all.release();
     s->rec_used.release();
+    s->items.release();
+    s->item_tpar.release();
+    s->item_cnt.release();
+    if (s->pinned_seg) cudaFreeHost(s->pinned_seg);
     if (s->pinned) cudaFreeHost(s->pinned);
     if (s->pinned_rec) cudaFreeHost(s->pinned_rec);
     if (s->pinned_args) cudaFreeHost(s->pinned_args);
@@ -633,8 +637,8 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
                     s->rec_ratio = fmax(s->rec_ratio * 0.98, 1.3 * (double)used / (double)prevP);
             }
         }
-        PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * (size_t)V));
-        PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * (size_t)V, st));
+        PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * 2 * (size_t)V));
+        PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * 2 * (size_t)V, st));
     }
     uint32_t *ks_all = nullptr;
     rc = emit_sort_ranges(s, s->views.data(), V, st, &ks_all);
@@ -657,6 +661,7 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
         }
         pf::ViewArgs a = view_args(vs, out + 4 * npix * (size_t)v, nullptr, record);
         a.rec_used = used;
+        a.seg_used = record ? s->rec_used.as<uint32_t>() + V + v : nullptr;
         s->host_args[v] = a;
     }
     {   // K6 of every view in one launch
@@ -717,6 +722,32 @@ int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const f
     s->ds.g_disp = g->detail_disp;
     s->ds.g_sv = g->detail_sv;
     int brc = PF_OK;
+    if (s->ds.K && (npix >= ((size_t)1 << 25) || V > 128))
+        return fail(PF_ERR_INVALID_ARGUMENT, "detail backward: at most 2^25 pixels per view and 128 views per call");
+    if (s->ds.K) {
+        // split detail backward: the item arena holds every segment the recording K6
+        // composited (one host sync: the counts of the forward just issued)
+        if (s->pinned_seg_n < V) {
+            if (s->pinned_seg) cudaFreeHost(s->pinned_seg);
+            s->pinned_seg = nullptr;
+            s->pinned_seg_n = 0;
+            PF_CUDA(cudaMallocHost(&s->pinned_seg, sizeof(uint32_t) * (size_t)(V + 16)));
+            s->pinned_seg_n = V + 16;
+        }
+        PF_CUDA(cudaMemcpyAsync(s->pinned_seg, s->rec_used.as<uint32_t>() + V,
+                                sizeof(uint32_t) * (size_t)V, cudaMemcpyDeviceToHost, st));
+        PF_CUDA(cudaStreamSynchronize(st));
+        for (int v = 0; v < V; ++v) s->views[v].nseg = s->pinned_seg[v];
+        const int64_t cap = pf::detail_items_needed(s, s->views.data(), V);
+        if (cap > (int64_t)0xFFFFFF00ll)
+            return fail(PF_ERR_OUT_OF_MEMORY, "detail segments of one backward launch exceed 2^32");
+        if (cap > 0) {
+            PF_CUDA(s->items.reserve(16 * (size_t)cap));
+            PF_CUDA(s->item_tpar.reserve(4 * (size_t)cap));
+        }
+        PF_CUDA(s->item_cnt.reserve(sizeof(uint32_t) * (size_t)V));
+        PF_CUDA(cudaMemsetAsync(s->item_cnt.ptr, 0, sizeof(uint32_t) * (size_t)V, st));
+    }
     s->host_args.resize(V);
     for (int v = 0; v < V; ++v)
         s->host_args[v] = view_args(s->views[v], nullptr, grad_out + 4 * npix * (size_t)v, true);

@@ -80,6 +80,7 @@ struct ViewState {
     DevBuf desc, wdone, rec;
     int64_t rec_cap = 0;                     // records the arena holds
     DevBuf saved;                            // float4[H*W] final (C + T bg, T)
+    int64_t nseg = 0;                        // detail: segments of the last recording K6
 };
 
 struct BallBVH;   // pf_bvh.cuh
@@ -94,7 +95,18 @@ struct ViewArgs {
     const float4 *grad_out;
     uint2 *desc;
     uint32_t *wdone, *rec, *rec_used;
+    uint32_t *seg_used;   // detail scenes: segments the recording K6 composited (sizes K7D items)
     uint32_t rec_cap, pad_;
+};
+
+// Items of the split detail backward (NEXT-2, pf_raster.cu): one per composited
+// detail segment with a gradient, {cell, view << 25 | pixel, wa bits, g_ts bits},
+// plus the parallel-ray chart parameter; written by K7, consumed by K7D.
+struct DetailItems {
+    uint4 *it;
+    float *tpar;
+    uint32_t *used;
+    uint32_t cap;
 };
 
 // one sort batch of up to kBatchViews views (kernel parameter of the binning)
@@ -130,7 +142,10 @@ struct pf_scene {
     pf::DevBuf ckeys0, ckeys1, cvals0, cvals1, ccnt, coffs;   // visible cells sorted by depth
     pf::DevBuf order_all, chunk_off_all;  // per-view tile orders / chunk offsets (V x T)
     pf::DevBuf acc;                 // backward packed accumulators
-    pf::DevBuf rec_used;            // u32[V] records used per view (K6 atomics)
+    pf::DevBuf rec_used;            // u32[2V] records used, then detail segments, per view (K6 atomics)
+    pf::DevBuf items, item_tpar, item_cnt;   // split detail backward: K7 -> K7D items, counters
+    uint32_t *pinned_seg = nullptr; // host readback of the segment counts (backward)
+    int pinned_seg_n = 0;
     double rec_ratio = 3.0;         // arena capacity in records per (tile, cell) pair
     uint32_t *pinned_rec = nullptr; // host copy of rec_used from the previous forward
     int pinned_rec_n = 0, rec_seen_views = 0;
@@ -198,6 +213,8 @@ cudaError_t launch_forward(pf_scene *s, const ViewState *views, int V, const Vie
                            cudaStream_t st);
 cudaError_t launch_backward(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
                             cudaStream_t st);
+// detail scenes: items the split backward's arena must hold (0: no split)
+int64_t detail_items_needed(const pf_scene *s, const ViewState *views, int V);
 cudaError_t pack_trace_nodes(pf_scene *s, BallBVH &bvh, DevBuf &nodes, cudaStream_t st);
 cudaError_t launch_trace(pf_scene *s, const BallBVH &bvh, const CamParams &cam, float *out,
                          unsigned long long *stats, cudaStream_t st);

@@ -118,7 +118,7 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
     float om[8];
     if (kDetail) sv_axis_weights(ds, P.R, om);
     long long xs = 0, xh = 0, xp = 0, xc = 0;
-    uint32_t chunks = 0;
+    uint32_t chunks = 0, nseg = 0;   // nseg: composited segments (detail: K7D item count)
     for (uint32_t base = rg.x; base < rg.y; base += 32, ++chunks) {
         if (__all_sync(0xffffffffu, done)) break;
         unsigned m = stage_chunk<kDipole, kCull>(S, ds, cam, vals, base + lane, rg.y, W, lane);
@@ -180,6 +180,7 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                         Rb.w[nrec * kRecWords + 1] = (uint32_t)j;
                     }
                     ++nrec;
+                    nseg += __popc(sm);
                 }
             }
             float wk = 0.0f;
@@ -239,7 +240,10 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
         }
         __syncwarp();
     }
-    if (kRecord && lane == 0) wdone[(size_t)tile * kWarps + warp] = chunks;
+    if (kRecord && lane == 0) {
+        wdone[(size_t)tile * kWarps + warp] = chunks;
+        if (kDetail && nseg) atomicAdd(VA.seg_used, nseg);
+    }
     if (P.in_image) {   // pixels without a ray keep T = 1: the background
         const float4 o = make_float4(fmaf(T, ds.bg[0], Cr), fmaf(T, ds.bg[1], Cg),
                                      fmaf(T, ds.bg[2], Cb), T);
@@ -610,6 +614,156 @@ struct BwdPixel {
 #else
 #define PF_DETAIL_FN __forceinline__
 #endif
+// The reverse chain of P:284-293 for one detail segment (after the compositing
+// replay gave wa = T_k alpha_k and g_ts = dL/dt_s of the displaced-face hit):
+// writes the lane's row of the dL/dv outer-product tile (brow: w_k, om_a wa G_c)
+// and of the site / displacement gradient tile (grow: dL/ds_k 2K, dL/dd_k K) and
+// adds the own-cell normal / position / radius terms to o.
+template <typename T, int KT>
+__device__ __forceinline__ void detail_reverse(const DeviceScene &ds, uint32_t cell, const DetailCtx &X,
+                                               double ys0, double ys1, double ys2, double qs0,
+                                               double qs1, const float ws[kMaxDetail],
+                                               const float dG[kMaxDetail], float wa, float g_ts,
+                                               float rad, const float4 &Gp, const float *om,
+                                               float *brow, float *grow, OwnGrad &o)
+{
+    const int K = KT == 8 ? 8 : ds.K;
+    const float tau = ds.sv_tau;
+    const double *F = ds.cellF + (size_t)kCellF * cell;
+    const double m0 = __ldg(F), m1 = __ldg(F + 1), m2 = __ldg(F + 2);
+    const double u0 = __ldg(F + 3), u1 = __ldg(F + 4), u2 = __ldg(F + 5);
+    const double v0 = __ldg(F + 6), v1 = __ldg(F + 7), v2 = __ldg(F + 8);
+    const double d0 = X.d[0], d1 = X.d[1], d2 = X.d[2];
+    const float2 *uv = reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell;
+    // ---- reverse of Eq. svrad: dL/dc = wa G
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) brow[k] = ws[k];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const float oa = om[a] * wa;
+        brow[8 + 3 * a] = oa * Gp.x;
+        brow[9 + 3 * a] = oa * Gp.y;
+        brow[10 + 3 * a] = oa * Gp.z;
+    }
+    const T tm0 = (T)m0, tm1 = (T)m1, tm2 = (T)m2, tu0 = (T)u0, tu1 = (T)u1, tu2 = (T)u2;
+    const T tv0 = (T)v0, tv1 = (T)v1, tv2 = (T)v2, td0 = (T)d0, td1 = (T)d1, td2 = (T)d2;
+    const T tA = (T)X.G.A, ttau = (T)tau;
+    T wsum = 0, sw = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        wsum += (T)ws[k];
+        sw += (T)ws[k] * (T)dG[k];
+    }
+    const T iwsum = (T)1 / wsum;
+    sw *= iwsum;   // renormalised: sum_k w_k (dG_k - sw) = 0 to working-precision rounding
+    T gq0 = 0, gq1 = 0;
+    const T cq = -ttau * (T)wa * iwsum;
+#pragma unroll
+    for (int k = 0; k < kMaxDetail; ++k) {
+        float gx = 0.0f, gy = 0.0f;
+        if (k < K) {
+            T ux, uy;
+            sv_unit<T>(__ldg(uv + k), qs0, qs1, ux, uy);
+            const T grho = cq * (T)ws[k] * ((T)dG[k] - sw);
+            gq0 += grho * ux;
+            gq1 += grho * uy;
+            gx = -(float)(grho * ux);
+            gy = -(float)(grho * uy);
+        }
+        grow[2 * k] = gx;
+        grow[2 * k + 1] = gy;
+        grow[16 + k] = 0.0f;
+    }
+    T gm0 = 0, gm1 = 0, gm2 = 0, gc0 = 0, gc1 = 0, gc2 = 0;
+    T gu0 = 0, gu1 = 0, gu2 = 0, gv0 = 0, gv1 = 0, gv2 = 0;
+    if (!X.G.parallel) {
+        const T s0 = (T)ys0, s1 = (T)ys1, s2 = (T)ys2;
+        // qs = (ys.u, ys.v)
+        const T gy0 = gq0 * tu0 + gq1 * tv0, gy1 = gq0 * tu1 + gq1 * tv1,
+                gy2 = gq0 * tu2 + gq1 * tv2;
+        gu0 = gq0 * s0; gu1 = gq0 * s1; gu2 = gq0 * s2;
+        gv0 = gq1 * s0; gv1 = gq1 * s1; gv2 = gq1 * s2;
+        // ys = ts d - c
+        const T gts = (T)g_ts + gy0 * td0 + gy1 * td1 + gy2 * td2;
+        gc0 = -gy0; gc1 = -gy1; gc2 = -gy2;
+        // ts = (c.m + delta) / (d.m)
+        const T iA = (T)1 / tA;
+        const T f = gts * iA;
+        gc0 += f * tm0; gc1 += f * tm1; gc2 += f * tm2;
+        gm0 = -f * s0; gm1 = -f * s1; gm2 = -f * s2;
+        T gdr = 0;
+        const float r = rad;
+        if (X.G.dr > r) o.r += (float)f;            // delta = r
+        else if (X.G.dr < -r) o.r -= (float)f;      // delta = -r
+        else gdr = f;
+        // Eq. svdisp at the base-face hit (the chart point in fp64 as in the forward)
+        // detail_plane's explicit op sequence, so x_bar (and the unit vectors taken
+        // there) is bit-identical to the forward's
+        const double B = dot3d(X.c, m0, m1, m2);
+        const double tb = __dmul_rn(B, __drcp_rn(X.G.A));
+        const double y0 = __fma_rn(tb, d0, -X.c[0]), y1 = __fma_rn(tb, d1, -X.c[1]),
+                     y2 = __fma_rn(tb, d2, -X.c[2]);
+        const double qb0 = __fma_rn(y0, u0, __fma_rn(y1, u1, __dmul_rn(y2, u2)));
+        const double qb1 = __fma_rn(y0, v0, __fma_rn(y1, v1, __dmul_rn(y2, v2)));
+        const float *wb = X.G.w;   // detail_plane's weights at x_bar
+        const float *dk = ds.ddisp + (size_t)K * cell;
+        T dr = 0, bsum = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k) {
+            bsum += (T)wb[k];
+            if (k < K) dr += (T)wb[k] * (T)__ldg(dk + k);
+        }
+        const T ibsum = (T)1 / bsum;
+        dr *= ibsum;
+        T gb0 = 0, gb1 = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxDetail; ++k) {
+            if (k < K) {
+                T ux, uy;
+                sv_unit<T>(__ldg(uv + k), qb0, qb1, ux, uy);
+                const T wk = (T)wb[k] * ibsum;
+                grow[16 + k] = (float)(wk * gdr);
+                const T grho = -ttau * wk * gdr * ((T)__ldg(dk + k) - dr);
+                gb0 += grho * ux;
+                gb1 += grho * uy;
+                grow[2 * k] -= (float)(grho * ux);
+                grow[2 * k + 1] -= (float)(grho * uy);
+            }
+        }
+        const T b0 = (T)y0, b1 = (T)y1, b2 = (T)y2;
+        const T hy0 = gb0 * tu0 + gb1 * tv0, hy1 = gb0 * tu1 + gb1 * tv1,
+                hy2 = gb0 * tu2 + gb1 * tv2;
+        gu0 += gb0 * b0; gu1 += gb0 * b1; gu2 += gb0 * b2;
+        gv0 += gb1 * b0; gv1 += gb1 * b1; gv2 += gb1 * b2;
+        const T f2 = (hy0 * td0 + hy1 * td1 + hy2 * td2) * iA;
+        gc0 += f2 * tm0 - hy0; gc1 += f2 * tm1 - hy1; gc2 += f2 * tm2 - hy2;
+        gm0 -= f2 * b0; gm1 -= f2 * b1; gm2 -= f2 * b2;
+    }
+    // frame: v = m x u, u = w/|w|, w = e_k x m, m = n/|n|
+    gm0 += tu1 * gv2 - tu2 * gv1;           // u x gv
+    gm1 += tu2 * gv0 - tu0 * gv2;
+    gm2 += tu0 * gv1 - tu1 * gv0;
+    gu0 += gv1 * tm2 - gv2 * tm1;           // gv x m
+    gu1 += gv2 * tm0 - gv0 * tm2;
+    gu2 += gv0 * tm1 - gv1 * tm0;
+    const T iwl = (T)__ldg(F + 10), inn = (T)__ldg(F + 9);   // stored as reciprocals
+    const int kax = (int)__ldg(F + 11);
+    const T ug = tu0 * gu0 + tu1 * gu1 + tu2 * gu2;
+    const T gw0 = (gu0 - tu0 * ug) * iwl, gw1 = (gu1 - tu1 * ug) * iwl,
+            gw2 = (gu2 - tu2 * ug) * iwl;
+    // + gw x e_k
+    if (kax == 0) { gm1 += gw2; gm2 -= gw1; }
+    else if (kax == 1) { gm0 -= gw2; gm2 += gw0; }
+    else { gm0 += gw1; gm1 -= gw0; }
+    const T mg = tm0 * gm0 + tm1 * gm1 + tm2 * gm2;
+    o.nx += (float)((gm0 - tm0 * mg) * inn);
+    o.ny += (float)((gm1 - tm1 * mg) * inn);
+    o.nz += (float)((gm2 - tm2 * mg) * inn);
+    o.px += (float)gc0;
+    o.py += (float)gc1;
+    o.pz += (float)gc2;
+}
+
 template <typename T, int KT>
 __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg,
                                             const WarpStage &S, int j, BwdPixel &px,
@@ -691,133 +845,8 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
             end_grad<true, true>(R, g, g.lo_q, g.lo, -gdt, S.r[j], ds.edges, ds.nbr_idx, acc, o,
                                  none, S.eb[j], g_ts);
         }
-        // ---- reverse of Eq. svrad: dL/dc = wa G
-#pragma unroll
-        for (int k = 0; k < kMaxDetail; ++k) buf[lane][k] = ws[k];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const float oa = om[a] * wa;
-            buf[lane][8 + 3 * a] = oa * px.G.x;
-            buf[lane][9 + 3 * a] = oa * px.G.y;
-            buf[lane][10 + 3 * a] = oa * px.G.z;
-        }
-        const T tm0 = (T)m0, tm1 = (T)m1, tm2 = (T)m2, tu0 = (T)u0, tu1 = (T)u1, tu2 = (T)u2;
-        const T tv0 = (T)v0, tv1 = (T)v1, tv2 = (T)v2, td0 = (T)d0, td1 = (T)d1, td2 = (T)d2;
-        const T tA = (T)X.G.A, ttau = (T)tau;
-        T wsum = 0, sw = 0;
-#pragma unroll
-        for (int k = 0; k < kMaxDetail; ++k) {
-            wsum += (T)ws[k];
-            sw += (T)ws[k] * (T)dG[k];
-        }
-        const T iwsum = (T)1 / wsum;
-        sw *= iwsum;   // renormalised: sum_k w_k (dG_k - sw) = 0 to working-precision rounding
-        T gq0 = 0, gq1 = 0;
-        const T cq = -ttau * (T)wa * iwsum;
-#pragma unroll
-        for (int k = 0; k < kMaxDetail; ++k) {
-            float gx = 0.0f, gy = 0.0f;
-            if (k < K) {
-                T ux, uy;
-                sv_unit<T>(__ldg(uv + k), qs0, qs1, ux, uy);
-                const T grho = cq * (T)ws[k] * ((T)dG[k] - sw);
-                gq0 += grho * ux;
-                gq1 += grho * uy;
-                gx = -(float)(grho * ux);
-                gy = -(float)(grho * uy);
-            }
-            gbuf[lane][2 * k] = gx;
-            gbuf[lane][2 * k + 1] = gy;
-            gbuf[lane][16 + k] = 0.0f;
-        }
-        T gm0 = 0, gm1 = 0, gm2 = 0, gc0 = 0, gc1 = 0, gc2 = 0;
-        T gu0 = 0, gu1 = 0, gu2 = 0, gv0 = 0, gv1 = 0, gv2 = 0;
-        if (!X.G.parallel) {
-            const T s0 = (T)ys0, s1 = (T)ys1, s2 = (T)ys2;
-            // qs = (ys.u, ys.v)
-            const T gy0 = gq0 * tu0 + gq1 * tv0, gy1 = gq0 * tu1 + gq1 * tv1,
-                    gy2 = gq0 * tu2 + gq1 * tv2;
-            gu0 = gq0 * s0; gu1 = gq0 * s1; gu2 = gq0 * s2;
-            gv0 = gq1 * s0; gv1 = gq1 * s1; gv2 = gq1 * s2;
-            // ys = ts d - c
-            const T gts = (T)g_ts + gy0 * td0 + gy1 * td1 + gy2 * td2;
-            gc0 = -gy0; gc1 = -gy1; gc2 = -gy2;
-            // ts = (c.m + delta) / (d.m)
-            const T iA = (T)1 / tA;
-            const T f = gts * iA;
-            gc0 += f * tm0; gc1 += f * tm1; gc2 += f * tm2;
-            gm0 = -f * s0; gm1 = -f * s1; gm2 = -f * s2;
-            T gdr = 0;
-            const float r = S.r[j];
-            if (X.G.dr > r) o.r += (float)f;            // delta = r
-            else if (X.G.dr < -r) o.r -= (float)f;      // delta = -r
-            else gdr = f;
-            // Eq. svdisp at the base-face hit (the chart point in fp64 as in the forward)
-            // detail_plane's explicit op sequence, so x_bar (and the unit vectors taken
-            // there) is bit-identical to the forward's
-            const double B = dot3d(X.c, m0, m1, m2);
-            const double tb = __dmul_rn(B, __drcp_rn(X.G.A));
-            const double y0 = __fma_rn(tb, d0, -X.c[0]), y1 = __fma_rn(tb, d1, -X.c[1]),
-                         y2 = __fma_rn(tb, d2, -X.c[2]);
-            const double qb0 = __fma_rn(y0, u0, __fma_rn(y1, u1, __dmul_rn(y2, u2)));
-            const double qb1 = __fma_rn(y0, v0, __fma_rn(y1, v1, __dmul_rn(y2, v2)));
-            const float *wb = X.G.w;   // detail_plane's weights at x_bar
-            const float *dk = ds.ddisp + (size_t)K * cell;
-            T dr = 0, bsum = 0;
-#pragma unroll
-            for (int k = 0; k < kMaxDetail; ++k) {
-                bsum += (T)wb[k];
-                if (k < K) dr += (T)wb[k] * (T)__ldg(dk + k);
-            }
-            const T ibsum = (T)1 / bsum;
-            dr *= ibsum;
-            T gb0 = 0, gb1 = 0;
-#pragma unroll
-            for (int k = 0; k < kMaxDetail; ++k) {
-                if (k < K) {
-                    T ux, uy;
-                    sv_unit<T>(__ldg(uv + k), qb0, qb1, ux, uy);
-                    const T wk = (T)wb[k] * ibsum;
-                    gbuf[lane][16 + k] = (float)(wk * gdr);
-                    const T grho = -ttau * wk * gdr * ((T)__ldg(dk + k) - dr);
-                    gb0 += grho * ux;
-                    gb1 += grho * uy;
-                    gbuf[lane][2 * k] -= (float)(grho * ux);
-                    gbuf[lane][2 * k + 1] -= (float)(grho * uy);
-                }
-            }
-            const T b0 = (T)y0, b1 = (T)y1, b2 = (T)y2;
-            const T hy0 = gb0 * tu0 + gb1 * tv0, hy1 = gb0 * tu1 + gb1 * tv1,
-                    hy2 = gb0 * tu2 + gb1 * tv2;
-            gu0 += gb0 * b0; gu1 += gb0 * b1; gu2 += gb0 * b2;
-            gv0 += gb1 * b0; gv1 += gb1 * b1; gv2 += gb1 * b2;
-            const T f2 = (hy0 * td0 + hy1 * td1 + hy2 * td2) * iA;
-            gc0 += f2 * tm0 - hy0; gc1 += f2 * tm1 - hy1; gc2 += f2 * tm2 - hy2;
-            gm0 -= f2 * b0; gm1 -= f2 * b1; gm2 -= f2 * b2;
-        }
-        // frame: v = m x u, u = w/|w|, w = e_k x m, m = n/|n|
-        gm0 += tu1 * gv2 - tu2 * gv1;           // u x gv
-        gm1 += tu2 * gv0 - tu0 * gv2;
-        gm2 += tu0 * gv1 - tu1 * gv0;
-        gu0 += gv1 * tm2 - gv2 * tm1;           // gv x m
-        gu1 += gv2 * tm0 - gv0 * tm2;
-        gu2 += gv0 * tm1 - gv1 * tm0;
-        const T iwl = (T)__ldg(F + 10), inn = (T)__ldg(F + 9);   // stored as reciprocals
-        const int kax = (int)__ldg(F + 11);
-        const T ug = tu0 * gu0 + tu1 * gu1 + tu2 * gu2;
-        const T gw0 = (gu0 - tu0 * ug) * iwl, gw1 = (gu1 - tu1 * ug) * iwl,
-                gw2 = (gu2 - tu2 * ug) * iwl;
-        // + gw x e_k
-        if (kax == 0) { gm1 += gw2; gm2 -= gw1; }
-        else if (kax == 1) { gm0 -= gw2; gm2 += gw0; }
-        else { gm0 += gw1; gm1 -= gw0; }
-        const T mg = tm0 * gm0 + tm1 * gm1 + tm2 * gm2;
-        o.nx += (float)((gm0 - tm0 * mg) * inn);
-        o.ny += (float)((gm1 - tm1 * mg) * inn);
-        o.nz += (float)((gm2 - tm2 * mg) * inn);
-        o.px += (float)gc0;
-        o.py += (float)gc1;
-        o.pz += (float)gc2;
+        detail_reverse<T, KT>(ds, cell, X, ys0, ys1, ys2, qs0, qs1, ws, dG, wa, g_ts, S.r[j],
+                              px.G, om, &buf[lane][0], &gbuf[lane][0], o);
     }
     const unsigned segall = __ballot_sync(0xffffffffu, seg);   // rows of buf that were written
     __syncwarp();
@@ -868,15 +897,229 @@ __device__ PF_DETAIL_FN void detail_segment(const Ray &R, const Seg &g, bool seg
     }
 }
 
+// ---------------------------------------------------------------------------
+// Split detail backward (PF_K7D_SPLIT).  The monolithic detail_segment runs the
+// whole per-segment chain in the record replay's lockstep, where a record holds
+// ~3 of 32 lanes.  Split: K7 replays the records (a pass = up to PF_K7D_GROUP
+// disjoint records) and does only what the compositing order needs -- the
+// segment colour (Eq. svrad, as K6), the compositing replay, dL/dt of the
+// interval ends (neighbour REDs, own-cell terms, g_ts of the displaced face) --
+// and emits one item per segment with a detail gradient; K7D then runs the chart
+// geometry, radiance pass and reverse chain of P:284-293 one item per lane, with
+// the per-cell column sums over the warp's 32 consecutive items.
+// ---------------------------------------------------------------------------
+template <int KT>
+__device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, bool seg,
+                                                 const WarpStage &S, int j, BwdPixel &px,
+                                                 const DeviceScene &ds, float *acc, int lane,
+                                                 const DetailCtx &X, const float *om, bool grouped,
+                                                 const DetailItems &DI, uint32_t pixtag)
+{
+    const uint32_t cell = S.cell[j];
+    OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
+    float gs = 0.0f, wa = 0.0f, g_ts = 0.0f, tpar = 0.0f;
+    if (seg) {
+        float cr, cg, cb;
+        if (X.G.parallel) tpar = __fadd_rn(g.tc, g.lo);
+        detail_color<KT>(ds, cell, X.d, X.c, X.G.parallel ? (double)tpar : X.G.ts, om, cr, cg, cb);
+        const float sig = S.sig[j];
+        const float Tk = px.T;
+        float alpha;
+        composite_step(sig, g.dt, cr, cg, cb, px.T, px.Cr, px.Cg, px.Cb, alpha);
+        const float Sr = __fsub_rn(px.fin.x, px.Cr), Sg = __fsub_rn(px.fin.y, px.Cg),
+                    Sb = __fsub_rn(px.fin.z, px.Cb);
+        float dtau = -px.GT_Tfin;
+        dtau = fmaf(px.G.x, fmaf(px.T, cr, -Sr), dtau);
+        dtau = fmaf(px.G.y, fmaf(px.T, cg, -Sg), dtau);
+        dtau = fmaf(px.G.z, fmaf(px.T, cb, -Sb), dtau);
+        wa = __fmul_rn(Tk, alpha);
+        gs = dtau * g.dt;
+        const float gdt = dtau * sig;
+        if (gdt != 0.0f) {
+            const float4 none = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            end_grad<true, true>(R, g, g.hi_q, g.hi, gdt, S.r[j], ds.edges, ds.nbr_idx, acc, o,
+                                 none, S.eb[j], g_ts);
+            end_grad<true, true>(R, g, g.lo_q, g.lo, -gdt, S.r[j], ds.edges, ds.nbr_idx, acc, o,
+                                 none, S.eb[j], g_ts);
+        }
+    }
+    // own-cell terms of the interval ends and sigma
+    float *accc = acc + 12 * (size_t)cell;
+    const unsigned segm = __ballot_sync(0xffffffffu, seg);
+    if (grouped || __popc(segm) <= PF_K7_DIRECT_MAX) {
+        if (seg) {
+            atomicAdd(reinterpret_cast<float4 *>(accc), make_float4(o.px, o.py, o.pz, o.w));
+            atomicAdd(reinterpret_cast<float2 *>(accc + 4), make_float2(o.r, gs));
+        }
+    } else {
+        float v[10] = {o.px, o.py, o.pz, o.w, o.r, gs, 0.0f, 0.0f, 0.0f, 0.0f};
+        warp_reduce9_atomic(v, accc, lane);
+    }
+    // one item per segment whose detail chain has a gradient to give
+    const bool emit = seg && (wa != 0.0f || g_ts != 0.0f);
+    const unsigned em = __ballot_sync(0xffffffffu, emit);
+    if (em) {
+        const int l0 = __ffs(em) - 1;
+        uint32_t base = 0;
+        if (lane == l0) base = atomicAdd(DI.used, (uint32_t)__popc(em));
+        base = __shfl_sync(0xffffffffu, base, l0);
+        if (emit) {
+            const uint32_t idx = base + (uint32_t)__popc(em & ((1u << lane) - 1u));
+            if (idx < DI.cap) {
+                DI.it[idx] = make_uint4(cell, pixtag, __float_as_uint(wa), __float_as_uint(g_ts));
+                DI.tpar[idx] = tpar;
+            }
+        }
+    }
+}
+
+#ifndef PF_K7D_SPLIT   // detail backward split into the replay (K7) and the chain (K7D)
+#define PF_K7D_SPLIT 1
+#endif
+#ifndef PF_K7D_MINB_REPLAY   // split detail K7 (replay + colour + items): CTAs per SM
+#define PF_K7D_MINB_REPLAY 3
+#endif
+#ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
+#define PF_K7D_MINB_CHAIN 2
+#endif
+constexpr int kChainStride = 2 * 33;   // per lane: a [33] row of each of the two tiles
+
+// K7D: the detail chain of the split backward, 32 consecutive items per warp
+// (grid-stride).  va: the call's device ViewArgs (camera, grad_out per view).
+template <int KT>
+__global__ void __launch_bounds__(256, PF_K7D_MINB_CHAIN)
+k7d_detail_chain(DeviceScene ds, const ViewArgs *__restrict__ va, DetailItems DI,
+                 float *__restrict__ acc)
+{
+    extern __shared__ float dyn_smem[];   // per warp: [32][33] outer-product tile, [32][33] gradient tile
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(dyn_smem + warp * 32 * kChainStride);
+    float (*gbuf)[33] = buf + 32;
+    const int K = KT == 8 ? 8 : ds.K;
+    const uint32_t n = min(*DI.used, DI.cap);
+    for (uint32_t base = (blockIdx.x * kWarps + warp) * 32u; base < n;
+         base += gridDim.x * kWarps * 32u) {
+        const uint32_t i = base + (uint32_t)lane;
+        const bool seg = i < n;
+        uint32_t cell = 0xffffffffu;
+        OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (seg) {
+            const uint4 it = DI.it[i];
+            cell = it.x;
+            const float wa = __uint_as_float(it.z), g_ts = __uint_as_float(it.w);
+            const ViewArgs &V = va[it.y >> 25];
+            const CamParams &cam = V.cam;
+            const uint32_t pix = it.y & 0x1ffffffu;
+            const int py = (int)(pix / (uint32_t)cam.W), pxx = (int)(pix - (uint32_t)py * cam.W);
+            DetailCtx X;
+            ray_dir(cam, pxx + 0.5, py + 0.5, X.d, nullptr);
+            Ray R;
+            R.dx = __double2float_rn(X.d[0]);
+            R.dy = __double2float_rn(X.d[1]);
+            R.dz = __double2float_rn(X.d[2]);
+            float om[8];
+            sv_axis_weights(ds, R, om);
+            cell_c(ds, cam, cell, X.c);
+            const float rad = __ldg(ds.cellA + cell).w;
+            detail_plane<KT>(ds, cell, X.d, X.c, rad, X.G);
+            const float4 Gp = V.grad_out[pix];
+            // Eq. svrad at x (the interval entry for a parallel ray), by detail_color's
+            // explicit op sequence: the weights w_k and the per-site c_k . G
+            const double *F = ds.cellF + (size_t)kCellF * cell;
+            const double tcol = X.G.parallel ? (double)DI.tpar[i] : X.G.ts;
+            const double ys0 = __fma_rn(tcol, X.d[0], -X.c[0]), ys1 = __fma_rn(tcol, X.d[1], -X.c[1]),
+                         ys2 = __fma_rn(tcol, X.d[2], -X.c[2]);
+            const double qs0 = __fma_rn(ys0, __ldg(F + 3), __fma_rn(ys1, __ldg(F + 4), __dmul_rn(ys2, __ldg(F + 5))));
+            const double qs1 = __fma_rn(ys0, __ldg(F + 6), __fma_rn(ys1, __ldg(F + 7), __dmul_rn(ys2, __ldg(F + 8))));
+            float ws[kMaxDetail], dG[kMaxDetail];
+            float2 st[kMaxDetail];
+            load_sites(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell, K, st);
+            soft_voronoi(st, K, qs0, qs1, ds.sv_tau, ws);
+            const float4 *sv = reinterpret_cast<const float4 *>(ds.dsv) + (size_t)6 * K * cell;
+#pragma unroll
+            for (int k = 0; k < kMaxDetail; ++k) {
+                dG[k] = 0.0f;
+                if (k < K) {
+                    float v[24];
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) {
+                        const float4 x = __ldg(sv + 6 * k + q);
+                        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+                    }
+                    float kr = 0.0f, kg = 0.0f, kb = 0.0f;
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {
+                        kr = fmaf(om[a], v[3 * a], kr);
+                        kg = fmaf(om[a], v[3 * a + 1], kg);
+                        kb = fmaf(om[a], v[3 * a + 2], kb);
+                    }
+                    dG[k] = fmaf(kr, Gp.x, fmaf(kg, Gp.y, kb * Gp.z));   // c_k . G
+                }
+            }
+            detail_reverse<double, KT>(ds, cell, X, ys0, ys1, ys2, qs0, qs1, ws, dG, wa, g_ts, rad,
+                                       Gp, om, &buf[lane][0], &gbuf[lane][0], o);
+            // own-cell terms of the chain as tile columns 24..30
+            gbuf[lane][24] = o.px;
+            gbuf[lane][25] = o.py;
+            gbuf[lane][26] = o.pz;
+            gbuf[lane][27] = o.r;
+            gbuf[lane][28] = o.nx;
+            gbuf[lane][29] = o.ny;
+            gbuf[lane][30] = o.nz;
+        }
+        __syncwarp();
+        // per-cell column sums over the warp's items (consecutive items mostly share a cell)
+        const unsigned valid = __ballot_sync(0xffffffffu, seg);
+        for (unsigned rem = valid; rem;) {
+            const uint32_t cr = __shfl_sync(0xffffffffu, cell, __ffs(rem) - 1);
+            const unsigned segm = __ballot_sync(0xffffffffu, seg && cell == cr);
+            rem &= ~segm;
+            const int k = lane >> 2, ac0 = (lane & 3) * 6;
+            float accv[6] = {0, 0, 0, 0, 0, 0};
+            for (unsigned mm = segm; mm; mm &= mm - 1) {
+                const int l = __ffs(mm) - 1;
+                const float wk = buf[l][k];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) accv[q] = fmaf(wk, buf[l][8 + ac0 + q], accv[q]);
+            }
+            if (k < K && ds.g_sv) {
+                float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cr + k) * 24 + ac0);
+                atomicAdd(dst, make_float2(accv[0], accv[1]));
+                atomicAdd(dst + 1, make_float2(accv[2], accv[3]));
+                atomicAdd(dst + 2, make_float2(accv[4], accv[5]));
+            }
+            if (lane < 31) {
+                float t = 0.0f;
+                for (unsigned mm = segm; mm; mm &= mm - 1) t += gbuf[__ffs(mm) - 1][lane];
+                if (lane < 16) {
+                    if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cr + lane, t);
+                } else if (lane < 24) {
+                    if (lane - 16 < K && ds.g_disp) atomicAdd(ds.g_disp + (size_t)K * cr + (lane - 16), t);
+                } else {
+                    // 24..26 -> p (slots 0..2), 27 -> r (slot 4), 28..30 -> n (slots 9..11)
+                    const int slot = lane < 27 ? lane - 24 : (lane == 27 ? 4 : lane - 19);
+                    if (t != 0.0f) atomicAdd(acc + 12 * (size_t)cr + slot, t);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // Backward of one segment (lanes with seg) + scatter of the cell's gradients.
-template <bool kDipole, int kDetail>
+template <bool kDipole, int kDetail, bool kSplit = false>
 __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, bool seg,
                                                  const WarpStage &S, int j, BwdPixel &px,
                                                  const DeviceScene &ds, float *acc, int lane,
                                                  float cr, float cg, float cb, const float4 &dnrm,
                                                  const DetailCtx *X, const float *om,
-                                                 float (*buf)[33], bool grouped = false)
+                                                 float (*buf)[33], bool grouped,
+                                                 const DetailItems &DI, uint32_t pixtag)
 {
+    if (kDetail && kSplit) {
+        detail_segment_a<kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, grouped, DI, pixtag);
+        return;
+    }
     if (kDetail) {
         // (an fp32 instantiation for non-grazing warps measured slower on B200: the
         // fp64 -> fp32 conversions cost more than the fp64 arithmetic they save)
@@ -944,10 +1187,11 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
 
 }  // namespace
 
-template <bool kDipole, int kDetail, bool kFused = false>
-__global__ void __launch_bounds__(256, kDetail ? PF_K7D_MINB : PF_K7_MINB)
+template <bool kDipole, int kDetail, bool kFused = false, bool kSplit = false>
+__global__ void __launch_bounds__(256, kDetail ? (kSplit ? PF_K7D_MINB_REPLAY : PF_K7D_MINB)
+                                               : PF_K7_MINB)
 k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, int ntiles,
-            float *__restrict__ acc)
+            float *__restrict__ acc, int view0, DetailItems DI)
 {
     __shared__ ViewArgs VAs[1];
     if (kFused) load_view_args(va, ntiles, VAs[0]);
@@ -989,6 +1233,9 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
         px.G = grad_out[pix];
     }
     px.GT_Tfin = __fmul_rn(px.G.w, px.fin.w);
+    // split detail backward: the item's (view, pixel)
+    const uint32_t pixtag = ((uint32_t)(kFused ? (int)blockIdx.x / ntiles : view0) << 25) |
+                            (uint32_t)(P.y * cam.W + P.x);
     float om[8];
     if (kDetail) sv_axis_weights(ds, P.R, om);
     DetailCtx X;
@@ -1062,8 +1309,9 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
                 }
                 const bool seg = g.dt > 0.0f;
                 if (!__any_sync(0xffffffffu, seg)) continue;
-                segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb,
-                                                   dpl, &X, om, buf);
+                segment_backward<kDipole, kDetail, kSplit>(P.R, g, seg, S, j, px, ds, acc, lane, cr,
+                                                           cg, cb, dpl, &X, om, buf, false, DI,
+                                                           pixtag);
                 if (seg && px.T < kTStop) done = true;
             }
             __syncwarp();
@@ -1132,12 +1380,31 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
                 }
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
-            segment_backward<kDipole, kDetail>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg, cb, dpl,
-                                               &X, om, buf, grouped);
+            segment_backward<kDipole, kDetail, kSplit>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg,
+                                                       cb, dpl, &X, om, buf, grouped, DI, pixtag);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();
     }
+}
+
+static bool backward_fused(const pf_scene *s, int T)
+{
+    return s->k6_per_view == 0 || (s->k6_per_view != 1 && T < kFuseTiles);
+}
+
+// items the split detail backward needs at once: all views of a fused launch, else
+// the largest view (K7 / K7D alternate per view on the stream)
+int64_t detail_items_needed(const pf_scene *s, const ViewState *views, int V)
+{
+    if (!s->ds.K || !PF_K7D_SPLIT) return 0;
+    const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
+    int64_t sum = 0, mx = 0;
+    for (int v = 0; v < V; ++v) {
+        sum += views[v].nseg;
+        mx = views[v].nseg > mx ? views[v].nseg : mx;
+    }
+    return backward_fused(s, T) ? sum : mx;
 }
 
 template <bool kDipole, int kDetail>
@@ -1145,27 +1412,57 @@ static int launch_backward_t(pf_scene *s, const ViewState *views, int V, const V
                              cudaStream_t st)
 {
     const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
-    constexpr int smem = kDetail ? kWarps * 32 * 58 * (int)sizeof(float) : 0;
-    if (smem && !s->attrs_k7) {
-        cudaFuncSetAttribute(k7_backward<kDipole, kDetail>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k7_backward<kDipole, kDetail, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    constexpr bool kSplit = kDetail && PF_K7D_SPLIT;
+    constexpr int smem = (kDetail && !kSplit) ? kWarps * 32 * 58 * (int)sizeof(float) : 0;
+    constexpr int smem_chain = kWarps * 32 * kChainStride * (int)sizeof(float);
+    if (!s->attrs_k7) {
+        if (smem) {
+            cudaFuncSetAttribute(k7_backward<kDipole, kDetail>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k7_backward<kDipole, kDetail, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        }
+        if (kSplit)
+            cudaFuncSetAttribute(k7d_detail_chain<kDetail>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_chain);
     }
     s->attrs_k7 = true;
     const ViewArgs *h = s->host_args.data();
-    const bool fused = s->k6_per_view == 0 || (s->k6_per_view != 1 && T < kFuseTiles);
-    if (fused) {
-        k7_backward<kDipole, kDetail, true><<<(unsigned)(T * V), 256, smem, st>>>(
-            s->ds, h[0], args, T, s->acc.as<float>());
+    float *acc = s->acc.as<float>();
+    // the split detail backward: items of view group g counted in item_cnt[g]
+    // (zeroed by the caller), K7D right after the group's K7
+    auto items = [&](int g, int64_t n) {
+        DetailItems DI = {};
+        if (kSplit) {
+            DI.it = s->items.as<uint4>();
+            DI.tpar = s->item_tpar.as<float>();
+            DI.used = s->item_cnt.as<uint32_t>() + g;
+            DI.cap = (uint32_t)n;
+        }
+        return DI;
+    };
+    auto chain = [&](const DetailItems &DI, int64_t n) {
+        if (!kSplit || n <= 0) return 0;
+        const int64_t blocks = (n + 255) / 256, cap_blocks = 148 * PF_K7D_MINB_CHAIN * 8;
+        k7d_detail_chain<kDetail><<<(unsigned)(blocks < cap_blocks ? blocks : cap_blocks), 256,
+                                    smem_chain, st>>>(s->ds, args, DI, acc);
         return 1;
+    };
+    if (backward_fused(s, T)) {
+        int64_t nseg = 0;
+        for (int v = 0; v < V; ++v) nseg += views[v].nseg;
+        const DetailItems DI = items(0, nseg);
+        k7_backward<kDipole, kDetail, true, kSplit><<<(unsigned)(T * V), 256, smem, st>>>(
+            s->ds, h[0], args, T, acc, 0, DI);
+        return 1 + chain(DI, nseg);
     }
     int n = 0;
     for (int v = 0; v < V; ++v) {
         if (views[v].P == 0) continue;
-        k7_backward<kDipole, kDetail><<<T, 256, smem, st>>>(s->ds, h[v], nullptr, T,
-                                                            s->acc.as<float>());
-        ++n;
+        const DetailItems DI = items(v, views[v].nseg);
+        k7_backward<kDipole, kDetail, false, kSplit><<<T, 256, smem, st>>>(s->ds, h[v], nullptr, T,
+                                                                           acc, v, DI);
+        n += 1 + chain(DI, views[v].nseg);
     }
     return n;
 }

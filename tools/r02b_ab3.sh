@@ -1,0 +1,7 @@
+#!/bin/bash
+# split detail backward (K7 replay + K7D chain) A/B + detail parity tests
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x -k "detail or fisheye" > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+VARIANTS="default build/split0.so build/rep2.so" BENCH_ARGS="--workload nerfsynth200k --detail 8" bash tools/ab.sh; mv gpurun_out/ab.log gpurun_out/ab_nerf_detail.log
+VARIANTS="default build/split0.so build/rep2.so" BENCH_ARGS="--detail 8" bash tools/ab.sh; mv gpurun_out/ab.log gpurun_out/ab_train_detail.log
