@@ -139,6 +139,8 @@ pf::ViewArgs view_args(pf::ViewState &vs, float *out, const float *grad_out, boo
     a.wdone = record ? vs.wdone.as<uint32_t>() : nullptr;
     a.rec = record ? vs.rec.as<uint32_t>() : nullptr;
     a.rec_cap = (uint32_t)vs.rec_cap;
+    a.col = (record && vs.col_cap) ? vs.col.as<float4>() : nullptr;   // detail scenes
+    a.col_cap = (uint32_t)vs.col_cap;
     return a;
 }
 
@@ -429,6 +431,13 @@ int pf_create_scene(const pf_scene_desc *d, pf_scene **out, pf_stream_t stream)
         if (v > 0.0) s->rec_ratio = v;
         s->rec_ratio_fixed = v > 0.0;
     }
+    if (const char *r = getenv("PF_COL_RATIO")) {   // debug knob: detail colour slots per pair
+        const double v = atof(r);
+        if (v >= 0.0) {
+            s->col_ratio = v;
+            s->col_ratio_fixed = true;
+        }
+    }
     pf::DeviceScene &ds = s->ds;
     ds.N = d->num_cells;
     ds.E = d->num_edges;
@@ -630,15 +639,21 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
         // adapt the record-arena size to what the previous forward used (records per
         // pair of THAT forward: bin_views has already overwritten views[v].P)
         if (s->rec_seen_views > 0 && !s->rec_ratio_fixed) {
-            for (int v = 0; v < s->rec_seen_views; ++v) {
+            const int pv = s->rec_seen_views;
+            for (int v = 0; v < pv; ++v) {
                 const int64_t prevP = s->rec_prev_P[v];
-                const uint32_t used = s->pinned_rec[v];
+                const uint32_t used = s->pinned_rec[v], segs = s->pinned_rec[pv + v];
                 if (prevP > 0 && used > 0)
                     s->rec_ratio = fmax(s->rec_ratio * 0.98, 1.3 * (double)used / (double)prevP);
+                const uint32_t cols = s->pinned_rec[2 * pv + v];   // slots claimed (warp blocks)
+                if (prevP > 0 && (segs > 0 || cols > 0) && !s->col_ratio_fixed)
+                    s->col_ratio = fmax(s->col_ratio * 0.98,
+                                        1.2 * (double)(segs > cols ? segs : cols) / (double)prevP);
             }
         }
-        PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * 2 * (size_t)V));
-        PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * 2 * (size_t)V, st));
+        // per view: records used, detail segments, detail colour slots used
+        PF_CUDA(s->rec_used.reserve(sizeof(uint32_t) * 3 * (size_t)V));
+        PF_CUDA(cudaMemsetAsync(s->rec_used.ptr, 0, sizeof(uint32_t) * 3 * (size_t)V, st));
     }
     uint32_t *ks_all = nullptr;
     rc = emit_sort_ranges(s, s->views.data(), V, st, &ks_all);
@@ -658,10 +673,16 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
             if (vs.rec_cap > (int64_t)0xFFFFFFF0ll) vs.rec_cap = 0xFFFFFFF0ll;
             PF_CUDA(vs.rec.reserve(72 * (size_t)vs.rec_cap));
             used = s->rec_used.as<uint32_t>() + v;
+            if (s->ds.K) {   // K6 -> K7 segment colours (a full arena: K7 recomputes)
+                vs.col_cap = (int64_t)(s->col_ratio * (double)vs.P) + (s->col_ratio_fixed ? 0 : 1024);
+                if (vs.col_cap > (int64_t)pf::kNoColCap) vs.col_cap = pf::kNoColCap;
+                PF_CUDA(vs.col.reserve(16 * (size_t)vs.col_cap));
+            }
         }
         pf::ViewArgs a = view_args(vs, out + 4 * npix * (size_t)v, nullptr, record);
         a.rec_used = used;
         a.seg_used = record ? s->rec_used.as<uint32_t>() + V + v : nullptr;
+        if (record && s->ds.K) a.col_used = s->rec_used.as<uint32_t>() + 2 * V + v;
         s->host_args[v] = a;
     }
     {   // K6 of every view in one launch
@@ -672,14 +693,14 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
                                    ex ? ex->contrib : nullptr, ex ? ex->normal_term : nullptr, st));
     }
     if (record) {
-        if (s->pinned_rec_n < V) {
+        if (s->pinned_rec_n < 3 * V) {
             if (s->pinned_rec) cudaFreeHost(s->pinned_rec);
             s->pinned_rec = nullptr;
             s->pinned_rec_n = 0;
-            PF_CUDA(cudaMallocHost(&s->pinned_rec, sizeof(uint32_t) * (size_t)(V + 16)));
-            s->pinned_rec_n = V + 16;
+            PF_CUDA(cudaMallocHost(&s->pinned_rec, sizeof(uint32_t) * (size_t)(3 * V + 16)));
+            s->pinned_rec_n = 3 * V + 16;
         }
-        PF_CUDA(cudaMemcpyAsync(s->pinned_rec, s->rec_used.ptr, sizeof(uint32_t) * (size_t)V,
+        PF_CUDA(cudaMemcpyAsync(s->pinned_rec, s->rec_used.ptr, sizeof(uint32_t) * 3 * (size_t)V,
                                 cudaMemcpyDeviceToHost, st));
         s->rec_prev_P.resize(V);
         for (int v = 0; v < V; ++v) s->rec_prev_P[v] = s->views[v].P;

@@ -53,6 +53,7 @@ struct DeviceScene {
     float *g_uv = nullptr, *g_disp = nullptr, *g_sv = nullptr;   // backward outputs (+=)
 };
 constexpr int kMaxDetail = 8;
+constexpr int64_t kNoColCap = 0x7fffff0ll;   // colour slots per view (27-bit record field)
 constexpr int kCellF = 12;
 
 // grow-only device buffer
@@ -81,6 +82,8 @@ struct ViewState {
     int64_t rec_cap = 0;                     // records the arena holds
     DevBuf saved;                            // float4[H*W] final (C + T bg, T)
     int64_t nseg = 0;                        // detail: segments of the last recording K6
+    DevBuf col;                              // detail: colour slots (float4 rgb + delta)
+    int64_t col_cap = 0;
 };
 
 struct BallBVH;   // pf_bvh.cuh
@@ -96,7 +99,9 @@ struct ViewArgs {
     uint2 *desc;
     uint32_t *wdone, *rec, *rec_used;
     uint32_t *seg_used;   // detail scenes: segments the recording K6 composited (sizes K7D items)
-    uint32_t rec_cap, pad_;
+    float4 *col;          // detail scenes: per-segment colour + displacement slots (K6 -> K7)
+    uint32_t *col_used;
+    uint32_t rec_cap, col_cap;
 };
 
 // Items of the split detail backward (NEXT-2, pf_raster.cu): one per composited
@@ -147,6 +152,8 @@ struct pf_scene {
     uint32_t *pinned_seg = nullptr; // host readback of the segment counts (backward)
     int pinned_seg_n = 0;
     double rec_ratio = 3.0;         // arena capacity in records per (tile, cell) pair
+    double col_ratio = 16.0;        // detail colour slots per pair (adapts like rec_ratio)
+    bool col_ratio_fixed = false;   // PF_COL_RATIO set (tests of the recompute path)
     uint32_t *pinned_rec = nullptr; // host copy of rec_used from the previous forward
     int pinned_rec_n = 0, rec_seen_views = 0;
     std::vector<int64_t> rec_prev_P; // per-view pair counts of the forward pinned_rec came from

@@ -730,6 +730,11 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
 // marked kOverflow and K7 recomputes it in full.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kOverflow = 0xffffffffu;
+// detail scenes: a record's second word is  slot | first colour slot << 5  (K6 stores
+// each segment's colour and displacement, float4 (rgb, delta), in the view's colour
+// arena, in lane order); kNoCol = no slots (arena full): K7 recomputes them
+constexpr uint32_t kNoCol = 0x7ffffffu;
+constexpr uint32_t kColBlock = 64;   // colour slots a K6 warp claims at a time
 constexpr int kRecWords = 18;   // mask, pos, 32 x u16 codes
 
 struct WarpRec {                 // a chunk's records in their global layout (flushed as is)

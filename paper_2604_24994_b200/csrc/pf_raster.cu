@@ -119,6 +119,7 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
     if (kDetail) sv_axis_weights(ds, P.R, om);
     long long xs = 0, xh = 0, xp = 0, xc = 0;
     uint32_t chunks = 0, nseg = 0;   // nseg: composited segments (detail: K7D item count)
+    uint32_t cnext = 0, cend = 0;    // detail: the warp's block of colour slots
     for (uint32_t base = rg.x; base < rg.y; base += 32, ++chunks) {
         if (__all_sync(0xffffffffu, done)) break;
         unsigned m = stage_chunk<kDipole, kCull>(S, ds, cam, vals, base + lane, rg.y, W, lane);
@@ -170,14 +171,33 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                     clip_interval<kRecord, kDipole>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
             }
             const bool seg = g.dt > 0.0f;
+            float4 *colp = nullptr;   // detail: this lane's colour slot (K7 reads it back)
             if (kRecord) {
                 const unsigned sm = __ballot_sync(0xffffffffu, seg);
                 if (sm) {
                     const uint32_t c = seg ? (end_code<kDipole>(g.lo_q) | (end_code<kDipole>(g.hi_q) << 8)) : 0u;
                     reinterpret_cast<uint16_t *>(Rb.w + nrec * kRecWords + 2)[lane] = (uint16_t)c;
+                    uint32_t cslot = kNoCol;
+                    if (kDetail && VA.col) {
+                        // colour slots of the record's segments, contiguous, from the
+                        // warp's current block of kColBlock slots (one atomic per block,
+                        // not per record: the counter is shared by the whole view)
+                        const uint32_t n = (uint32_t)__popc(sm);
+                        if (cnext + n > cend) {
+                            uint32_t b = 0;
+                            if (lane == 0) b = atomicAdd(VA.col_used, kColBlock);
+                            cnext = __shfl_sync(0xffffffffu, b, 0);
+                            cend = cnext + kColBlock;
+                        }
+                        cslot = cnext;
+                        cnext += n;
+                        if (cslot >= kNoCol || cslot + n > VA.col_cap) cslot = kNoCol;
+                        if (seg && cslot != kNoCol)
+                            colp = VA.col + cslot + __popc(sm & ((1u << lane) - 1u));
+                    }
                     if (lane == 0) {
                         Rb.w[nrec * kRecWords] = sm;
-                        Rb.w[nrec * kRecWords + 1] = (uint32_t)j;
+                        Rb.w[nrec * kRecWords + 1] = (uint32_t)j | (cslot << 5);
                     }
                     ++nrec;
                     nseg += __popc(sm);
@@ -188,9 +208,11 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                 float alpha;
                 const float Tk = T;
                 float cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
-                if (kDetail)
+                if (kDetail) {
                     detail_color<kDetail>(ds, S.cell[j], dd, dc,
                                  G.parallel ? (double)__fadd_rn(g.tc, g.lo) : G.ts, om, cr, cg, cb);
+                    if (kRecord && colp) *colp = make_float4(cr, cg, cb, G.delta);
+                }
                 composite_step(S.sig[j], g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
                 wk = __fmul_rn(Tk, alpha);
                 if (kCount) ++xc;
@@ -913,15 +935,17 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
                                                  const WarpStage &S, int j, BwdPixel &px,
                                                  const DeviceScene &ds, float *acc, int lane,
                                                  const DetailCtx &X, const float *om, bool grouped,
-                                                 const DetailItems &DI, uint32_t pixtag)
+                                                 const DetailItems &DI, uint32_t pixtag,
+                                                 bool have_col, float cr, float cg, float cb)
 {
     const uint32_t cell = S.cell[j];
     OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
     float gs = 0.0f, wa = 0.0f, g_ts = 0.0f, tpar = 0.0f;
     if (seg) {
-        float cr, cg, cb;
-        if (X.G.parallel) tpar = __fadd_rn(g.tc, g.lo);
-        detail_color<KT>(ds, cell, X.d, X.c, X.G.parallel ? (double)tpar : X.G.ts, om, cr, cg, cb);
+        // the chart parameter of a ray parallel to the face (K7D uses it only then)
+        tpar = __fadd_rn(g.tc, g.lo);
+        if (!have_col)   // K6's colour slot was not available: Eq. svrad as K6
+            detail_color<KT>(ds, cell, X.d, X.c, X.G.parallel ? (double)tpar : X.G.ts, om, cr, cg, cb);
         const float sig = S.sig[j];
         const float Tk = px.T;
         float alpha;
@@ -982,7 +1006,8 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
 #ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
 #define PF_K7D_MINB_CHAIN 2
 #endif
-constexpr int kChainStride = 2 * 33;   // per lane: a [33] row of each of the two tiles
+constexpr int kChainRow = 34;   // even: 8-byte aligned float2 reads of the outer-product rows
+constexpr int kChainStride = 2 * kChainRow;   // per lane: a row of each of the two tiles
 
 // K7D: the detail chain of the split backward, 32 consecutive items per warp
 // (grid-stride).  va: the call's device ViewArgs (camera, grad_out per view).
@@ -993,8 +1018,8 @@ k7d_detail_chain(DeviceScene ds, const ViewArgs *__restrict__ va, DetailItems DI
 {
     extern __shared__ float dyn_smem[];   // per warp: [32][33] outer-product tile, [32][33] gradient tile
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float (*buf)[33] = reinterpret_cast<float (*)[33]>(dyn_smem + warp * 32 * kChainStride);
-    float (*gbuf)[33] = buf + 32;
+    float (*buf)[kChainRow] = reinterpret_cast<float (*)[kChainRow]>(dyn_smem + warp * 32 * kChainStride);
+    float (*gbuf)[kChainRow] = buf + 32;
     const int K = KT == 8 ? 8 : ds.K;
     const uint32_t n = min(*DI.used, DI.cap);
     for (uint32_t base = (blockIdx.x * kWarps + warp) * 32u; base < n;
@@ -1074,23 +1099,28 @@ k7d_detail_chain(DeviceScene ds, const ViewArgs *__restrict__ va, DetailItems DI
             const uint32_t cr = __shfl_sync(0xffffffffu, cell, __ffs(rem) - 1);
             const unsigned segm = __ballot_sync(0xffffffffu, seg && cell == cr);
             rem &= ~segm;
+            // one pass over the run's items: lane (k = lane / 4, 6 consecutive (a, c)) of
+            // the outer product (float2 rows: stride kRow) and column `lane` of gbuf
             const int k = lane >> 2, ac0 = (lane & 3) * 6;
-            float accv[6] = {0, 0, 0, 0, 0, 0};
+            float2 a0 = make_float2(0.0f, 0.0f), a1 = a0, a2 = a0;
+            float t = 0.0f;
             for (unsigned mm = segm; mm; mm &= mm - 1) {
                 const int l = __ffs(mm) - 1;
                 const float wk = buf[l][k];
-#pragma unroll
-                for (int q = 0; q < 6; ++q) accv[q] = fmaf(wk, buf[l][8 + ac0 + q], accv[q]);
+                const float2 *row = reinterpret_cast<const float2 *>(&buf[l][8 + ac0]);
+                const float2 b0 = row[0], b1 = row[1], b2 = row[2];
+                a0.x = fmaf(wk, b0.x, a0.x); a0.y = fmaf(wk, b0.y, a0.y);
+                a1.x = fmaf(wk, b1.x, a1.x); a1.y = fmaf(wk, b1.y, a1.y);
+                a2.x = fmaf(wk, b2.x, a2.x); a2.y = fmaf(wk, b2.y, a2.y);
+                t += gbuf[l][lane];
             }
             if (k < K && ds.g_sv) {
                 float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cr + k) * 24 + ac0);
-                atomicAdd(dst, make_float2(accv[0], accv[1]));
-                atomicAdd(dst + 1, make_float2(accv[2], accv[3]));
-                atomicAdd(dst + 2, make_float2(accv[4], accv[5]));
+                atomicAdd(dst, a0);
+                atomicAdd(dst + 1, a1);
+                atomicAdd(dst + 2, a2);
             }
             if (lane < 31) {
-                float t = 0.0f;
-                for (unsigned mm = segm; mm; mm &= mm - 1) t += gbuf[__ffs(mm) - 1][lane];
                 if (lane < 16) {
                     if ((lane >> 1) < K && ds.g_uv) atomicAdd(ds.g_uv + (size_t)2 * K * cr + lane, t);
                 } else if (lane < 24) {
@@ -1114,10 +1144,12 @@ __device__ __forceinline__ void segment_backward(const Ray &R, const Seg &g, boo
                                                  float cr, float cg, float cb, const float4 &dnrm,
                                                  const DetailCtx *X, const float *om,
                                                  float (*buf)[33], bool grouped,
-                                                 const DetailItems &DI, uint32_t pixtag)
+                                                 const DetailItems &DI, uint32_t pixtag,
+                                                 bool have_col = false)
 {
     if (kDetail && kSplit) {
-        detail_segment_a<kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, grouped, DI, pixtag);
+        detail_segment_a<kDetail>(R, g, seg, S, j, px, ds, acc, lane, *X, om, grouped, DI, pixtag,
+                                  have_col, cr, cg, cb);
         return;
     }
     if (kDetail) {
@@ -1320,11 +1352,12 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
         // recorded entries only: stage them (lane k <-> record k)
         const uint32_t nrec = d.y;
         const uint32_t *R0 = rec + (size_t)d.x * kRecWords;
-        uint32_t my_mask = 0;
+        uint32_t my_mask = 0, my_cslot = kNoCol;
         if (lane < (int)nrec) {
             const uint2 mp = __ldg(reinterpret_cast<const uint2 *>(R0 + (size_t)lane * kRecWords));
             my_mask = mp.x;
-            const uint32_t pos = mp.y;
+            const uint32_t pos = mp.y & 31u;
+            my_cslot = mp.y >> 5;
             const uint32_t cell = __ldg(vals + base + pos);
             const float4 A = __ldg(ds.cellA + cell);
             double x0, x1, x2;
@@ -1361,7 +1394,27 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
             float4 dpl;
             float cr, cg, cb;
             if (seg) sphere_hit(P.R, S, j, g, ds, cam, PR);   // identical to K6 (recorded hit)
-            prepare(j, seg, dpl, cr, cg, cb);
+            // split detail: the segment's colour and displacement as K6 stored them
+            const float4 *colp = nullptr;
+            if (kSplit) {
+                const uint32_t cs = __shfl_sync(0xffffffffu, my_cslot, j),
+                               mj = __shfl_sync(0xffffffffu, my_mask, j);
+                if (seg && cs != kNoCol && VA.col)
+                    colp = VA.col + cs + __popc(mj & ((1u << lane) - 1u));
+            }
+            if (kSplit && colp) {
+                // the displaced face (m, delta) without the chart evaluation: m as
+                // detail_plane rounds it, delta as K6 computed it (bit-identical ends)
+                const double *F = ds.cellF + (size_t)kCellF * S.cell[j];
+                const float4 cv = __ldg(colp);
+                dpl = make_float4(__double2float_rn(__ldg(F)), __double2float_rn(__ldg(F + 1)),
+                                  __double2float_rn(__ldg(F + 2)), cv.w);
+                cr = cv.x;
+                cg = cv.y;
+                cb = cv.z;
+            } else {
+                prepare(j, seg, dpl, cr, cg, cb);
+            }
             if (seg) {
                 const uint32_t eb = S.eb[j];
                 g.lo = coded_end<kDipole>(P.R, ds.edges, ds.nbr_idx, eb, code & 0xffu, true, g,
@@ -1381,7 +1434,8 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
             }
             if (seg) g.dt = __fsub_rn(g.hi, g.lo);
             segment_backward<kDipole, kDetail, kSplit>(P.R, g, seg, S, j, px, ds, acc, lane, cr, cg,
-                                                       cb, dpl, &X, om, buf, grouped, DI, pixtag);
+                                                       cb, dpl, &X, om, buf, grouped, DI, pixtag,
+                                                       colp != nullptr);
             if (seg && px.T < kTStop) done = true;   // for a later overflow chunk
         }
         __syncwarp();

@@ -745,6 +745,16 @@ def test_detail_record_overflow_fallback(monkeypatch):
     _full_parity(sc, cams[:1], oracle.O3, seed=23)
 
 
+@pytest.mark.parametrize("ratio", ["0", "0.5"])
+def test_detail_colour_slots_overflow(monkeypatch, ratio):
+    """Split detail backward: K6's per-segment colour slots (K6 -> K7) missing for
+    every record (ratio 0) or for part of them (0.5 slots per pair): K7 recomputes
+    the colour and displaced face of those records; parity unchanged."""
+    monkeypatch.setenv("PF_COL_RATIO", ratio)
+    sc, cams = case("small360+detail")
+    _full_parity(sc, cams[:1], oracle.O3, seed=29)
+
+
 def test_detail_autograd_and_by_products():
     """torch.autograd through the detail parameters equals the explicit backward;
     by-products (sum T alpha) match the oracle's."""
