@@ -73,6 +73,24 @@ constexpr int kFuseTiles = 4096;   // views with fewer tiles: one fused K6 / K7 
 // device array into shared memory (small views: no per-view launch tails); else
 // one launch per view with its ViewArgs by value (constant-bank operands; measured
 // faster for 1080p views, whose launches are ~14 waves long)
+#ifndef PF_K6D_QUEUE   // detail K6: segment colours evaluated 32 at a time (ColQueue)
+#define PF_K6D_QUEUE 1
+#endif
+// Detail K6: the colour of a composited segment (Eq. svrad: soft-Voronoi weights at
+// the displaced-face hit and the 8 x 8 x 3 SV blend) does not change the
+// transmittance, so it need not be evaluated in the cell-by-cell lockstep, where a
+// cell holds a few of the warp's 32 rays.  The warp queues (chart parameter, cell,
+// weight T_k alpha_k) per segment and evaluates 32 queued colours at once, one per
+// lane; each pixel then adds its own entries in queue (= list) order with the same
+// fmaf as composite_step, so the image is bit-identical to the in-line evaluation.
+struct ColQueue {
+    double t[64];                // Q + t d: the displaced-face hit (or the parallel entry)
+    uint32_t cell[64], slot[64]; // slot: the K6 -> K7 colour slot (kNoCol: none)
+    float w[64], delta[64];      // T_k alpha_k, the clamped displacement
+    float cr[32], cg[32], cb[32];
+    uint8_t lane[64];            // the segment's pixel (lane of the warp)
+};
+
 template <bool kCount, bool kRecord, bool kDipole, int kDetail, bool kWide = false,
           bool kFused = false>
 __global__ void __launch_bounds__(256, kDetail ? PF_K6D_MINB
@@ -117,6 +135,53 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
     bool done = !P.valid;
     float om[8];
     if (kDetail) sv_axis_weights(ds, P.R, om);
+    constexpr bool kQueue = kDetail && PF_K6D_QUEUE;
+    // the queue follows the plane-cull buffers in dynamic shared memory
+    ColQueue &Q = reinterpret_cast<ColQueue *>(PB + (kCull ? kWarps : 0))[warp];
+    int qn = 0;                  // queued entries (warp-uniform)
+    unsigned long long qmine = 0;   // this lane's entries
+    auto flush = [&](int n) {
+        __syncwarp();
+        const int pl = lane < n ? (int)Q.lane[lane] : lane;
+        float omq[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) omq[a] = __shfl_sync(0xffffffffu, om[a], pl);
+        if (lane < n) {
+            const uint32_t cell = Q.cell[lane];
+            const int ti = (threadIdx.x & ~31) + pl;
+            const double dq[3] = {PR.dx[ti], PR.dy[ti], PR.dz[ti]};
+            double cq[3];
+            cell_c(ds, cam, cell, cq);
+            float cr, cg, cb;
+            detail_color<kDetail>(ds, cell, dq, cq, Q.t[lane], omq, cr, cg, cb);
+            Q.cr[lane] = cr;
+            Q.cg[lane] = cg;
+            Q.cb[lane] = cb;
+            if (kRecord && Q.slot[lane] != kNoCol)
+                VA.col[Q.slot[lane]] = make_float4(cr, cg, cb, Q.delta[lane]);
+        }
+        __syncwarp();
+        const unsigned mine = (unsigned)qmine & (n == 32 ? 0xffffffffu : ((1u << n) - 1u));
+        for (unsigned mm = mine; mm; mm &= mm - 1) {
+            const int p = __ffs(mm) - 1;
+            const float w = Q.w[p];
+            Cr = fmaf(w, Q.cr[p], Cr);
+            Cg = fmaf(w, Q.cg[p], Cg);
+            Cb = fmaf(w, Q.cb[p], Cb);
+        }
+        const int rest = qn - n;   // entries n.. move to the front (n = 32 > rest)
+        if (lane < rest) {
+            Q.t[lane] = Q.t[n + lane];
+            Q.cell[lane] = Q.cell[n + lane];
+            Q.slot[lane] = Q.slot[n + lane];
+            Q.w[lane] = Q.w[n + lane];
+            Q.delta[lane] = Q.delta[n + lane];
+            Q.lane[lane] = Q.lane[n + lane];
+        }
+        qmine = n == 32 ? (qmine >> 32) : 0ull;
+        qn = rest;
+        __syncwarp();
+    };
     long long xs = 0, xh = 0, xp = 0, xc = 0;
     uint32_t chunks = 0, nseg = 0;   // nseg: composited segments (detail: K7D item count)
     uint32_t cnext = 0, cend = 0;    // detail: the warp's block of colour slots
@@ -208,17 +273,41 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                 float alpha;
                 const float Tk = T;
                 float cr = S.cr[j], cg = S.cg[j], cb = S.cb[j];
-                if (kDetail) {
-                    detail_color<kDetail>(ds, S.cell[j], dd, dc,
-                                 G.parallel ? (double)__fadd_rn(g.tc, g.lo) : G.ts, om, cr, cg, cb);
-                    if (kRecord && colp) *colp = make_float4(cr, cg, cb, G.delta);
+                if (kQueue) {
+                    // composite_step without the colour (it is added at the flush)
+                    const float ex = __expf(-__fmul_rn(S.sig[j], g.dt));
+                    alpha = __fsub_rn(1.0f, ex);
+                    T = __fmul_rn(T, ex);
+                } else {
+                    if (kDetail) {
+                        detail_color<kDetail>(ds, S.cell[j], dd, dc,
+                                     G.parallel ? (double)__fadd_rn(g.tc, g.lo) : G.ts, om, cr, cg, cb);
+                        if (kRecord && colp) *colp = make_float4(cr, cg, cb, G.delta);
+                    }
+                    composite_step(S.sig[j], g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
                 }
-                composite_step(S.sig[j], g.dt, cr, cg, cb, T, Cr, Cg, Cb, alpha);
                 wk = __fmul_rn(Tk, alpha);
                 if (kCount) ++xc;
                 if (T < kTStop) {
                     done = true;
                     if (kCount) xs = (long long)(base + j - rg.x) + 1;
+                }
+            }
+            if (kQueue) {
+                const unsigned pm = __ballot_sync(0xffffffffu, seg);
+                if (pm) {
+                    if (seg) {
+                        const int pos = qn + __popc(pm & ((1u << lane) - 1u));
+                        Q.t[pos] = G.parallel ? (double)__fadd_rn(g.tc, g.lo) : G.ts;
+                        Q.cell[pos] = S.cell[j];
+                        Q.slot[pos] = (kRecord && colp) ? (uint32_t)(colp - VA.col) : kNoCol;
+                        Q.w[pos] = wk;
+                        Q.delta[pos] = G.delta;
+                        Q.lane[pos] = (uint8_t)lane;
+                        qmine |= 1ull << pos;
+                    }
+                    qn += __popc(pm);
+                    if (qn >= 32) flush(32);
                 }
             }
             if (st_contrib && __any_sync(0xffffffffu, seg)) {
@@ -262,6 +351,7 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
         }
         __syncwarp();
     }
+    if (kQueue && qn) flush(qn);
     if (kRecord && lane == 0) {
         wdone[(size_t)tile * kWarps + warp] = chunks;
         if (kDetail && nseg) atomicAdd(VA.seg_used, nseg);
@@ -289,7 +379,9 @@ static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const Vi
 {
     const int T = views[0].cam.tiles_x * views[0].cam.tiles_y;
     // the plane-cull buffers are dynamic shared memory (static + dynamic may pass 48 KB)
-    const size_t dyn = PF_K6_PCULL ? kWarps * sizeof(PlaneBuf) : 0;
+    // (+ the detail colour queues, ColQueue, after them)
+    const size_t dynq = (kDetail && PF_K6D_QUEUE) ? kWarps * sizeof(ColQueue) : 0;
+    const size_t dyn = (PF_K6_PCULL ? kWarps * sizeof(PlaneBuf) : 0) + dynq;
     if (s->cull_on < 0) {   // debug knob, read once per handle: 0 clips by every list plane
         const char *e = getenv("PF_PLANE_CULL");
         s->cull_on = (e && e[0] == '0') ? 0 : 1;
@@ -297,6 +389,10 @@ static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const Vi
     bool wide = false;
     for (int v = 0; v < V; ++v) wide = wide || views[v].cam.model == PF_FISHEYE;
     if (dyn && !s->attrs_k6) {   // once per handle (the attribute is per device)
+        cudaFuncSetAttribute(k6_forward<true, false, kDipole, kDetail>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k6_forward<true, false, kDipole, kDetail, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         cudaFuncSetAttribute(k6_forward<false, true, kDipole, kDetail>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         cudaFuncSetAttribute(k6_forward<false, false, kDipole, kDetail>,
@@ -324,7 +420,7 @@ static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const Vi
     if (fused) {
         const unsigned grid = (unsigned)(T * V);
         if (counters)
-            k6_forward<true, false, kDipole, kDetail, false, true><<<grid, 256, 0, st>>>(
+            k6_forward<true, false, kDipole, kDetail, false, true><<<grid, 256, dynq, st>>>(
                 s->ds, h[0], args, T, (long long *)counters, nullptr, nullptr, 0);
         else if (record)
             k6_forward<false, true, kDipole, kDetail, false, true><<<grid, 256, dyn, st>>>(
@@ -339,7 +435,7 @@ static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const Vi
     }
     for (int v = 0; v < V; ++v) {
         if (counters)
-            k6_forward<true, false, kDipole, kDetail><<<T, 256, 0, st>>>(
+            k6_forward<true, false, kDipole, kDetail><<<T, 256, dynq, st>>>(
                 s->ds, h[v], nullptr, T, (long long *)counters, nullptr, nullptr, 0);
         else if (record)
             k6_forward<false, true, kDipole, kDetail><<<T, 256, dyn, st>>>(
