@@ -658,7 +658,25 @@ def main():
         ktag = "k6_forward_inference"                    # render workloads run the inference K6
     traffic, traffic_src = load_traffic(ktag, workload_tag(args))
     prof = load_traffic(ktag, workload_tag(args), full=True) or {}
-    roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
+    kname = dom
+    if args.detail and dom == "K7_backward" and d_n > nv * args.steps:
+        # split detail backward (DESIGN 13): the stage is the K7 replay + the K7D chain,
+        # one launch of each per view (1080p); the captures are per-view launches too
+        kname = "K7_backward (K7 replay + K7D chain)"
+        parts = [load_traffic(t, workload_tag(args), full=True)
+                 for t in ("k7_backward_detail", "k7d_detail_chain")]
+        if all(parts):
+            traffic = sum(p_["traffic_bytes"] for p_ in parts)
+            traffic_src = " + ".join(p_["source"] for p_ in parts)
+            prof = {"warp_inst": sum(p_.get("warp_inst", 0.0) for p_ in parts),
+                    "issue_pct_of_peak": None}
+        else:
+            traffic, traffic_src, prof = None, None, {}
+        per_view_ms = d_ms / (nv * args.steps)
+        d_avg, views_per_launch = per_view_ms, 1.0       # per view: both kernels
+        d_flops = f_bwd
+        achieved = d_flops / (d_avg / 1e3) / 1e12 if d_avg > 0 else 0.0
+    roofline = {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write)",
                 "traffic_source": traffic_src or ("no committed ncu capture of this kernel "

@@ -1,0 +1,32 @@
+#!/bin/bash
+# Round-2 evidence: every bench line (committed under profiles/r02_bench/), the reference
+# arm, the ncu launch list of the default bench and full captures of the hot kernels,
+# each named prof_<kernel>@<workload> (the bench matches captures by workload)
+mkdir -p gpurun_out/bench
+rm -f gpurun_out/prof_*.ncu-rep gpurun_out/launches.csv
+B=gpurun_out/bench
+timeout 900 python bench.py > $B/bench_train8_1m.json 2> $B/bench_train8_1m.err
+timeout 900 python bench.py --dipoles --no-cpu > $B/bench_train8_1m_dipoles.json 2>&1
+timeout 900 python bench.py --workload mip360_1m --no-cpu > $B/bench_mip360_1m.json 2>&1
+timeout 900 python bench.py --workload nerfsynth200k --no-cpu > $B/bench_nerfsynth200k.json 2>&1
+timeout 1500 python bench.py --workload sweep64_3m --no-cpu --no-e2e --steps 3 > $B/bench_sweep64_3m.json 2>&1
+timeout 900 python bench.py --fisheye --no-cpu > $B/bench_train8_1m_fisheye.json 2>&1
+timeout 900 python bench.py --workload nerfsynth200k --detail 8 --no-cpu > $B/bench_nerfsynth200k_detail8.json 2>&1
+timeout 900 python bench.py --detail 8 --no-cpu --steps 5 > $B/bench_train8_1m_detail8.json 2>&1
+timeout 900 python bench.py --lists knn --no-cpu > $B/bench_train8_1m_knn.json 2>&1
+timeout 900 python bench.py --workload mip360_1m --trace --no-cpu --steps 5 > $B/bench_mip360_1m_trace.json 2>&1
+timeout 900 python bench.py --workload mip360_1m --trace --fisheye --no-cpu --steps 5 > $B/bench_mip360_1m_trace_fisheye.json 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $B/bench_reference.json 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu \
+    > gpurun_out/ncu_launch.log 2>&1
+NCU="timeout 900 ncu --set full --import-source on --clock-control none"
+$NCU -k regex:k6_forward -c 1 -o "gpurun_out/prof_k6_forward@train8_1m" python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k6.log 2>&1
+$NCU -k regex:k7_backward -c 1 -o "gpurun_out/prof_k7_backward@train8_1m" python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k7.log 2>&1
+$NCU --kernel-name-base mangled -k regex:k6_forwardILb0ELb0ELb0ELi0ELb0ELb0E -c 1 -o "gpurun_out/prof_k6_forward_inference@mip360_1m" \
+    python bench.py --workload mip360_1m --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k6i.log 2>&1
+$NCU -k regex:k6_forward -c 1 -o "gpurun_out/prof_k6_forward_detail@train8_1m+detail8" python bench.py --detail 8 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k6d.log 2>&1
+$NCU -k regex:k7_backward -c 1 -o "gpurun_out/prof_k7_backward_detail@train8_1m+detail8" python bench.py --detail 8 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k7d.log 2>&1
+$NCU -k regex:k7d_detail_chain -c 1 -o "gpurun_out/prof_k7d_detail_chain@train8_1m+detail8" python bench.py --detail 8 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k7dc.log 2>&1
+$NCU -k regex:k4_scatter -c 1 -o "gpurun_out/prof_k4_scatter@train8_1m" python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k4.log 2>&1
+nvidia-smi -q -d CLOCK > gpurun_out/smi_clocks.txt 2>&1
