@@ -719,7 +719,7 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
 // K6 -> K7 segment records.  For every 32-entry chunk of its tile list a warp
 // walked, K6 writes a descriptor (first record, count); for every chunk entry
 // that produced a non-empty segment in at least one lane it writes a 72-byte
-// record: the lane mask, the entry's position in the chunk, and per lane the
+// record: the lane mask, the entry (cell id, or its chunk slot), and per lane the
 // binding constraints of the interval (lo, hi) coded in one byte each
 // (0 sphere, 1 near, 2+k plane k of the cell's list, 254 dipole face,
 // 255 = not codable).  K7
@@ -730,7 +730,8 @@ __device__ __forceinline__ void detail_color(const DeviceScene &ds, uint32_t cel
 // marked kOverflow and K7 recomputes it in full.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kOverflow = 0xffffffffu;
-// detail scenes: a record's second word is  slot | first colour slot << 5  (K6 stores
+// A record's second word is the cell id (plain scenes; K7 stages it without the
+// tile-list gather) or, for detail scenes,  slot | first colour slot << 5  (K6 stores
 // each segment's colour and displacement, float4 (rgb, delta), in the view's colour
 // arena, in lane order); kNoCol = no slots (arena full): K7 recomputes them
 constexpr uint32_t kNoCol = 0x7ffffffu;

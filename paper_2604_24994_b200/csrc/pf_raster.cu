@@ -262,7 +262,9 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                     }
                     if (lane == 0) {
                         Rb.w[nrec * kRecWords] = sm;
-                        Rb.w[nrec * kRecWords + 1] = (uint32_t)j | (cslot << 5);
+                        // plain scenes: the cell id itself (K7 skips the list gather);
+                        // detail scenes: the chunk slot and the first colour slot
+                        Rb.w[nrec * kRecWords + 1] = kDetail ? ((uint32_t)j | (cslot << 5)) : S.cell[j];
                     }
                     ++nrec;
                     nseg += __popc(sm);
@@ -1452,9 +1454,8 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
         if (lane < (int)nrec) {
             const uint2 mp = __ldg(reinterpret_cast<const uint2 *>(R0 + (size_t)lane * kRecWords));
             my_mask = mp.x;
-            const uint32_t pos = mp.y & 31u;
-            my_cslot = mp.y >> 5;
-            const uint32_t cell = __ldg(vals + base + pos);
+            if (kDetail) my_cslot = mp.y >> 5;
+            const uint32_t cell = kDetail ? __ldg(vals + base + (mp.y & 31u)) : mp.y;
             const float4 A = __ldg(ds.cellA + cell);
             double x0, x1, x2;
             const double t = cell_offset(cam, A, W, x0, x1, x2);

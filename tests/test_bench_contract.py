@@ -51,3 +51,14 @@ def test_gpus_flag_fails_loudly_without_enough_gpus():
     assert out.returncode != 0
     assert "needs 2 visible GPUs" in out.stderr
     assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+
+
+def test_ncu_figures_only_for_the_captured_workload():
+    """The roofline's traffic / issue figures come from a committed ncu capture of the
+    same kernel on the same workload; another workload's capture is never attached."""
+    sys.path.insert(0, ROOT)
+    import bench
+    tr, src = bench.load_traffic("k6_forward", "train8_1m")
+    assert tr and tr > 0 and src.startswith("profiles/")
+    assert bench.load_traffic("k6_forward", "nerfsynth200k") == (None, None)
+    assert bench.load_traffic("k6_forward", "train8_1m+dipoles", full=True) is None

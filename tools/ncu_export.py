@@ -1,6 +1,6 @@
 """Export ncu evidence into profiles/ (tracked):
 
-  python tools/ncu_export.py <round-tag> [gpurun_out]
+  python tools/ncu_export.py <round-tag> [gpurun_out] [out dir, default profiles/]
 
 writes
   profiles/<tag>_launches.csv        kernel, grid, block, duration_ns (one row per launch)
@@ -21,7 +21,7 @@ from collections import OrderedDict, defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
 src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
-out = os.path.join(ROOT, "profiles")
+out = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "profiles")
 os.makedirs(out, exist_ok=True)
 
 

@@ -3,7 +3,7 @@
 # arm, the ncu launch list of the default bench and full captures of the hot kernels,
 # each named prof_<kernel>@<workload> (the bench matches captures by workload)
 mkdir -p gpurun_out/bench
-rm -f gpurun_out/prof_*.ncu-rep gpurun_out/launches.csv
+rm -rf gpurun_out/prof_*.ncu-rep gpurun_out/launches.csv gpurun_out/export
 B=gpurun_out/bench
 timeout 900 python bench.py > $B/bench_train8_1m.json 2> $B/bench_train8_1m.err
 timeout 900 python bench.py --dipoles --no-cpu > $B/bench_train8_1m_dipoles.json 2>&1
@@ -30,3 +30,12 @@ $NCU -k regex:k7_backward -c 1 -o "gpurun_out/prof_k7_backward_detail@train8_1m+
 $NCU -k regex:k7d_detail_chain -c 1 -o "gpurun_out/prof_k7d_detail_chain@train8_1m+detail8" python bench.py --detail 8 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k7dc.log 2>&1
 $NCU -k regex:k4_scatter -c 1 -o "gpurun_out/prof_k4_scatter@train8_1m" python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_k4.log 2>&1
 nvidia-smi -q -d CLOCK > gpurun_out/smi_clocks.txt 2>&1
+# export the captures to text here (the .ncu-rep files would exceed gpurun's 64 MiB
+# copy-back limit), then keep only the summaries
+mkdir -p gpurun_out/export
+python tools/ncu_export.py r02 gpurun_out gpurun_out/export > gpurun_out/export/export.log 2>&1
+for r in gpurun_out/prof_*.ncu-rep; do
+  b=$(basename "$r" .ncu-rep)
+  python tools/ncu_cuda_lines.py "$r" 60 > "gpurun_out/export/${b}_lines.txt" 2>&1
+done
+rm -f gpurun_out/prof_*.ncu-rep
