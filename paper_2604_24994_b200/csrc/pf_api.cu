@@ -162,7 +162,7 @@ int upload_view_args(pf_scene *s, const pf::ViewArgs *a, int V, int slot, cudaSt
     pf::ViewArgs *h = s->pinned_args + (size_t)slot * s->pinned_args_n;
     memcpy(h, a, sizeof(pf::ViewArgs) * (size_t)V);
     pf::ViewArgs *d = s->vargs.as<pf::ViewArgs>() + (size_t)slot * s->pinned_args_n;
-    PF_CUDA(cudaMemcpyAsync(d, h, sizeof(pf::ViewArgs) * (size_t)V, cudaMemcpyHostToDevice, st));
+    PF_CUDA(pf::small_copy(s, d, h, sizeof(pf::ViewArgs) * (size_t)V, st));
     *dev = d;
     return PF_OK;
 }
@@ -290,9 +290,17 @@ int bin_views_of(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st)
         s->pinned_n = 2 * V + 16;
     }
     // per view: the pair total, and the visible cells (a sum over its blocks)
-    PF_CUDA(cudaMemcpyAsync(s->pinned, ptot, sizeof(int64_t) * (size_t)V, cudaMemcpyDeviceToHost, st));
-    std::vector<int> hb((size_t)nbx * V);
-    PF_CUDA(cudaMemcpyAsync(hb.data(), s->bvis.ptr, sizeof(int) * hb.size(), cudaMemcpyDeviceToHost, st));
+    const size_t nhb = (size_t)nbx * V;
+    if (s->pinned_hb_n < nhb) {
+        if (s->pinned_hb) cudaFreeHost(s->pinned_hb);
+        s->pinned_hb = nullptr;
+        s->pinned_hb_n = 0;
+        PF_CUDA(cudaMallocHost(&s->pinned_hb, sizeof(int) * nhb));
+        s->pinned_hb_n = nhb;
+    }
+    const int *hb = s->pinned_hb;
+    PF_CUDA(pf::small_copy(s, s->pinned, ptot, sizeof(int64_t) * (size_t)V, st));
+    PF_CUDA(pf::small_copy(s, s->pinned_hb, s->bvis.ptr, sizeof(int) * nhb, st));
     PF_CUDA(cudaStreamSynchronize(st));
     for (int v = 0; v < V; ++v) {
         const int64_t P = s->pinned[v];
@@ -315,6 +323,25 @@ int bin_views(pf_scene *s, int V, cudaStream_t st)
 
 // ---------------------------------------------------------------------------
 namespace pf {
+
+// Small host <-> device transfers of the call (ViewArgs up; pair / visible / record
+// counts down) as a one-block kernel reading or writing pinned host memory directly
+// (UVA maps cudaMallocHost memory), NOT as cudaMemcpyAsync: a training loop keeps the
+// copy engines busy with its own transfers (the next dL/dimage up, the last gradients
+// down), and a 2 KB copy queued behind a 265 MB one stalls the whole forward.
+__global__ void k_small_copy(const uint32_t *__restrict__ src, uint32_t *__restrict__ dst, int n)
+{
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t small_copy(pf_scene *s, void *dst, const void *src, size_t bytes, cudaStream_t st)
+{
+    if (!bytes) return cudaSuccess;
+    ++s->launches;
+    k_small_copy<<<1, 256, 0, st>>>(static_cast<const uint32_t *>(src), static_cast<uint32_t *>(dst),
+                                    (int)(bytes / 4));
+    return cudaGetLastError();
+}
 
 cudaError_t DevBuf::reserve(size_t n)
 {
@@ -551,6 +578,7 @@ int pf_destroy(pf_scene *s)
         v.desc.release();
         v.wdone.release();
         v.rec.release();
+        v.col.release();
     }
     s->debug_view.rect.release();
     s->debug_view.count.release();
@@ -570,6 +598,7 @@ int pf_destroy(pf_scene *s)
     if (s->pinned_seg) cudaFreeHost(s->pinned_seg);
     if (s->pinned) cudaFreeHost(s->pinned);
     if (s->pinned_rec) cudaFreeHost(s->pinned_rec);
+    if (s->pinned_hb) cudaFreeHost(s->pinned_hb);
     if (s->pinned_args) cudaFreeHost(s->pinned_args);
     s->vargs.release();
     for (auto &e : s->events) {
@@ -700,6 +729,7 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
             PF_CUDA(cudaMallocHost(&s->pinned_rec, sizeof(uint32_t) * (size_t)(3 * V + 16)));
             s->pinned_rec_n = 3 * V + 16;
         }
+        // (read at the next forward; a copy-engine transfer is fine here: nothing waits on it)
         PF_CUDA(cudaMemcpyAsync(s->pinned_rec, s->rec_used.ptr, sizeof(uint32_t) * 3 * (size_t)V,
                                 cudaMemcpyDeviceToHost, st));
         s->rec_prev_P.resize(V);
@@ -755,8 +785,8 @@ int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const f
             PF_CUDA(cudaMallocHost(&s->pinned_seg, sizeof(uint32_t) * (size_t)(V + 16)));
             s->pinned_seg_n = V + 16;
         }
-        PF_CUDA(cudaMemcpyAsync(s->pinned_seg, s->rec_used.as<uint32_t>() + V,
-                                sizeof(uint32_t) * (size_t)V, cudaMemcpyDeviceToHost, st));
+        PF_CUDA(pf::small_copy(s, s->pinned_seg, s->rec_used.as<uint32_t>() + V,
+                               sizeof(uint32_t) * (size_t)V, st));
         PF_CUDA(cudaStreamSynchronize(st));
         for (int v = 0; v < V; ++v) s->views[v].nseg = s->pinned_seg[v];
         const int64_t cap = pf::detail_items_needed(s, s->views.data(), V);

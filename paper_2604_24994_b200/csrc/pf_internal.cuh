@@ -164,6 +164,8 @@ struct pf_scene {
     int32_t fwd_views = 0;          // views saved by the last forward
     int64_t *pinned = nullptr;      // pinned host readback of pair totals
     int pinned_n = 0;
+    int *pinned_hb = nullptr;       // pinned host readback of the per-block visible counts
+    size_t pinned_hb_n = 0;
     int64_t launches = 0;
     bool profiling = false;
     cudaStream_t side = nullptr;    // K0 of a training forward runs here, beside K1-K5
@@ -227,6 +229,10 @@ cudaError_t launch_trace(pf_scene *s, const BallBVH &bvh, const CamParams &cam, 
                          unsigned long long *stats, cudaStream_t st);
 cudaError_t launch_unpack(pf_scene *s, float *gs, float *gw, float *gr, float *gd, float *gc,
                           float *gn, cudaStream_t st);
+
+// small transfers without the copy engines: a one-block kernel copying 4-byte words
+// between device and pinned host memory (pf_api.cu)
+cudaError_t small_copy(pf_scene *s, void *dst, const void *src, size_t bytes, cudaStream_t st);
 
 // stage timing helpers (pf_api.cu)
 void stage_begin(pf_scene *s, int stage, cudaStream_t st, cudaEvent_t *ev);
