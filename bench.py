@@ -708,11 +708,12 @@ def main():
     n_vis = float((bcount > 0).sum().item())
     # depth-first binning (DESIGN 6, K4): per sort batch of <= 8 views, the visible
     # cells are radix-sorted by (view, depth key) over 32 + view bits, then the pairs by
-    # (view, tile) over tile + view bits with 32-bit keys; algorithmic bytes per item
-    # and pass: cells 8 (histogram key read) + 12 read + 12 write, pairs 4 + 8 + 8
+    # (view, tile) over tile + view bits with 32-bit keys (9- and 8-bit digits);
+    # algorithmic bytes per item and pass: cells 8 (histogram key read) + 12 read + 12
+    # write, pairs 4 + 8 + 8
     vbits = math.ceil(math.log2(min(nv, 8))) if nv > 1 else 0
     tbits = math.ceil(math.log2((W + 15) // 16 * ((H + 15) // 16)))
-    passes_cells = math.ceil((32 + vbits) / 8)
+    passes_cells = math.ceil((32 + vbits) / 9)          # 9-bit digits (PF_SORT_BITS_WIDE)
     passes_pairs = math.ceil((tbits + vbits) / 8)
     sort_bytes = 32.0 * n_vis * nv * passes_cells + 20.0 * P * nv * passes_pairs
     sort_ms_step = sort_ms / args.steps

@@ -1101,6 +1101,9 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
 #ifndef PF_K7D_MINB_REPLAY   // split detail K7 (replay + colour + items): CTAs per SM
 #define PF_K7D_MINB_REPLAY 3
 #endif
+#ifndef PF_K7D_PREFETCH   // K7D: the next batch's item loaded one iteration ahead
+#define PF_K7D_PREFETCH 1
+#endif
 #ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
 #define PF_K7D_MINB_CHAIN 2
 #endif
@@ -1120,14 +1123,24 @@ k7d_detail_chain(DeviceScene ds, const ViewArgs *__restrict__ va, DetailItems DI
     float (*gbuf)[kChainRow] = buf + 32;
     const int K = KT == 8 ? 8 : ds.K;
     const uint32_t n = min(*DI.used, DI.cap);
-    for (uint32_t base = (blockIdx.x * kWarps + warp) * 32u; base < n;
-         base += gridDim.x * kWarps * 32u) {
+    const uint32_t stride = gridDim.x * kWarps * 32u;
+    uint32_t base = (blockIdx.x * kWarps + warp) * 32u;
+    // the next batch's item is loaded while this one is processed (the chain starts
+    // with a dependent walk: item -> view, pixel, cell -> their records)
+    uint4 itn = (PF_K7D_PREFETCH && base + lane < n) ? DI.it[base + lane] : make_uint4(0u, 0u, 0u, 0u);
+    for (; base < n; base += stride) {
         const uint32_t i = base + (uint32_t)lane;
         const bool seg = i < n;
+        uint4 it;
+        if (PF_K7D_PREFETCH) {
+            it = itn;
+            if (base + stride + lane < n) itn = DI.it[base + stride + lane];
+        } else {
+            it = seg ? DI.it[i] : make_uint4(0u, 0u, 0u, 0u);
+        }
         uint32_t cell = 0xffffffffu;
         OwnGrad o = {0, 0, 0, 0, 0, 0, 0, 0};
         if (seg) {
-            const uint4 it = DI.it[i];
             cell = it.x;
             const float wa = __uint_as_float(it.z), g_ts = __uint_as_float(it.w);
             const ViewArgs &V = va[it.y >> 25];
