@@ -522,9 +522,34 @@ k2_rescan(const int *__restrict__ cnt, int64_t n, const long long *__restrict__ 
     }
 }
 
+// small inputs (the per-block visible counts of a batch, a few thousand entries):
+// one block walks the array in 1024-item steps with a running carry (one launch
+// instead of three)
+constexpr int64_t kScanSmall = 1 << 15;
+__global__ void __launch_bounds__(1024) k2_scan_small(const int *__restrict__ cnt, int n,
+                                                      uint32_t *__restrict__ offs, long long *total)
+{
+    __shared__ long long sw[33];
+    long long carry = 0;
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + threadIdx.x;
+        const long long v = i < n ? cnt[i] : 0;
+        long long tot;
+        const long long ex = block_excl_scan<long long>(v, sw, &tot);
+        if (i < n) offs[i] = (uint32_t)(ex + carry);
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
 cudaError_t exclusive_scan_counts(pf_scene *s, const int *cnt, int64_t n, uint32_t *offs,
                                   long long *d_total, cudaStream_t st)
 {
+    if (n <= kScanSmall) {
+        k2_scan_small<<<1, 1024, 0, st>>>(cnt, (int)n, offs, d_total);
+        ++s->launches;
+        return cudaGetLastError();
+    }
     int nb = ceil_div(n, kScanChunk);
     cudaError_t err = s->scan_tmp.reserve(sizeof(long long) * (size_t)(nb + 1));
     if (err != cudaSuccess) return err;

@@ -1101,8 +1101,8 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
 #ifndef PF_K7D_MINB_REPLAY   // split detail K7 (replay + colour + items): CTAs per SM
 #define PF_K7D_MINB_REPLAY 3
 #endif
-#ifndef PF_K7D_PREFETCH   // K7D: the next batch's item loaded one iteration ahead
-#define PF_K7D_PREFETCH 1
+#ifndef PF_K7D_PREFETCH   // K7D: next item one iteration ahead (measured: within noise, off)
+#define PF_K7D_PREFETCH 0
 #endif
 #ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
 #define PF_K7D_MINB_CHAIN 2
