@@ -1104,6 +1104,9 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
 #ifndef PF_K7D_PREFETCH   // K7D: next item one iteration ahead (measured: within noise, off)
 #define PF_K7D_PREFETCH 0
 #endif
+#ifndef PF_K7D_RUNFAST   // K7D column sums: counted loop over a contiguous run of lanes
+#define PF_K7D_RUNFAST 1
+#endif
 #ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
 #define PF_K7D_MINB_CHAIN 2
 #endif
@@ -1215,8 +1218,7 @@ k7d_detail_chain(DeviceScene ds, const ViewArgs *__restrict__ va, DetailItems DI
             const int k = lane >> 2, ac0 = (lane & 3) * 6;
             float2 a0 = make_float2(0.0f, 0.0f), a1 = a0, a2 = a0;
             float t = 0.0f;
-            for (unsigned mm = segm; mm; mm &= mm - 1) {
-                const int l = __ffs(mm) - 1;
+            auto add_item = [&](int l) {
                 const float wk = buf[l][k];
                 const float2 *row = reinterpret_cast<const float2 *>(&buf[l][8 + ac0]);
                 const float2 b0 = row[0], b1 = row[1], b2 = row[2];
@@ -1224,6 +1226,13 @@ k7d_detail_chain(DeviceScene ds, const ViewArgs *__restrict__ va, DetailItems DI
                 a1.x = fmaf(wk, b1.x, a1.x); a1.y = fmaf(wk, b1.y, a1.y);
                 a2.x = fmaf(wk, b2.x, a2.x); a2.y = fmaf(wk, b2.y, a2.y);
                 t += gbuf[l][lane];
+            };
+            const int l0 = __ffs(segm) - 1, nrun = __popc(segm);
+            if (PF_K7D_RUNFAST && (segm >> l0) == (nrun == 32 ? 0xffffffffu : (1u << nrun) - 1u)) {
+                // a contiguous run of lanes (the common case): a plain counted loop
+                for (int l = l0; l < l0 + nrun; ++l) add_item(l);
+            } else {
+                for (unsigned mm = segm; mm; mm &= mm - 1) add_item(__ffs(mm) - 1);
             }
             if (k < K && ds.g_sv) {
                 float2 *dst = reinterpret_cast<float2 *>(ds.g_sv + ((size_t)K * cr + k) * 24 + ac0);
