@@ -673,6 +673,109 @@ __device__ __forceinline__ float4 detail_plane(const DeviceScene &ds, uint32_t c
     return make_float4(__double2float_rn(m0), __double2float_rn(m1), __double2float_rn(m2), G.delta);
 }
 
+// detail_plane for the lanes of one cell at once (K6, every lane calls it; `pre`
+// lanes want the face).  The fp64 chart runs per lane as in detail_plane; the
+// soft-Voronoi weights at the base-face hit are spread over the warp, lane 8g + k
+// taking site k of the g-th wanting lane (up to 4 lanes per round): the same per-site
+// operations, the argmin with detail_plane's first-minimum tie rule, then each lane
+// gathers its 8 weights and normalises / blends them in site order -- bit-identical to
+// detail_plane (delta, ts; G.w is not produced: K6 does not use it).
+template <int KT>
+__device__ __forceinline__ float4 detail_plane_warp(const DeviceScene &ds, uint32_t cell, bool pre,
+                                                    const double d[3], const double c[3], float r,
+                                                    DetailGeo &G, int lane)
+{
+    const double *F = ds.cellF + (size_t)kCellF * cell;
+    const double m0 = __ldg(F), m1 = __ldg(F + 1), m2 = __ldg(F + 2);
+    float q0f = 0.0f, q1f = 0.0f;
+    double B = 0.0, iA = 0.0;
+    G.delta = 0.0f;
+    G.dr = 0.0f;
+    G.ts = 0.0;
+    G.parallel = true;
+    if (pre) {
+        G.A = dot3d(d, m0, m1, m2);
+        B = dot3d(c, m0, m1, m2);
+        G.parallel = (G.A == 0.0);
+        if (!G.parallel) {
+            iA = __drcp_rn(G.A);
+            const double tb = __dmul_rn(B, iA);
+            const double y0 = __fma_rn(tb, d[0], -c[0]), y1 = __fma_rn(tb, d[1], -c[1]),
+                         y2 = __fma_rn(tb, d[2], -c[2]);
+            const double q0 = __fma_rn(y0, __ldg(F + 3), __fma_rn(y1, __ldg(F + 4), __dmul_rn(y2, __ldg(F + 5))));
+            const double q1 = __fma_rn(y0, __ldg(F + 6), __fma_rn(y1, __ldg(F + 7), __dmul_rn(y2, __ldg(F + 8))));
+            q0f = __double2float_rn(q0);
+            q1f = __double2float_rn(q1);
+        }
+    }
+    const int K = KT == 8 ? 8 : ds.K;
+    const int k = lane & 7, gbase = lane & ~7;
+    const float2 sk = k < K ? __ldg(reinterpret_cast<const float2 *>(ds.duv) + (size_t)K * cell + k)
+                            : make_float2(0.0f, 0.0f);
+    const float *dk = ds.ddisp + (size_t)K * cell;
+    const float tau = ds.sv_tau;
+    unsigned want = __ballot_sync(0xffffffffu, pre && !G.parallel);
+    while (want) {
+        // this round: the first (up to) 4 wanting lanes, group g = lane / 8 serves the g-th
+        const int g = lane >> 3;
+        unsigned rest = want, mg = 0u;   // rest: want without its 4 lowest set bits
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (i == g) mg = rest;       // want without its g lowest set bits
+            rest &= rest - 1u;
+        }
+        const int src = mg ? __ffs(mg) - 1 : lane;
+        const unsigned round = want & ~rest;
+        want = rest;
+        const float qa = __shfl_sync(0xffffffffu, q0f, src), qb = __shfl_sync(0xffffffffu, q1f, src);
+        const float dx = qa - sk.x, dy = qb - sk.y;
+        const float r2 = k < K ? fmaf(dx, dx, dy * dy) : 3.0e38f;
+        // argmin over the group's 8 sites, ties to the lower site index
+        float mr = r2;
+        int mk = k;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const float orr = __shfl_xor_sync(0xffffffffu, mr, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, mk, o);
+            if (orr < mr || (orr == mr && ok < mk)) {
+                mr = orr;
+                mk = ok;
+            }
+        }
+        const float jx = __shfl_sync(0xffffffffu, sk.x, gbase | mk),
+                    jy = __shfl_sync(0xffffffffu, sk.y, gbase | mk);
+        const float rj = sqrt_approx(mr), tx = fmaf(2.0f, qa, -jx), ty = fmaf(2.0f, qb, -jy);
+        float w = 0.0f;
+        if (k < K) {
+            const float num = fmaf(jx - sk.x, tx - sk.x, (jy - sk.y) * (ty - sk.y));
+            const float den = sqrt_approx(r2) + rj;
+            const float diff = den > 0.0f ? num * rcp_approx(den) : 0.0f;
+            w = __expf(-tau * diff);
+        }
+        // each wanting lane of the round gathers its group's weights in site order
+        const bool mine = (round >> lane) & 1u;
+        const int gme = __popc(round & ((1u << lane) - 1u));
+        float wk[kMaxDetail];
+        float sum = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < kMaxDetail; ++kk) {
+            wk[kk] = __shfl_sync(0xffffffffu, w, ((mine ? gme : 0) << 3) | kk);
+            if (kk < K) sum += wk[kk];
+        }
+        if (mine) {
+            const float inv = rcp_approx(sum);
+            float dr = 0.0f;
+#pragma unroll
+            for (int kk = 0; kk < kMaxDetail; ++kk)
+                if (kk < K) dr = fmaf(wk[kk] * inv, __ldg(dk + kk), dr);
+            G.dr = dr;
+            G.delta = fminf(fmaxf(dr, -r), r);
+            G.ts = __dmul_rn(__dadd_rn(B, (double)G.delta), iA);
+        }
+    }
+    return make_float4(__double2float_rn(m0), __double2float_rn(m1), __double2float_rn(m2), G.delta);
+}
+
 // Eq. svrad at the point Q + t d (t = the displaced-face hit, or the interval
 // entry for a parallel ray): sum_k w_k sum_a om_a v_{k,a}
 template <int KT>

@@ -73,6 +73,9 @@ constexpr int kFuseTiles = 4096;   // views with fewer tiles: one fused K6 / K7 
 // device array into shared memory (small views: no per-view launch tails); else
 // one launch per view with its ViewArgs by value (constant-bank operands; measured
 // faster for 1080p views, whose launches are ~14 waves long)
+#ifndef PF_K6D_WARPSV   // detail K6: the chart's soft-Voronoi weights spread over the warp
+#define PF_K6D_WARPSV 1
+#endif
 #ifndef PF_K6D_QUEUE   // detail K6: segment colours evaluated 32 at a time (ColQueue)
 #define PF_K6D_QUEUE 1
 #endif
@@ -219,7 +222,12 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
                     clip_interval<kRecord, false>(P.R, ds.edges, S.eb[j], S.deg[j], g, hit, dpl);
                 const bool pre = g.dt > 0.0f;
                 if (__any_sync(0xffffffffu, pre)) {
-                    if (pre) {
+                    if (PF_K6D_WARPSV) {   // the chart's soft-Voronoi spread over the warp
+                        dd[0] = PR.dx[threadIdx.x]; dd[1] = PR.dy[threadIdx.x]; dd[2] = PR.dz[threadIdx.x];
+                        cell_c(ds, cam, S.cell[j], dc);
+                        const float4 f = detail_plane_warp<kDetail>(ds, S.cell[j], pre, dd, dc, S.r[j], G, lane);
+                        if (pre) dpl = f;
+                    } else if (pre) {
                         dd[0] = PR.dx[threadIdx.x]; dd[1] = PR.dy[threadIdx.x]; dd[2] = PR.dz[threadIdx.x];
                         cell_c(ds, cam, S.cell[j], dc);
                         dpl = detail_plane<kDetail>(ds, S.cell[j], dd, dc, S.r[j], G);
@@ -1104,8 +1112,8 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
 #ifndef PF_K7D_PREFETCH   // K7D: next item one iteration ahead (measured: within noise, off)
 #define PF_K7D_PREFETCH 0
 #endif
-#ifndef PF_K7D_RUNFAST   // K7D column sums: counted loop over a contiguous run of lanes
-#define PF_K7D_RUNFAST 1
+#ifndef PF_K7D_RUNFAST   // K7D column sums: counted loop over contiguous runs (measured slower: 21.9 -> 22.6 ms, off)
+#define PF_K7D_RUNFAST 0
 #endif
 #ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
 #define PF_K7D_MINB_CHAIN 2
