@@ -187,7 +187,14 @@ typedef struct {
     float *detail_sv;   /* [N,K,8,3] or NULL; 8-byte aligned */
 } pf_grads;
 
-/* pf_render_backward with the gradient arrays in a struct (adds dL/d normals). */
+/* pf_render_backward with the gradient arrays in a struct (adds dL/d normals).
+ * Detail scenes (num_detail > 0): the backward runs as a replay of the forward's
+ * records (K7) that emits one work item per detail segment, then the detail chain
+ * of P:284-293 over the items (K7D); the item arena is sized from the segment count
+ * the forward recorded, read with ONE stream synchronisation at the start of the
+ * call.  Limits there: width * height < 2^25 and num_views <= 128
+ * (PF_ERR_INVALID_ARGUMENT otherwise).  With PF_VALIDATE the call synchronises once
+ * more at its end and checks that every item fitted its arena (PF_ERR_STATE). */
 PF_API int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t num_views,
                                  const float *grad_out, const pf_grads *grads, pf_stream_t stream);
 

@@ -810,6 +810,16 @@ int pf_render_backward_ex(pf_scene *s, const pf_camera *cams, int32_t V, const f
     }
     s->ds.g_uv = s->ds.g_disp = s->ds.g_sv = nullptr;
     if (brc != PF_OK) return brc;
+    if (s->ds.K && (s->flags & PF_VALIDATE) && pf::detail_items_needed(s, s->views.data(), V) > 0) {
+        // every K7 item must have fitted the arena sized from the forward's segment
+        // count (the replay finds exactly the recorded segments)
+        PF_CUDA(pf::small_copy(s, s->pinned_seg, s->item_cnt.ptr, sizeof(uint32_t) * (size_t)V, st));
+        PF_CUDA(cudaStreamSynchronize(st));
+        const int64_t cap = pf::detail_items_needed(s, s->views.data(), V);
+        for (int v = 0; v < V; ++v)
+            if ((int64_t)s->pinned_seg[v] > cap)
+                return fail(PF_ERR_STATE, "detail backward: more K7 items than the forward recorded segments");
+    }
     PF_CUDA(pf::launch_unpack(s, g->sites, g->weights, g->radii, g->density, g->rgb,
                               s->ds.cellN ? g->normals : nullptr, st));
     return PF_OK;

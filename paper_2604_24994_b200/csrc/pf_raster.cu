@@ -73,8 +73,12 @@ constexpr int kFuseTiles = 4096;   // views with fewer tiles: one fused K6 / K7 
 // device array into shared memory (small views: no per-view launch tails); else
 // one launch per view with its ViewArgs by value (constant-bank operands; measured
 // faster for 1080p views, whose launches are ~14 waves long)
-#ifndef PF_K6D_WARPSV   // detail K6: the chart's soft-Voronoi weights spread over the warp
-#define PF_K6D_WARPSV 1
+// detail K6: the chart's soft-Voronoi weights spread over the warp (detail_plane_warp).
+// Bit-identical, but measured slower (nerfsynth200k+detail8 K6 15.8 -> 20.4 ms): a hit
+// cell holds ~18 of the warp's 32 rays, so the lockstep chart is half-used already and
+// the spread version needs ~5 rounds of shuffles per cell. Off.
+#ifndef PF_K6D_WARPSV
+#define PF_K6D_WARPSV 0
 #endif
 #ifndef PF_K6D_QUEUE   // detail K6: segment colours evaluated 32 at a time (ColQueue)
 #define PF_K6D_QUEUE 1
