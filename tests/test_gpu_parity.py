@@ -2,6 +2,8 @@
 the same seeded inputs.  Bars (BASELINE.json north_star):
 binning bit-exact; images <= 1e-4 abs per fp32 channel; gradients <= 1e-3
 relative (normwise per array)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -979,3 +981,33 @@ def test_fused_and_per_view_launches_agree(monkeypatch):
     for k, a in res["0"][1].items():
         b = res["1"][1][k]
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
+
+
+def test_detail_colour_queue_bit_identical(tmp_path):
+    """K6's deferred colour evaluation (ColQueue, DESIGN §13 item 4) composites every
+    pixel's colours in list order with composite_step's fmaf: the image must be
+    bit-identical to the in-line evaluation (a PF_K6D_QUEUE=0 build of the same
+    sources, run in a subprocess), for K = 8 and a generic K."""
+    import subprocess
+    import sys
+    from paper_2604_24994_b200 import _build
+    lib = _build.build(out=str(tmp_path / "q0.so"), defines=("PF_K6D_QUEUE=0",))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for name, K in (("small360", 8), ("small", 3)):
+        sc = pf_synth.add_detail(pf_synth.make_scene(name), K=K, seed=5)
+        cams = pf_synth.make_cameras(name)[:2]
+        r = renderer(sc, flags=0)
+        ref = r.forward(cams).cpu().numpy()
+        r.close()
+        dump = str(tmp_path / f"{name}.npy")
+        code = ("import sys, numpy as np; sys.path.insert(0, %r); import pf_synth; "
+                "import paper_2604_24994_b200 as pf; "
+                "sc = pf_synth.add_detail(pf_synth.make_scene(%r), K=%d, seed=5); "
+                "cams = pf_synth.make_cameras(%r)[:2]; "
+                "r = pf.Renderer.from_scene(sc, 'cuda:0'); "
+                "np.save(%r, r.forward(cams).cpu().numpy())") % (root, name, K, name, dump)
+        out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "PF_LIBRARY_PATH": lib},
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        got = np.load(dump)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), name
