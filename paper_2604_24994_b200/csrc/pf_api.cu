@@ -566,6 +566,7 @@ int pf_destroy(pf_scene *s)
     s->keys1.release();
     s->vals1.release();
     s->sort_hist.release();
+    s->sort_status.release();
     s->scan_tmp.release();
     s->scan_totals.release();
     s->acc.release();

@@ -142,6 +142,7 @@ struct pf_scene {
     bool edges_built = false;
     // sort / emit scratch
     pf::DevBuf keys0, keys1, vals1, sort_hist, scan_tmp, scan_totals;
+    pf::DevBuf sort_status;         // onesweep: digit histograms, tickets, look-back status
     pf::DevBuf vals_all, ranges_all;   // sorted pairs of all views of the last call
     pf::DevBuf bvis, bvis_off, ptot;   // visible-cell counts per (view, block), pair totals
     pf::DevBuf ckeys0, ckeys1, cvals0, cvals1, ccnt, coffs;   // visible cells sorted by depth

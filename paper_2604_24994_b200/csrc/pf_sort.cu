@@ -74,11 +74,21 @@ constexpr size_t scatter_smem()
            (size_t)kSortWarps * kRadix * sizeof(uint32_t) + 2 * kRadix * sizeof(uint32_t);
 }
 
-template <class KeyT, int kRadixBits>
+// Onesweep mode (kOne): the block takes its partition from a ticket counter (so a
+// partition only ever waits on partitions already running), publishes its digit counts,
+// and finds each digit's exclusive prefix over the earlier partitions by decoupled
+// look-back on `status` ([partition][digit]: count | flag; kAgg = this partition's
+// count, kPre = inclusive prefix); the digit's global start comes from the one
+// upfront histogram of every pass (k4_hist_all).  Without kOne: per-pass histogram +
+// scan offsets (digit_offs[digit * nb + block]).
+constexpr uint32_t kAgg = 1u << 30, kPre = 2u << 30, kValMask = kAgg - 1u;
+
+template <class KeyT, int kRadixBits, bool kOne = false>
 __global__ void __launch_bounds__(kSortThreads)
 k4_scatter(const KeyT *__restrict__ kin, const uint32_t *__restrict__ vin, KeyT *__restrict__ kout,
            uint32_t *__restrict__ vout, int64_t n, int shift, int nb,
-           const uint32_t *__restrict__ digit_offs)
+           const uint32_t *__restrict__ digit_offs, uint32_t *status = nullptr,
+           uint32_t *ticket = nullptr)
 {
     constexpr int kRadix = 1 << kRadixBits;
     extern __shared__ __align__(16) unsigned char sort_smem[];
@@ -87,11 +97,14 @@ k4_scatter(const KeyT *__restrict__ kin, const uint32_t *__restrict__ vin, KeyT 
     uint32_t(*wh)[kRadix] = reinterpret_cast<uint32_t(*)[kRadix]>(sv + kSortTile);
     uint32_t *dstart = reinterpret_cast<uint32_t *>(wh + kSortWarps);
     uint32_t *gbase = dstart + kRadix;
+    __shared__ int part_s;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (kOne && threadIdx.x == 0) part_s = (int)atomicAdd(ticket, 1u);
     for (int q = threadIdx.x; q < kSortWarps * kRadix; q += kSortThreads) (&wh[0][0])[q] = 0;
     __syncthreads();
+    const int part = kOne ? part_s : (int)blockIdx.x;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const int64_t bbase = (int64_t)blockIdx.x * kSortTile;
+    const int64_t bbase = (int64_t)part * kSortTile;
     const int64_t wbase = bbase + (int64_t)warp * (32 * kSortItems);
     KeyT key[kSortItems];
     uint32_t val[kSortItems], rank[kSortItems];
@@ -127,7 +140,27 @@ k4_scatter(const KeyT *__restrict__ kin, const uint32_t *__restrict__ vin, KeyT 
             run += c;
         }
         dstart[d] = run;
-        gbase[d] = digit_offs[(int64_t)d * nb + blockIdx.x];
+        if (kOne) {
+            uint32_t *st = status + (size_t)part * kRadix + d;
+            if (part == 0) {
+                atomicExch(st, run | kPre);
+                gbase[d] = digit_offs[d];
+            } else {
+                atomicExch(st, run | kAgg);
+                uint32_t excl = 0;
+                for (int j = part - 1; j >= 0;) {
+                    const uint32_t v = __ldcv(status + (size_t)j * kRadix + d);
+                    if (!(v & (kAgg | kPre))) continue;   // partition j not published yet
+                    excl += v & kValMask;
+                    if (v & kPre) break;
+                    --j;
+                }
+                atomicExch(st, (excl + run) | kPre);
+                gbase[d] = digit_offs[d] + excl;
+            }
+        } else {
+            gbase[d] = digit_offs[(int64_t)d * nb + blockIdx.x];
+        }
     }
     __syncthreads();
     if (warp == 0) {   // exclusive scan of the digit totals (kRadix / 32 per lane)
@@ -170,6 +203,82 @@ k4_scatter(const KeyT *__restrict__ kin, const uint32_t *__restrict__ vin, KeyT 
     }
 }
 
+// Onesweep: the digit histograms of every pass in one read of the keys
+template <class KeyT, int kRadixBits>
+__global__ void __launch_bounds__(kSortThreads)
+k4_hist_all(const KeyT *__restrict__ keys, int64_t n, int npass, uint32_t *__restrict__ ghist)
+{
+    constexpr int kRadix = 1 << kRadixBits, kMaxPass = (int)(8 * sizeof(KeyT) + kRadixBits - 1) / kRadixBits;
+    __shared__ uint32_t h[kMaxPass][kRadix];
+    for (int q = threadIdx.x; q < kMaxPass * kRadix; q += kSortThreads) (&h[0][0])[q] = 0u;
+    __syncthreads();
+    // warp-aggregated: the high digits take few values (view bits, float order
+    // bits), so per-key shared atomics would serialise on a handful of bins
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t base = ((int64_t)blockIdx.x * kSortWarps + warp) * 32; base < n;
+         base += (int64_t)gridDim.x * kSortThreads) {
+        const int64_t i = base + lane;
+        const bool valid = i < n;
+        const KeyT k = valid ? keys[i] : KeyT(0);
+        for (int p = 0; p < npass; ++p) {
+            const int d = valid ? (int)((k >> (p * kRadixBits)) & (kRadix - 1)) : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (valid && lane == __ffs(peers) - 1) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < npass * kRadix; q += kSortThreads) {
+        const uint32_t c = (&h[0][0])[q];
+        if (c) atomicAdd(ghist + q, c);
+    }
+}
+
+// exclusive scan of each pass's kRadix digit counts (block p = pass p, in place)
+template <int kRadixBits>
+__global__ void __launch_bounds__(kSortThreads) k4_scan_digits(uint32_t *__restrict__ ghist)
+{
+    constexpr int kRadix = 1 << kRadixBits, kPer = (kRadix + kSortThreads - 1) / kSortThreads;
+    __shared__ uint32_t ws[kSortWarps];
+    uint32_t *g = ghist + (size_t)blockIdx.x * kRadix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int d = threadIdx.x * kPer + q;
+        v[q] = d < kRadix ? g[d] : 0u;
+        sum += v[q];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kSortWarps ? ws[lane] : 0u, wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < kSortWarps) ws[lane] = wi - w;
+    }
+    __syncthreads();
+    uint32_t run = inc - sum + ws[warp];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int d = threadIdx.x * kPer + q;
+        if (d < kRadix) g[d] = run;
+        run += v[q];
+    }
+}
+
+#ifndef PF_SORT_ONESWEEP   // 1: upfront histograms + decoupled look-back scatter per pass
+#define PF_SORT_ONESWEEP 1
+#endif
+
 template <class KeyT, int kRadixBits>
 static cudaError_t radix_sort_t(pf_scene *s, KeyT *keys, uint32_t *vals, KeyT *keys_alt,
                                 uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
@@ -193,6 +302,38 @@ static cudaError_t radix_sort_t(pf_scene *s, KeyT *keys, uint32_t *vals, KeyT *k
     constexpr size_t smem = scatter_smem<KeyT, kRadixBits>();
     cudaFuncSetAttribute(k4_scatter<KeyT, kRadixBits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    const int npass = (end_bit + kRadixBits - 1) / kRadixBits;
+    if (PF_SORT_ONESWEEP && n < (int64_t)kValMask) {
+        // ghist [npass][kRadix] | tickets [npass] | status [npass][nb][kRadix], zeroed at once
+        const size_t words = (size_t)npass * kRadix + npass + (size_t)npass * nb * kRadix;
+        err = s->sort_status.reserve(words * sizeof(uint32_t));
+        if (err != cudaSuccess) return err;
+        uint32_t *ghist = s->sort_status.as<uint32_t>(), *tick = ghist + (size_t)npass * kRadix,
+                 *status = tick + npass;
+        cudaFuncSetAttribute(k4_scatter<KeyT, kRadixBits, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        stage_begin(s, 4, st, &ev);
+        err = cudaMemsetAsync(ghist, 0, words * sizeof(uint32_t), st);
+        if (err != cudaSuccess) return err;
+        const int hb = nb < 1184 ? nb : 1184;   // 8 blocks per SM, grid-stride
+        k4_hist_all<KeyT, kRadixBits><<<hb, kSortThreads, 0, st>>>(keys, n, npass, ghist);
+        k4_scan_digits<kRadixBits><<<npass, kSortThreads, 0, st>>>(ghist);
+        s->launches += 2;
+        for (int p = 0; p < npass; ++p) {
+            k4_scatter<KeyT, kRadixBits, true><<<nb, kSortThreads, smem, st>>>(
+                ka, va, kb, vb, n, p * kRadixBits, nb, ghist + (size_t)p * kRadix,
+                status + (size_t)p * nb * kRadix, tick + p);
+            ++s->launches;
+            err = cudaGetLastError();
+            if (err != cudaSuccess) return err;
+            KeyT *tk = ka; ka = kb; kb = tk;
+            uint32_t *tv = va; va = vb; vb = tv;
+            alt = !alt;
+        }
+        stage_end(s, 4, st, ev);
+        *result_in_alt = alt;
+        return cudaGetLastError();
+    }
     stage_begin(s, 4, st, &ev);
     for (int shift = 0; shift < end_bit; shift += kRadixBits) {
         k4_histogram<KeyT, kRadixBits><<<nb, kSortThreads, 0, st>>>(ka, n, shift, nb, hist);
