@@ -275,8 +275,13 @@ __global__ void __launch_bounds__(kSortThreads) k4_scan_digits(uint32_t *__restr
     }
 }
 
-#ifndef PF_SORT_ONESWEEP   // 1: upfront histograms + decoupled look-back scatter per pass
-#define PF_SORT_ONESWEEP 1
+// 1: upfront histograms of every pass + a decoupled look-back scatter per pass (no
+// per-pass histogram / scan launches).  Bit-exact (binning and Cech tests pass) but
+// measured slower on B200: train8_1m sort 0.69 -> 0.94 ms per step (one thread per
+// digit walks the look-back partition by partition; ~150-400 partitions are in flight
+// at once, so most walks are long), nerfsynth200k 0.32 -> 0.38 ms.  Off.
+#ifndef PF_SORT_ONESWEEP
+#define PF_SORT_ONESWEEP 0
 #endif
 
 template <class KeyT, int kRadixBits>
