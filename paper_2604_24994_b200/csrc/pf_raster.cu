@@ -1119,6 +1119,9 @@ __device__ __forceinline__ void detail_segment_a(const Ray &R, const Seg &g, boo
 #ifndef PF_K7D_RUNFAST   // K7D column sums: counted loop over contiguous runs (measured slower: 21.9 -> 22.6 ms, off)
 #define PF_K7D_RUNFAST 0
 #endif
+#ifndef PF_K7D_ROWORDER   // split detail K7: row-major tile order (measured: train8 +1.2 ms, nerfsynth -0.2 ms; off)
+#define PF_K7D_ROWORDER 0
+#endif
 #ifndef PF_K7D_MINB_CHAIN   // K7D (the chain, thread per item): CTAs per SM
 #define PF_K7D_MINB_CHAIN 2
 #endif
@@ -1374,7 +1377,10 @@ k7_backward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va,
     __shared__ WarpCtx WC[kWarps];
     __shared__ float4 WN[kDipole ? kWarps * 32 : 1];
     extern __shared__ float dyn_smem[];   // detail variant: [kWarps][32][33] reduction tiles
-    const int tile = (int)VA.order[kFused ? blockIdx.x % ntiles : blockIdx.x], lane = threadIdx.x & 31,
+    // split detail K7: tiles in row-major order, so the K7D items of concurrent CTAs come
+    // from neighbouring tiles (shared cells: L2 reuse in K7D); else the LPT order
+    const int bt = kFused ? (int)(blockIdx.x % ntiles) : (int)blockIdx.x;
+    const int tile = (kSplit && PF_K7D_ROWORDER) ? bt : (int)VA.order[bt], lane = threadIdx.x & 31,
               warp = threadIdx.x >> 5;
     WarpStage &S = WS[warp];
     if (lane == 0) S.nrm = kDipole ? WN + warp * 32 : nullptr;
