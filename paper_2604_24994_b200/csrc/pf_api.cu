@@ -272,10 +272,18 @@ int bin_views_of(pf_scene *s, pf::ViewState *views, int V, cudaStream_t st)
     const int nbx = pf::vis_blocks(s->ds.N);
     PF_CUDA(s->bvis.reserve(sizeof(int) * ((size_t)nbx * V + 16)));
     for (int v = 0; v < V; ++v) {
-        pf::ViewState &vs = views[v];
-        int rc = reserve_view_bins(s, vs);
+        int rc = reserve_view_bins(s, views[v]);
         if (rc) return rc;
-        PF_CUDA(pf::launch_preprocess(s, vs, st));
+    }
+    for (int b0 = 0; b0 < V; b0 += pf::kBatchViews) {
+        const int b1 = (b0 + pf::kBatchViews < V) ? b0 + pf::kBatchViews : V;
+        bool fish = false;
+        for (int v = b0; v < b1; ++v) fish = fish || views[v].cam.model == PF_FISHEYE;
+        if (fish || b1 - b0 == 1) {   // fisheye K1 (tile tests per view), or a single view
+            for (int v = b0; v < b1; ++v) PF_CUDA(pf::launch_preprocess(s, views[v], st));
+        } else {
+            PF_CUDA(pf::launch_preprocess_batch(s, batch_views(views, b0, b1), st));
+        }
     }
     for (int b0 = 0; b0 < V; b0 += pf::kBatchViews) {
         const int b1 = (b0 + pf::kBatchViews < V) ? b0 + pf::kBatchViews : V;

@@ -193,6 +193,8 @@ namespace pf {
 cudaError_t launch_edge_records(pf_scene *s, cudaStream_t st);
 cudaError_t launch_validate(pf_scene *s, int *d_flag, cudaStream_t st);
 cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st);
+// K1 of up to kBatchViews pinhole views in one launch (cells read once)
+cudaError_t launch_preprocess_batch(pf_scene *s, const BatchViews &bv, cudaStream_t st);
 cudaError_t radix_sort_pairs(pf_scene *s, uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                              uint32_t *vals_alt, int64_t n, int end_bit, bool *result_in_alt,
                              cudaStream_t st);

@@ -313,6 +313,40 @@ __device__ __forceinline__ void camera_coords(const CamParams &cam, const float 
         c[k] = (double)M[k] * v0 + (double)M[4 + k] * v1 + (double)M[8 + k] * v2;
 }
 
+// one cell, one pinhole view: tile rect, pair count, key bits (every op a
+// separate IEEE-rn fp32 op, the binning is an fp32 specification)
+__device__ __forceinline__ uint32_t k1_pinhole(const CamParams &cam, float sx, float sy, float sz,
+                                               float w, float r, int4 &rc, int &cnt)
+{
+    const float *M = cam.M;
+    float v0 = __fsub_rn(sx, M[3]);
+    float v1 = __fsub_rn(sy, M[7]);
+    float v2 = __fsub_rn(sz, M[11]);
+    // camera coordinates: c_k = (R_0k v0 + R_1k v1) + R_2k v2
+    float ca = __fadd_rn(__fadd_rn(__fmul_rn(M[0], v0), __fmul_rn(M[4], v1)), __fmul_rn(M[8], v2));
+    float cb = __fadd_rn(__fadd_rn(__fmul_rn(M[1], v0), __fmul_rn(M[5], v1)), __fmul_rn(M[9], v2));
+    float cz = __fadd_rn(__fadd_rn(__fmul_rn(M[2], v0), __fmul_rn(M[6], v1)), __fmul_rn(M[10], v2));
+    // sort key K_i = pow(Q, p_i) = |p_i - Q|^2 - w_i   (Theorem 2, P:596-603)
+    float K = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)),
+                                  __fmul_rn(v2, v2)),
+                        w);
+    rc = make_int4(0, 0, 0, 0);
+    cnt = 0;
+    if ((__fadd_rn(cz, r) > cam.near_plane) && (r > 0.0f)) {
+        bool in_front = __fsub_rn(cz, r) > cam.near_plane;
+        float xlo, xhi, ylo, yhi;
+        sphere_extent(ca, cz, r, cam.fx, cam.cx, cam.near_plane, in_front, xlo, xhi);
+        sphere_extent(cb, cz, r, cam.fy, cam.cy, cam.near_plane, in_front, ylo, yhi);
+        int tx0 = tile_lo(xlo, cam.tiles_x), tx1 = tile_hi(xhi, cam.tiles_x);
+        int ty0 = tile_lo(ylo, cam.tiles_y), ty1 = tile_hi(yhi, cam.tiles_y);
+        if (tx1 > tx0 && ty1 > ty0) {
+            rc = make_int4(tx0, ty0, tx1, ty1);
+            cnt = (tx1 - tx0) * (ty1 - ty0);
+        }
+    }
+    return order_bits(K);
+}
+
 __global__ void __launch_bounds__(256)
 k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights,
               const float *__restrict__ radii, int64_t N, CamParams cam, int4 *__restrict__ rect,
@@ -371,36 +405,44 @@ k1_preprocess(const float *__restrict__ sites, const float *__restrict__ weights
         return;
     }
     if (i >= N) return;
-    const float *M = cam.M;
-    float v0 = __fsub_rn(sites[3 * i + 0], M[3]);
-    float v1 = __fsub_rn(sites[3 * i + 1], M[7]);
-    float v2 = __fsub_rn(sites[3 * i + 2], M[11]);
-    // camera coordinates: c_k = (R_0k v0 + R_1k v1) + R_2k v2
-    float ca = __fadd_rn(__fadd_rn(__fmul_rn(M[0], v0), __fmul_rn(M[4], v1)), __fmul_rn(M[8], v2));
-    float cb = __fadd_rn(__fadd_rn(__fmul_rn(M[1], v0), __fmul_rn(M[5], v1)), __fmul_rn(M[9], v2));
-    float cz = __fadd_rn(__fadd_rn(__fmul_rn(M[2], v0), __fmul_rn(M[6], v1)), __fmul_rn(M[10], v2));
-    // sort key K_i = pow(Q, p_i) = |p_i - Q|^2 - w_i   (Theorem 2, P:596-603)
-    float K = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)),
-                                  __fmul_rn(v2, v2)),
-                        weights[i]);
-    float r = radii[i];
-    keybits[i] = order_bits(K);
-    int4 rc = make_int4(0, 0, 0, 0);
-    int cnt = 0;
-    if ((__fadd_rn(cz, r) > cam.near_plane) && (r > 0.0f)) {
-        bool in_front = __fsub_rn(cz, r) > cam.near_plane;
-        float xlo, xhi, ylo, yhi;
-        sphere_extent(ca, cz, r, cam.fx, cam.cx, cam.near_plane, in_front, xlo, xhi);
-        sphere_extent(cb, cz, r, cam.fy, cam.cy, cam.near_plane, in_front, ylo, yhi);
-        int tx0 = tile_lo(xlo, cam.tiles_x), tx1 = tile_hi(xhi, cam.tiles_x);
-        int ty0 = tile_lo(ylo, cam.tiles_y), ty1 = tile_hi(yhi, cam.tiles_y);
-        if (tx1 > tx0 && ty1 > ty0) {
-            rc = make_int4(tx0, ty0, tx1, ty1);
-            cnt = (tx1 - tx0) * (ty1 - ty0);
-        }
-    }
+    int4 rc;
+    int cnt;
+    keybits[i] = k1_pinhole(cam, sites[3 * i + 0], sites[3 * i + 1], sites[3 * i + 2], weights[i],
+                            radii[i], rc, cnt);
     rect[i] = rc;
     count[i] = cnt;
+}
+
+// K1 of a batch of pinhole views in one launch: each cell's site, weight and radius
+// read once for all views of the batch (the per-view code is k1_pinhole, the same
+// instructions as the one-view kernel: bit-identical binning)
+__global__ void __launch_bounds__(256)
+k1_preprocess_batch(const float *__restrict__ sites, const float *__restrict__ weights,
+                    const float *__restrict__ radii, int64_t N, BatchViews bv)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const float x = sites[3 * i + 0], y = sites[3 * i + 1], z = sites[3 * i + 2];
+    const float w = weights[i], r = radii[i];
+    for (int v = 0; v < bv.n; ++v) {
+        int4 rc;
+        int cnt;
+        const uint32_t kb = k1_pinhole(bv.cam[v], x, y, z, w, r, rc, cnt);
+        const_cast<uint32_t *>(bv.keybits[v])[i] = kb;
+        const_cast<int4 *>(bv.rect[v])[i] = rc;
+        const_cast<int *>(bv.count[v])[i] = cnt;
+    }
+}
+
+cudaError_t launch_preprocess_batch(pf_scene *s, const BatchViews &bv, cudaStream_t st)
+{
+    cudaEvent_t ev;
+    stage_begin(s, 1, st, &ev);
+    k1_preprocess_batch<<<ceil_div(s->ds.N, 256), 256, 0, st>>>(s->ds.sites, s->ds.weights,
+                                                               s->ds.radii, s->ds.N, bv);
+    ++s->launches;
+    stage_end(s, 1, st, ev);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_preprocess(pf_scene *s, ViewState &v, cudaStream_t st)
