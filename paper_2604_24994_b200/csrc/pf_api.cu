@@ -616,6 +616,9 @@ int pf_destroy(pf_scene *s)
     }
     for (auto e : s->event_pool) cudaEventDestroy(e);
     if (s->side) cudaStreamDestroy(s->side);
+    if (s->pair) cudaStreamDestroy(s->pair);
+    if (s->pair_fork) cudaEventDestroy(s->pair_fork);
+    if (s->pair_join) cudaEventDestroy(s->pair_join);
     if (s->side_fork) cudaEventDestroy(s->side_fork);
     if (s->side_join) cudaEventDestroy(s->side_join);
     delete s;
@@ -653,6 +656,9 @@ int pf_render_forward_ex(pf_scene *s, const pf_camera *cams, int32_t V, float *o
                 cudaEventCreateWithFlags(&s->side_join, cudaEventDisableTiming) != cudaSuccess) {
                 cudaGetLastError();
                 if (s->side) cudaStreamDestroy(s->side);
+    if (s->pair) cudaStreamDestroy(s->pair);
+    if (s->pair_fork) cudaEventDestroy(s->pair_fork);
+    if (s->pair_join) cudaEventDestroy(s->pair_join);
                 s->side = nullptr;
             }
         }

@@ -171,6 +171,10 @@ struct pf_scene {
     bool profiling = false;
     cudaStream_t side = nullptr;    // K0 of a training forward runs here, beside K1-K5
     cudaEvent_t side_fork = nullptr, side_join = nullptr;
+    // per-view K6 / K7 launches alternate between the call's stream and this one, so
+    // one view's tail overlaps the next view's start (pf_raster.cu, view_streams)
+    cudaStream_t pair = nullptr;
+    cudaEvent_t pair_fork = nullptr, pair_join = nullptr;
     std::vector<pf::StageEvent> events;
     int64_t stage_l0 = 0;   // s->launches at the open stage's begin
     std::vector<cudaEvent_t> event_pool;

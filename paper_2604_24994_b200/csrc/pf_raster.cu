@@ -386,6 +386,37 @@ k6_forward(DeviceScene ds, const ViewArgs one, const ViewArgs *__restrict__ va, 
     }
 }
 
+#ifndef PF_VIEW_STREAMS   // per-view K6 / K7 launches on two alternating streams
+#define PF_VIEW_STREAMS 1
+#endif
+// The stream of view v's per-view launch: even views on the call's stream, odd ones on
+// the handle's second stream (forked from / joined back into the call's stream by
+// view_streams_begin / _end), so a view's last wave overlaps the next view's first.
+static bool view_streams_begin(pf_scene *s, cudaStream_t st, int V)
+{
+    if (!PF_VIEW_STREAMS || V < 2) return false;
+    if (!s->pair) {
+        if (cudaStreamCreateWithFlags(&s->pair, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->pair_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->pair_join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            if (s->pair) cudaStreamDestroy(s->pair);
+            s->pair = nullptr;
+            return false;
+        }
+    }
+    cudaEventRecord(s->pair_fork, st);
+    cudaStreamWaitEvent(s->pair, s->pair_fork, 0);
+    return true;
+}
+
+static void view_streams_end(pf_scene *s, cudaStream_t st, bool on)
+{
+    if (!on) return;
+    cudaEventRecord(s->pair_join, s->pair);
+    cudaStreamWaitEvent(st, s->pair_join, 0);
+}
+
 template <bool kDipole, int kDetail>
 static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const ViewArgs *args,
                             int64_t *counters, bool record, float *stc, float *stn,
@@ -447,20 +478,23 @@ static int launch_forward_t(pf_scene *s, const ViewState *views, int V, const Vi
         }
         return 1;
     }
+    const bool two = !counters && view_streams_begin(s, st, V);
     for (int v = 0; v < V; ++v) {
+        cudaStream_t sv = (two && (v & 1)) ? s->pair : st;
         if (counters)
-            k6_forward<true, false, kDipole, kDetail><<<T, 256, dynq, st>>>(
+            k6_forward<true, false, kDipole, kDetail><<<T, 256, dynq, sv>>>(
                 s->ds, h[v], nullptr, T, (long long *)counters, nullptr, nullptr, 0);
         else if (record)
-            k6_forward<false, true, kDipole, kDetail><<<T, 256, dyn, st>>>(
+            k6_forward<false, true, kDipole, kDetail><<<T, 256, dyn, sv>>>(
                 s->ds, h[v], nullptr, T, nullptr, stc, stn, s->cull_on);
         else {
             auto kern = k6_forward<false, false, kDipole, kDetail>;
             if constexpr (!kDetail)
                 if (wide) kern = k6_forward<false, false, kDipole, kDetail, true>;
-            kern<<<T, 256, dyn, st>>>(s->ds, h[v], nullptr, T, nullptr, stc, stn, s->cull_on);
+            kern<<<T, 256, dyn, sv>>>(s->ds, h[v], nullptr, T, nullptr, stc, stn, s->cull_on);
         }
     }
+    view_streams_end(s, st, two);
     return V;
 }
 
@@ -1648,13 +1682,18 @@ static int launch_backward_t(pf_scene *s, const ViewState *views, int V, const V
         return 1 + chain(DI, nseg);
     }
     int n = 0;
+    // plain scenes: views alternate between two streams (the split detail backward
+    // shares one item arena between a view's K7 and K7D: one stream)
+    const bool two = !kSplit && view_streams_begin(s, st, V);
     for (int v = 0; v < V; ++v) {
         if (views[v].P == 0) continue;
         const DetailItems DI = items(v, views[v].nseg);
-        k7_backward<kDipole, kDetail, false, kSplit><<<T, 256, smem, st>>>(s->ds, h[v], nullptr, T,
+        cudaStream_t sv = (two && (v & 1)) ? s->pair : st;
+        k7_backward<kDipole, kDetail, false, kSplit><<<T, 256, smem, sv>>>(s->ds, h[v], nullptr, T,
                                                                            acc, v, DI);
         n += 1 + chain(DI, views[v].nseg);
     }
+    view_streams_end(s, st, two);
     return n;
 }
 
