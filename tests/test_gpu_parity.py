@@ -757,6 +757,21 @@ def test_detail_colour_slots_overflow(monkeypatch, ratio):
     _full_parity(sc, cams[:1], oracle.O3, seed=29)
 
 
+def test_detail_per_view_launches(monkeypatch):
+    """The per-view launch path of 1080p views (K6 on two alternating streams, K7 and
+    K7D per view) forced on a small scene (PF_K6_PER_VIEW=1): parity with the oracle
+    unchanged."""
+    monkeypatch.setenv("PF_K6_PER_VIEW", "1")
+    sc, cams = case("small360+detail")
+    _full_parity(sc, cams[:3], oracle.O3, seed=31)
+
+
+def test_per_view_launches_plain(monkeypatch):
+    monkeypatch.setenv("PF_K6_PER_VIEW", "1")
+    sc, cams = case("small360")
+    _full_parity(sc, cams[:3], oracle.O3, seed=37)
+
+
 def test_detail_autograd_and_by_products():
     """torch.autograd through the detail parameters equals the explicit backward;
     by-products (sum T alpha) match the oracle's."""
