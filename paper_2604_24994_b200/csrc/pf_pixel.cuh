@@ -15,6 +15,16 @@
 #ifndef PF_RAY_FAST   // pixel rays without fp64 divides (ray_dir)
 #define PF_RAY_FAST 1
 #endif
+#ifndef PF_K6_POSTRACK   // K6 kept-plane loop: track kept positions, map to list indices once
+                         // (measured: recording K6 11.71 -> 11.22 ms per 8 train8_1m views)
+#define PF_K6_POSTRACK 1
+#endif
+#ifndef PF_PREDTRACK   // tracked plane clip (K6 recording, K7): predicated moves, not min/max
+#define PF_PREDTRACK 0
+#endif
+#ifndef PF_K6_KEPT_UNROLL4   // (with PF_K6_POSTRACK) kept-plane loop unrolled by 4
+#define PF_K6_KEPT_UNROLL4 0
+#endif
 
 namespace pf {
 
@@ -189,6 +199,17 @@ __device__ __forceinline__ void clip_plane(const Ray &R, const float4 E, int q, 
     const float b = fmaf(E.x, g.ex, fmaf(E.y, g.ey, fmaf(E.z, g.ez, E.w)));
     const float t = __fmul_rn(b, rcp_approx(a));
     const bool up = a >= 0.0f;
+    if (kTrack && PF_PREDTRACK) {
+        // the bound moves iff t is strictly inside it (a NaN t never moves it, as
+        // fminf/fmaxf ignore it); only the sign of a zero bound can differ from the
+        // min/max form below, which leaves dt = hi - lo and the codes unchanged
+        const bool ch = up && t < g.hi, cl = !up && t > g.lo;
+        g.hi = ch ? t : g.hi;
+        g.hi_q = ch ? q : g.hi_q;
+        g.lo = cl ? t : g.lo;
+        g.lo_q = cl ? q : g.lo_q;
+        return;
+    }
     const float th = up ? t : __int_as_float(0x7f800000);
     const float tl = up ? __int_as_float(0xff800000) : t;
     const float nh = fminf(g.hi, th), nl = fmaxf(g.lo, tl);
@@ -330,6 +351,36 @@ __device__ __forceinline__ void clip_interval_kept(const Ray &R, const PlaneBuf 
     g.hi = g.s;
     g.hi_q = kEndSphere;
     int k = 0;
+#if PF_K6_POSTRACK
+    // track 2 + the kept position, mapped to 2 + the list index once at the end
+    // (the same binding plane: positions are increasing in list order)
+#if PF_K6_KEPT_UNROLL4
+    for (; k + 4 <= n; k += 4) {
+        const float4 E0 = B.E[k], E1 = B.E[k + 1], E2 = B.E[k + 2], E3 = B.E[k + 3];
+        clip_plane<kTrack>(R, E0, k + 2, g);
+        clip_plane<kTrack>(R, E1, k + 3, g);
+        clip_plane<kTrack>(R, E2, k + 4, g);
+        clip_plane<kTrack>(R, E3, k + 5, g);
+    }
+    if (k + 2 <= n) {
+        const float4 E0 = B.E[k], E1 = B.E[k + 1];
+        clip_plane<kTrack>(R, E0, k + 2, g);
+        clip_plane<kTrack>(R, E1, k + 3, g);
+        k += 2;
+    }
+#else
+    for (; k + 2 <= n; k += 2) {
+        const float4 E0 = B.E[k], E1 = B.E[k + 1];
+        clip_plane<kTrack>(R, E0, k + 2, g);
+        clip_plane<kTrack>(R, E1, k + 3, g);
+    }
+#endif
+    if (k < n) clip_plane<kTrack>(R, B.E[k], k + 2, g);
+    if (kTrack) {
+        if (g.hi_q >= 2) g.hi_q = (int)B.q[g.hi_q - 2] + 2;
+        if (g.lo_q >= 2) g.lo_q = (int)B.q[g.lo_q - 2] + 2;
+    }
+#else
     for (; k + 2 <= n; k += 2) {
         const float4 E0 = B.E[k], E1 = B.E[k + 1];
         const uint32_t qq = kTrack ? *reinterpret_cast<const uint16_t *>(B.q + k) : 0u;
@@ -337,6 +388,7 @@ __device__ __forceinline__ void clip_interval_kept(const Ray &R, const PlaneBuf 
         clip_plane<kTrack>(R, E1, (int)(qq >> 8) + 2, g);
     }
     if (k < n) clip_plane<kTrack>(R, B.E[k], kTrack ? (int)B.q[k] + 2 : 0, g);
+#endif
     if (kDipole) clip_plane<kTrack>(R, dplane, kEndDipole, g);
     const float dt = __fsub_rn(g.hi, g.lo);
     g.dt = (active && dt > 0.0f) ? dt : 0.0f;
